@@ -1,0 +1,122 @@
+/*
+ * flashinside.h -- C ABI of the B200-native FlashInside engine (sm_100a).
+ *
+ * This is the drop-in boundary for the reference's inside-algorithm engine
+ * API.  The reference is pure Python/NumPy; its plug-in seam is the engine
+ * registry ENGINES (pkg/src/flashpcfg/inside.py:343-348) whose entries have
+ * the signature  engine(g, tokens, meter=None) -> InsideChart
+ * (inside.py:150-151, :216-217, :274-275), plus the backward
+ * inside_backward(g, tokens, chart) -> (GrammarGrad, MarginalTable)
+ * (inside.py:375-376).  A ctypes binding calls the
+ * entry points below; the Python package paper_2310_14997_b200 does exactly
+ * that and re-exposes the reference's names.
+ *
+ * Conventions
+ *   - All pointers are DEVICE pointers on the current CUDA device unless the
+ *     name says otherwise; all arrays are C-contiguous fp32 / int32.
+ *   - Every call is stream-ordered on `stream` (a cudaStream_t, may be NULL)
+ *     and returns FI_OK or an error code; fi_last_error() gives the message
+ *     (thread-local).  No C++ exception crosses this boundary.
+ *   - The workspace `ws` (fi_workspace_bytes) is caller-allocated device
+ *     memory.  The forward leaves the chart in it; the backward consumes it.
+ *     The library never allocates or frees caller memory.
+ *
+ * Shapes (N = n_nt, P = n_pt, B = batch, l = max_len):
+ *   L, R      : (N, N+P)   log_left / log_right  (grammar.py:99-100)
+ *   root      : (N,)       log_root
+ *   unary     : (B, l, P)  unary[b, i, T] = log_emit[T, tokens[b][i]]
+ *                          (the width-1 chart row, inside.py:296-298)
+ *   lengths   : (B,)       2 <= lengths[b] <= l
+ *   log_z     : (B,)       per-sentence log partition (InsideChart.log_z)
+ *   grad_log_z: (B,)       upstream gradient dLoss/dlog_z
+ *   dL, dR    : (N, N+P)   sum_b grad_log_z[b] * dlog_z[b]/dL  (GrammarGrad)
+ *   droot     : (N,)
+ *   dunary    : (B, l, P)  gradient w.r.t. unary (d_emit = scatter of it,
+ *                          inside.py:420-423)
+ */
+#ifndef FLASHINSIDE_H_
+#define FLASHINSIDE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FI_OK 0
+#define FI_ERR_ARG 1         /* invalid shape / pointer (InsideError analogue) */
+#define FI_ERR_CUDA 2        /* CUDA runtime / driver failure                  */
+#define FI_ERR_UNSUPPORTED 3 /* no sm_100a device or unsupported size          */
+
+#define FI_GEMM_BF16 0 /* projection GEMM operands bf16, fp32 accumulate      */
+#define FI_GEMM_TF32 1 /* projection GEMM operands tf32 (single pass)           */
+#define FI_GEMM_FP32 2 /* "fp32 mode": bf16x3 split operands (hi*hi + lo*hi +
+                          hi*lo), ~2^-16 relative per product, fp32 accumulate */
+
+typedef struct fi_shape {
+  int32_t n_nt;        /* N */
+  int32_t n_pt;        /* P */
+  int32_t batch;       /* B */
+  int32_t max_len;     /* l */
+  int32_t gemm_dtype;  /* FI_GEMM_BF16 | FI_GEMM_TF32 | FI_GEMM_FP32 */
+  int32_t store_chart; /* 1: keep o[w] for every span (chart export, marginals) */
+} fi_shape;
+
+/* Byte offsets of the chart arrays inside the workspace, for chart export.
+ * Row r of an array with row stride `np` lives at offset + 4*r*np.
+ *   row(w, b, i) = rowbase(w) + b*(l-w+1) + i,
+ *   rowbase(w)   = B * ((w-1)*(l+1) - (w-1)*w/2). */
+typedef struct fi_chart_layout {
+  int64_t np;       /* padded N (row stride, floats)          */
+  int64_t pp;       /* padded P                               */
+  int64_t rows;     /* total span rows = rowbase(l) + B       */
+  int64_t off_a;    /* a[w]  fp32, widths 1..l-1              */
+  int64_t off_b;    /* b[w]  fp32, widths 1..l-1              */
+  int64_t off_o;    /* o[w]  fp32, widths 2..l (-1 if absent) */
+  int64_t off_x;    /* x†    fp32 per row                     */
+  int64_t off_lq;   /* log|go|-o, widths 2..l (after backward)*/
+  int64_t off_flag; /* int32 error flags (bit0: non-finite logZ in backward) */
+} fi_chart_layout;
+
+/* Workspace bytes needed for `shape` (0 on invalid shape). */
+size_t fi_workspace_bytes(const fi_shape* shape);
+
+/* Chart layout of the workspace for `shape`. */
+int fi_get_chart_layout(const fi_shape* shape, fi_chart_layout* out);
+
+/* Forward inside pass (replaces inside_flash, inside.py:274-340, batched).
+ * Writes log_z[B]; keeps the chart in ws for fi_inside_backward. */
+int fi_inside_forward(const fi_shape* shape, const float* L, const float* R, const float* root,
+                      const float* unary, const int32_t* lengths, float* log_z, void* ws,
+                      void* stream);
+
+/* Backward / outside pass (replaces inside_backward + _projection_backward,
+ * inside.py:375-447) by recomputation from the chart in ws. */
+int fi_inside_backward(const fi_shape* shape, const float* L, const float* R, const float* root,
+                       const float* unary, const int32_t* lengths, const float* log_z,
+                       const float* grad_log_z, float* dL, float* dR, float* droot,
+                       float* dunary, void* ws, void* stream);
+
+/* Span marginals mu_sym (MarginalTable, inside.py:425-430) for widths >= 2,
+ * rows ordered like the chart from rowbase(2); shape (rows - rowbase(2), N).
+ * Requires store_chart = 1 and a completed backward with the same grad_log_z. */
+int fi_marginals(const fi_shape* shape, const int32_t* lengths, const float* grad_log_z,
+                 float* mu, void* ws, void* stream);
+
+/* Test hook: C[M,N] = A * B^T in the engine's tcgen05 GEMM (fp32 out).
+ * a_mn / b_mn select MN-major operands: A is (M,K) K-major or (K,M) MN-major,
+ * B is (N,K) K-major or (K,N) MN-major; elements bf16 (dtype 0) or fp32/tf32. */
+int fi_test_gemm(int32_t dtype, int32_t a_mn, int32_t b_mn, int32_t M, int32_t N, int32_t K,
+                 const void* A, const void* B, float* C, void* stream);
+
+/* Number of kernels the last forward/backward call enqueued (for bench accounting). */
+int32_t fi_last_launch_count(void);
+
+const char* fi_last_error(void);
+int32_t fi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLASHINSIDE_H_ */

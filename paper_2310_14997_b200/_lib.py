@@ -1,0 +1,126 @@
+"""ctypes binding of the C ABI in include/flashinside.h.
+
+Loading fails loudly: there is no CPU fallback for the engine.  The
+signatures mirror the header one for one; this module is also the model for
+the reference-side binding shown in INTEGRATION.md.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from ctypes import POINTER, Structure, c_float, c_int32, c_int64, c_size_t, c_void_p, c_char_p
+
+from . import _build
+
+FI_OK = 0
+FI_ERR_ARG = 1
+FI_ERR_CUDA = 2
+FI_ERR_UNSUPPORTED = 3
+FI_GEMM_BF16 = 0
+FI_GEMM_TF32 = 1
+FI_GEMM_FP32 = 2
+
+GEMM_DTYPES = {"bf16": FI_GEMM_BF16, "tf32": FI_GEMM_TF32, "fp32": FI_GEMM_FP32}
+
+
+class FiShape(Structure):
+    _fields_ = [
+        ("n_nt", c_int32),
+        ("n_pt", c_int32),
+        ("batch", c_int32),
+        ("max_len", c_int32),
+        ("gemm_dtype", c_int32),
+        ("store_chart", c_int32),
+    ]
+
+
+class FiChartLayout(Structure):
+    _fields_ = [
+        ("np", c_int64),
+        ("pp", c_int64),
+        ("rows", c_int64),
+        ("off_a", c_int64),
+        ("off_b", c_int64),
+        ("off_o", c_int64),
+        ("off_x", c_int64),
+        ("off_lq", c_int64),
+        ("off_flag", c_int64),
+    ]
+
+
+# (name, restype, argtypes) exactly as declared in include/flashinside.h
+_PF = POINTER(c_float)
+SIGNATURES = [
+    ("fi_workspace_bytes", c_size_t, [POINTER(FiShape)]),
+    ("fi_get_chart_layout", c_int32, [POINTER(FiShape), POINTER(FiChartLayout)]),
+    ("fi_inside_forward", c_int32,
+     [POINTER(FiShape), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+      c_void_p]),
+    ("fi_inside_backward", c_int32,
+     [POINTER(FiShape), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+      c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("fi_marginals", c_int32,
+     [POINTER(FiShape), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("fi_test_gemm", c_int32,
+     [c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p,
+      c_void_p]),
+    ("fi_last_launch_count", c_int32, []),
+    ("fi_last_error", c_char_p, []),
+    ("fi_version", c_int32, []),
+]
+
+_LIB = None
+
+
+class EngineError(RuntimeError):
+    """A C-ABI call returned an error code."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"flashinside error {code}: {msg}")
+        self.code = code
+
+
+def load(build_if_missing: bool = True) -> ctypes.CDLL:
+    """Load (building first if needed) the engine library; raise if impossible."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if build_if_missing and _build.needs_build():
+        _build.build()
+    if not _build.LIB_PATH.exists():
+        raise RuntimeError(f"FlashInside engine library missing: {_build.LIB_PATH} "
+                           "(run __graft_entry__.build()); there is no CPU fallback")
+    lib = ctypes.CDLL(str(_build.LIB_PATH))
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _LIB = lib
+    return lib
+
+
+def check(code: int) -> None:
+    if code != FI_OK:
+        msg = load().fi_last_error()
+        raise EngineError(code, msg.decode() if msg else "")
+
+
+def shape(n_nt: int, n_pt: int, batch: int, max_len: int, gemm_dtype: str = "bf16",
+          store_chart: bool = False) -> FiShape:
+    if gemm_dtype not in GEMM_DTYPES:
+        raise ValueError(f"gemm_dtype must be one of {sorted(GEMM_DTYPES)}, got {gemm_dtype!r}")
+    return FiShape(int(n_nt), int(n_pt), int(batch), int(max_len), GEMM_DTYPES[gemm_dtype],
+                   1 if store_chart else 0)
+
+
+def workspace_bytes(s: FiShape) -> int:
+    n = load().fi_workspace_bytes(ctypes.byref(s))
+    if n == 0:
+        check(FI_ERR_ARG)
+    return int(n)
+
+
+def chart_layout(s: FiShape) -> FiChartLayout:
+    out = FiChartLayout()
+    check(load().fi_get_chart_layout(ctypes.byref(s), ctypes.byref(out)))
+    return out

@@ -1,0 +1,568 @@
+// C ABI of the FlashInside engine: workspace planning and the width sweeps
+// that sequence the sm_100a kernels (fi_kernels.cuh, fi_gemm.cuh).
+//
+// Forward  (inside_flash, inside.py:274-340, batched over sentences):
+//   K1 W = exp([L|R]) once per call            -> k_prep_weights
+//   width 1: x†, E1 = exp(unary - x†)          -> k_prep_width1
+//            [a1|b1] = x† + log(E1 W_NP^T)     -> tcgen05 GEMM, EPI_FWD
+//   w = 2..l: split contraction -> o, x†, E    -> k_split_fwd (cluster/DSMEM)
+//            [aw|bw] = x† + log(Ew W_NN^T)     -> tcgen05 GEMM, EPI_FWD
+// Backward (inside_backward + _projection_backward, inside.py:375-447):
+//   seed lq at each top span, d_root           -> k_seed_bwd
+//   m = l-1..1: G_m (gather split backward)    -> k_gather_bwd
+//            lq_m = log|G_m W| - x†            -> tcgen05 GEMM, EPI_DGRAD
+//            (m = 1: dunary = E1 * (G_1 W_NP)) -> tcgen05 GEMM, EPI_DUNARY
+//   dW = G^T E over all spans, d{L,R} = W*dW   -> tcgen05 GEMM, EPI_WGRAD
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <cudaTypedefs.h>
+
+#include "../../include/flashinside.h"
+#include "fi_gemm.cuh"
+#include "fi_kernels.cuh"
+
+using namespace fi;
+
+namespace {
+
+thread_local char g_err[512] = "";
+thread_local int g_launches = 0;
+
+int set_err(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+#define FI_CUDA(expr)                                                                   \
+  do {                                                                                  \
+    cudaError_t e_ = (expr);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return set_err(FI_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                     __FILE__, __LINE__);                                               \
+  } while (0)
+
+#define FI_TRY(expr)           \
+  do {                         \
+    int r_ = (expr);           \
+    if (r_ != FI_OK) return r_; \
+  } while (0)
+
+// ------------------------------------------------------------------ layout
+struct Plan {
+  int N, P, B, l, Np, Pp, esz, clusters, v, threads, cols_per_cta;
+  long long rows;
+  size_t wnn, wnp, e1, eall, gall, a, b, o, lq, x, top, flag, total;
+  // element offsets of the lo planes of the GEMM operands (fp32 mode only)
+  long long wnn_lo, wnp_lo, e1_lo, eall_lo, gall_lo;
+  bool store_o, tf32, split;
+};
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+int make_plan(const fi_shape* s, Plan* p) {
+  if (!s) return set_err(FI_ERR_ARG, "null shape");
+  if (s->n_nt < 1 || s->n_pt < 1 || s->batch < 1)
+    return set_err(FI_ERR_ARG, "n_nt, n_pt and batch must be >= 1 (got %d, %d, %d)", s->n_nt,
+                   s->n_pt, s->batch);
+  if (s->max_len < 2)
+    return set_err(FI_ERR_ARG, "need sentences of length >= 2, got max_len %d", s->max_len);
+  if (s->gemm_dtype != FI_GEMM_BF16 && s->gemm_dtype != FI_GEMM_TF32 &&
+      s->gemm_dtype != FI_GEMM_FP32)
+    return set_err(FI_ERR_ARG, "unknown gemm_dtype %d", s->gemm_dtype);
+  if (s->n_nt > 16384 || s->n_pt > 16384)
+    return set_err(FI_ERR_UNSUPPORTED, "symbol counts above 16384 are not supported");
+  p->N = s->n_nt;
+  p->P = s->n_pt;
+  p->B = s->batch;
+  p->l = s->max_len;
+  p->Np = p->N <= 1024 ? static_cast<int>(align_up(p->N, 256)) : static_cast<int>(align_up(p->N, 1024));
+  p->Pp = static_cast<int>(align_up(p->P, 256));
+  p->tf32 = s->gemm_dtype == FI_GEMM_TF32;
+  p->split = s->gemm_dtype == FI_GEMM_FP32;
+  p->esz = p->tf32 ? 4 : 2;
+  const int planes = p->split ? 2 : 1;
+  p->store_o = s->store_chart != 0;
+  if (p->Np <= 1024) {
+    p->clusters = 1;
+    p->threads = p->Np / 4;
+    p->v = 1;
+  } else {
+    p->threads = 256;
+    p->clusters = p->Np / 1024 < 8 ? p->Np / 1024 : 8;
+    p->v = p->Np / (p->clusters * 1024);
+  }
+  p->cols_per_cta = p->Np / p->clusters;
+  p->rows = rowbase(p->l, p->B, p->l) + p->B;
+  const long long rows = p->rows;
+  if (static_cast<long long>(p->B) * p->l > 65535 || rows > (1LL << 30))
+    return set_err(FI_ERR_UNSUPPORTED, "batch x length above 65535 spans per width");
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + bytes, 1024);
+    return o;
+  };
+  auto plane = [&](long long elems, long long* lo) {
+    *lo = p->split ? elems : 0;
+    return take(static_cast<size_t>(elems) * p->esz * planes);
+  };
+  p->wnn = plane(2LL * p->Np * p->Np, &p->wnn_lo);
+  p->wnp = plane(2LL * p->Np * p->Pp, &p->wnp_lo);
+  p->e1 = plane(1LL * p->B * p->l * p->Pp, &p->e1_lo);
+  p->eall = plane(rows * p->Np, &p->eall_lo);
+  p->gall = plane(2LL * rows * p->Np, &p->gall_lo);
+  p->a = take(4ull * rows * p->Np);
+  p->b = take(4ull * rows * p->Np);
+  p->o = p->store_o ? take(4ull * rows * p->Np) : static_cast<size_t>(-1);
+  p->lq = take(4ull * rows * p->Np);
+  p->x = take(4ull * rows);
+  p->top = take(4ull * p->B * p->Np);
+  p->flag = take(256);
+  p->total = off;
+  return FI_OK;
+}
+
+template <typename P>
+P* at(void* ws, size_t off) {
+  return reinterpret_cast<P*>(static_cast<uint8_t*>(ws) + off);
+}
+
+// ------------------------------------------------------------ TMA descriptors
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+int load_encode() {
+  if (g_encode) return FI_OK;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+    return set_err(FI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return FI_OK;
+}
+
+struct Operand {
+  const void* ptr;
+  long long inner;  // contiguous extent (elements)
+  long long outer;  // rows
+  long long ld;     // row stride (elements)
+  bool mn_major;
+  long long lo;     // element offset of the lo plane (fp32 mode), else 0
+};
+
+template <typename T>
+int encode(CUtensorMap* m, const Operand& op, int box_inner, int box_outer) {
+  // tf32 MN-major tiles must land in the 32B-atom swizzle the UMMA expects
+  const CUtensorMapSwizzle sw = (sizeof(T) == 4 && op.mn_major)
+                                    ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                                    : CU_TENSOR_MAP_SWIZZLE_128B;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(op.inner), static_cast<cuuint64_t>(op.outer)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(op.ld * sizeof(T))};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer)};
+  cuuint32_t estr[2] = {1, 1};
+  CUtensorMapDataType dt =
+      sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  CUresult r = g_encode(m, dt, 2, const_cast<void*>(op.ptr), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_err(FI_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d): inner=%lld outer=%lld",
+                   static_cast<int>(r), op.inner, op.outer);
+  return FI_OK;
+}
+
+int num_sms() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cached[dev]) cudaDeviceGetAttribute(&cached[dev], cudaDevAttrMultiProcessorCount, dev);
+  return cached[dev] > 0 ? cached[dev] : 148;
+}
+
+template <typename T, int BN, bool AMN, bool BMN, int EPI, bool SPLIT>
+int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_row0,
+                const GemmEpi& ep, cudaStream_t st) {
+  using Cf = GemmCfg<T, BN>;
+  CUtensorMap ta, tb, ta2, tb2;
+  const int abi = AMN ? Cf::ATOM : Cf::BK, abo = AMN ? Cf::BK : Cf::BM;
+  const int bbi = BMN ? Cf::ATOM : Cf::BK, bbo = BMN ? Cf::BK : BN;
+  FI_TRY(encode<T>(&ta, A, abi, abo));
+  FI_TRY(encode<T>(&tb, B, bbi, bbo));
+  if (SPLIT) {
+    Operand a2 = A, b2 = B;
+    a2.ptr = static_cast<const T*>(A.ptr) + A.lo;
+    b2.ptr = static_cast<const T*>(B.ptr) + B.lo;
+    FI_TRY(encode<T>(&ta2, a2, abi, abo));
+    FI_TRY(encode<T>(&tb2, b2, bbi, bbo));
+  } else {
+    ta2 = ta;
+    tb2 = tb;
+  }
+  GemmShape sh;
+  sh.M = M;
+  sh.N = N;
+  sh.K = K;
+  sh.a_row0 = a_row0;
+  sh.num_m = (M + Cf::BM - 1) / Cf::BM;
+  sh.num_n = N / BN;
+  sh.num_k = (K + Cf::BK - 1) / Cf::BK;
+  auto kern = k_gemm<T, BN, AMN, BMN, EPI, SPLIT>;
+  static bool attr_done[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr_done[dev & 63]) {
+    FI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Cf::SMEM_BYTES));
+    attr_done[dev & 63] = true;
+  }
+  const int tiles = sh.num_m * sh.num_n;
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  if (grid <= 0) return FI_OK;
+  kern<<<grid, 256, Cf::SMEM_BYTES, st>>>(ta, tb, ta2, tb2, sh, ep);
+  ++g_launches;
+  FI_CUDA(cudaGetLastError());
+  return FI_OK;
+}
+
+// Pick the widest N tile that still gives one tile per SM (small-M widths).
+template <typename T, bool AMN, bool BMN, int EPI, bool SPLIT>
+int run_gemm_s(const Operand& A, const Operand& B, int M, int N, int K, int a_row0,
+               const GemmEpi& ep, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return FI_OK;
+  const long long mt = (M + 127) / 128;
+  const int sms = num_sms();
+  if (N % 256 == 0 && mt * (N / 256) >= sms)
+    return launch_gemm<T, 256, AMN, BMN, EPI, SPLIT>(A, B, M, N, K, a_row0, ep, st);
+  if (N % 128 == 0 && mt * (N / 128) >= sms)
+    return launch_gemm<T, 128, AMN, BMN, EPI, SPLIT>(A, B, M, N, K, a_row0, ep, st);
+  if (N % 64 == 0) return launch_gemm<T, 64, AMN, BMN, EPI, SPLIT>(A, B, M, N, K, a_row0, ep, st);
+  return set_err(FI_ERR_ARG, "GEMM N=%d must be a multiple of 64", N);
+}
+
+// Dispatch on the split (fp32 / bf16x3) mode; tf32 operands are never split.
+template <typename T, bool AMN, bool BMN, int EPI>
+int run_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_row0,
+             const GemmEpi& ep, cudaStream_t st) {
+  if constexpr (sizeof(T) == 2) {
+    if (A.lo || B.lo) return run_gemm_s<T, AMN, BMN, EPI, true>(A, B, M, N, K, a_row0, ep, st);
+  }
+  return run_gemm_s<T, AMN, BMN, EPI, false>(A, B, M, N, K, a_row0, ep, st);
+}
+
+template <typename K, typename... Args>
+int launch_cluster(K kern, int cluster, dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  FI_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+  ++g_launches;
+  return FI_OK;
+}
+
+int check_ptrs(std::initializer_list<const void*> ps) {
+  for (const void* p : ps)
+    if (!p) return set_err(FI_ERR_ARG, "null pointer argument");
+  return FI_OK;
+}
+
+// ------------------------------------------------------------------ forward
+template <typename T>
+int forward_impl(const Plan& p, const float* L, const float* R, const float* root,
+                 const float* unary, const int* lengths, float* logZ, void* ws,
+                 cudaStream_t st) {
+  T* wnn = at<T>(ws, p.wnn);
+  T* wnp = at<T>(ws, p.wnp);
+  T* e1 = at<T>(ws, p.e1);
+  T* eall = at<T>(ws, p.eall);
+  float* A = at<float>(ws, p.a);
+  float* Bc = at<float>(ws, p.b);
+  float* O = p.store_o ? at<float>(ws, p.o) : nullptr;
+  float* X = at<float>(ws, p.x);
+  float* TOP = at<float>(ws, p.top);
+
+  {  // K1: exp of the child tables, once per call
+    dim3 grid((p.Np + p.Pp + 255) / 256, 2 * p.Np);
+    k_prep_weights<T><<<grid, 256, 0, st>>>(L, R, wnn, wnp, p.N, p.P, p.Np, p.Pp, p.wnn_lo,
+                                            p.wnp_lo);
+    ++g_launches;
+    FI_CUDA(cudaGetLastError());
+  }
+  k_prep_width1<T><<<p.B * p.l, 256, 0, st>>>(unary, lengths, e1, X, p.l, p.P, p.Pp, p.e1_lo);
+  ++g_launches;
+  FI_CUDA(cudaGetLastError());
+
+  const Operand opWnn{wnn, p.Np, 2LL * p.Np, p.Np, false, p.wnn_lo};
+  const Operand opWnp{wnp, p.Pp, 2LL * p.Np, p.Pp, false, p.wnp_lo};
+  const Operand opE1{e1, p.Pp, static_cast<long long>(p.B) * p.l, p.Pp, false, p.e1_lo};
+  const Operand opEall{eall, p.Np, p.rows, p.Np, false, p.eall_lo};
+
+  GemmEpi ep = {};
+  ep.X = X;
+  ep.outA = A;
+  ep.outB = Bc;
+  ep.Np = p.Np;
+  ep.M = p.B * p.l;
+  ep.row0 = 0;
+  FI_TRY((run_gemm<T, false, false, EPI_FWD>(opE1, opWnp, ep.M, 2 * p.Np, p.Pp, 0, ep, st)));
+
+  for (int w = 2; w <= p.l; ++w) {
+    const int n_w = p.l - w + 1;
+    SplitArgs sa;
+    sa.A = A;
+    sa.Bc = Bc;
+    sa.O = O;
+    sa.E = w < p.l ? static_cast<void*>(eall) : nullptr;
+    sa.e_lo = p.eall_lo;
+    sa.X = X;
+    sa.TOP = TOP;
+    sa.logZ = logZ;
+    sa.root = root;
+    sa.lengths = lengths;
+    sa.B = p.B;
+    sa.lmax = p.l;
+    sa.N = p.N;
+    sa.Np = p.Np;
+    sa.w = w;
+    sa.cols_per_cta = p.cols_per_cta;
+    const dim3 grid(p.clusters, p.B * n_w);
+    if (p.v == 1)
+      FI_TRY(launch_cluster(k_split_fwd<T, 1>, p.clusters, grid, dim3(p.threads), st, sa));
+    else
+      FI_TRY(launch_cluster(k_split_fwd<T, 2>, p.clusters, grid, dim3(p.threads), st, sa));
+    if (w < p.l) {
+      ep.M = p.B * n_w;
+      ep.row0 = rowbase(w, p.B, p.l);
+      FI_TRY((run_gemm<T, false, false, EPI_FWD>(opEall, opWnn, ep.M, 2 * p.Np, p.Np,
+                                                  static_cast<int>(ep.row0), ep, st)));
+    }
+  }
+  return FI_OK;
+}
+
+// ----------------------------------------------------------------- backward
+template <typename T>
+int backward_impl(const Plan& p, const float* L, const float* R, const float* root,
+                  const float* unary, const int* lengths, const float* logZ, const float* g,
+                  float* dL, float* dR, float* droot, float* dunary, void* ws, cudaStream_t st) {
+  T* wnn = at<T>(ws, p.wnn);
+  T* wnp = at<T>(ws, p.wnp);
+  T* e1 = at<T>(ws, p.e1);
+  T* eall = at<T>(ws, p.eall);
+  T* gall = at<T>(ws, p.gall);
+  float* A = at<float>(ws, p.a);
+  float* Bc = at<float>(ws, p.b);
+  float* LQ = at<float>(ws, p.lq);
+  float* X = at<float>(ws, p.x);
+  float* TOP = at<float>(ws, p.top);
+  int* flag = at<int>(ws, p.flag);
+
+  FI_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+  k_seed_bwd<<<(p.Np + 255) / 256, 256, 0, st>>>(root, TOP, logZ, g, lengths, LQ, droot, flag,
+                                                 p.B, p.l, p.N, p.Np);
+  ++g_launches;
+  FI_CUDA(cudaGetLastError());
+
+  const Operand opWnnMN{wnn, p.Np, 2LL * p.Np, p.Np, true, p.wnn_lo};  // K = 2Np, N = Np
+  const Operand opWnpMN{wnp, p.Pp, 2LL * p.Np, p.Pp, true, p.wnp_lo};
+  const Operand opGall{gall, 2LL * p.Np, p.rows, 2LL * p.Np, false, p.gall_lo};
+
+  for (int m = p.l - 1; m >= 1; --m) {
+    const int n_m = p.l - m + 1;
+    GatherArgs ga;
+    ga.A = A;
+    ga.Bc = Bc;
+    ga.LQ = LQ;
+    ga.X = X;
+    ga.G = gall;
+    ga.g_lo = p.gall_lo;
+    ga.lengths = lengths;
+    ga.g = g;
+    ga.B = p.B;
+    ga.lmax = p.l;
+    ga.Np = p.Np;
+    ga.m = m;
+    ga.cols_per_cta = p.cols_per_cta;
+    const dim3 grid(p.clusters, p.B * n_m);
+    if (p.v == 1)
+      k_gather_bwd<T, 1><<<grid, p.threads, 0, st>>>(ga);
+    else
+      k_gather_bwd<T, 2><<<grid, p.threads, 0, st>>>(ga);
+    ++g_launches;
+    FI_CUDA(cudaGetLastError());
+
+    GemmEpi ep = {};
+    ep.X = X;
+    ep.Np = p.Np;
+    ep.M = p.B * n_m;
+    ep.row0 = rowbase(m, p.B, p.l);
+    ep.lengths = lengths;
+    ep.width = m;
+    ep.n_w = n_m;
+    if (m >= 2) {
+      ep.LQ = LQ;
+      FI_TRY((run_gemm<T, false, true, EPI_DGRAD>(opGall, opWnnMN, ep.M, p.Np, 2 * p.Np,
+                                                   static_cast<int>(ep.row0), ep, st)));
+    } else {
+      ep.dunary = dunary;
+      ep.unary = unary;
+      ep.P = p.P;
+      ep.lmax = p.l;
+      FI_TRY((run_gemm<T, false, true, EPI_DUNARY>(opGall, opWnpMN, ep.M, p.Pp, 2 * p.Np, 0, ep,
+                                                    st)));
+    }
+  }
+
+  // weight gradients: dW = G^T E summed over every span, then * exp(table)
+  GemmEpi ep = {};
+  ep.Lsrc = L;
+  ep.Rsrc = R;
+  ep.dL = dL;
+  ep.dR = dR;
+  ep.n_nt = p.N;
+  ep.ld_lr = p.N + p.P;
+  ep.Np = p.Np;
+  ep.M = 2 * p.Np;
+  const long long r2 = rowbase(2, p.B, p.l), rl = rowbase(p.l, p.B, p.l);
+  if (rl > r2) {
+    const Operand opG{gall + r2 * 2 * p.Np, 2LL * p.Np, rl - r2, 2LL * p.Np, true, p.gall_lo};
+    const Operand opE{eall + r2 * p.Np, p.Np, rl - r2, p.Np, true, p.eall_lo};
+    ep.col_off = 0;
+    ep.valid_cols = p.N;
+    FI_TRY((run_gemm<T, true, true, EPI_WGRAD>(opG, opE, 2 * p.Np, p.Np,
+                                                static_cast<int>(rl - r2), 0, ep, st)));
+  } else {  // l == 2: no width >= 2 span is ever projected
+    for (int r = 0; r < p.N; ++r) {
+      FI_CUDA(cudaMemsetAsync(dL + static_cast<long long>(r) * (p.N + p.P), 0, 4ull * p.N, st));
+      FI_CUDA(cudaMemsetAsync(dR + static_cast<long long>(r) * (p.N + p.P), 0, 4ull * p.N, st));
+    }
+  }
+  {
+    const Operand opG{gall, 2LL * p.Np, static_cast<long long>(p.B) * p.l, 2LL * p.Np, true,
+                      p.gall_lo};
+    const Operand opE{e1, p.Pp, static_cast<long long>(p.B) * p.l, p.Pp, true, p.e1_lo};
+    ep.col_off = p.N;
+    ep.valid_cols = p.P;
+    FI_TRY((run_gemm<T, true, true, EPI_WGRAD>(opG, opE, 2 * p.Np, p.Pp, p.B * p.l, 0, ep, st)));
+  }
+  return FI_OK;
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+size_t fi_workspace_bytes(const fi_shape* shape) {
+  Plan p;
+  if (make_plan(shape, &p) != FI_OK) return 0;
+  return p.total;
+}
+
+int fi_get_chart_layout(const fi_shape* shape, fi_chart_layout* out) {
+  Plan p;
+  FI_TRY(make_plan(shape, &p));
+  if (!out) return set_err(FI_ERR_ARG, "null layout");
+  out->np = p.Np;
+  out->pp = p.Pp;
+  out->rows = p.rows;
+  out->off_a = static_cast<int64_t>(p.a);
+  out->off_b = static_cast<int64_t>(p.b);
+  out->off_o = p.store_o ? static_cast<int64_t>(p.o) : -1;
+  out->off_x = static_cast<int64_t>(p.x);
+  out->off_lq = static_cast<int64_t>(p.lq);
+  out->off_flag = static_cast<int64_t>(p.flag);
+  return FI_OK;
+}
+
+int fi_inside_forward(const fi_shape* shape, const float* L, const float* R, const float* root,
+                      const float* unary, const int32_t* lengths, float* log_z, void* ws,
+                      void* stream) {
+  g_launches = 0;
+  Plan p;
+  FI_TRY(make_plan(shape, &p));
+  FI_TRY(check_ptrs({L, R, root, unary, lengths, log_z, ws}));
+  FI_TRY(load_encode());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (p.tf32) return forward_impl<float>(p, L, R, root, unary, lengths, log_z, ws, st);
+  return forward_impl<__nv_bfloat16>(p, L, R, root, unary, lengths, log_z, ws, st);
+}
+
+int fi_inside_backward(const fi_shape* shape, const float* L, const float* R, const float* root,
+                       const float* unary, const int32_t* lengths, const float* log_z,
+                       const float* grad_log_z, float* dL, float* dR, float* droot,
+                       float* dunary, void* ws, void* stream) {
+  g_launches = 0;
+  Plan p;
+  FI_TRY(make_plan(shape, &p));
+  FI_TRY(check_ptrs({L, R, root, unary, lengths, log_z, grad_log_z, dL, dR, droot, dunary, ws}));
+  FI_TRY(load_encode());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (p.tf32)
+    return backward_impl<float>(p, L, R, root, unary, lengths, log_z, grad_log_z, dL, dR, droot,
+                                dunary, ws, st);
+  return backward_impl<__nv_bfloat16>(p, L, R, root, unary, lengths, log_z, grad_log_z, dL, dR,
+                                      droot, dunary, ws, st);
+}
+
+int fi_marginals(const fi_shape* shape, const int32_t* lengths, const float* grad_log_z,
+                 float* mu, void* ws, void* stream) {
+  Plan p;
+  FI_TRY(make_plan(shape, &p));
+  FI_TRY(check_ptrs({lengths, grad_log_z, mu, ws}));
+  if (!p.store_o) return set_err(FI_ERR_ARG, "marginals need store_chart = 1");
+  const long long nrows = p.rows - rowbase(2, p.B, p.l);
+  if (nrows <= 0) return FI_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  k_marginals<<<static_cast<unsigned>(nrows), 256, 0, st>>>(
+      at<float>(ws, p.lq), at<float>(ws, p.o), grad_log_z, lengths, mu, p.B, p.l, p.Np, p.N);
+  FI_CUDA(cudaGetLastError());
+  return FI_OK;
+}
+
+int fi_test_gemm(int32_t dtype, int32_t a_mn, int32_t b_mn, int32_t M, int32_t N, int32_t K,
+                 const void* A, const void* B, float* C, void* stream) {
+  FI_TRY(check_ptrs({A, B, C}));
+  FI_TRY(load_encode());
+  if (M < 1 || N < 64 || N % 64 || K < 1)
+    return set_err(FI_ERR_ARG, "test GEMM needs M>=1, N%%64==0, K>=1");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  GemmEpi ep = {};
+  ep.M = M;
+  ep.C = C;
+  ep.ldc = N;
+  const Operand opA = a_mn ? Operand{A, M, K, M, true, 0} : Operand{A, K, M, K, false, 0};
+  const Operand opB = b_mn ? Operand{B, N, K, N, true, 0} : Operand{B, K, N, K, false, 0};
+#define FI_GEMM_CASE(T, AMN, BMN) \
+  if (!!a_mn == AMN && !!b_mn == BMN) return run_gemm<T, AMN, BMN, EPI_STORE>(opA, opB, M, N, K, 0, ep, st);
+  if (dtype == FI_GEMM_TF32) {
+    FI_GEMM_CASE(float, false, false)
+    FI_GEMM_CASE(float, false, true)
+    FI_GEMM_CASE(float, true, true)
+  } else {
+    FI_GEMM_CASE(__nv_bfloat16, false, false)
+    FI_GEMM_CASE(__nv_bfloat16, false, true)
+    FI_GEMM_CASE(__nv_bfloat16, true, true)
+  }
+#undef FI_GEMM_CASE
+  return set_err(FI_ERR_ARG, "unsupported majorness combination (A MN-major needs B MN-major)");
+}
+
+int32_t fi_last_launch_count(void) { return g_launches; }
+const char* fi_last_error(void) { return g_err; }
+int32_t fi_version(void) { return 1; }
+
+}  // extern "C"

@@ -1,0 +1,346 @@
+// Persistent, warp-specialised tcgen05 GEMM for sm_100a with fused
+// FlashInside epilogues.
+//
+//   C[M, N] = A[M, K] * B[N, K]^T        (fp32 accumulate in TMEM)
+//
+// A and B are staged by TMA into 128B-swizzled shared memory; either operand
+// may be K-major (rows of K contiguous) or MN-major (rows of MN contiguous,
+// i.e. the K index is the outer, strided dimension).  One elected thread
+// issues tcgen05.mma (M=128, N=BN, K=16 for bf16 / 8 for tf32) into one of
+// two TMEM accumulators, so the epilogue of tile t overlaps the main loop of
+// tile t+1.  The epilogue reads TMEM with tcgen05.ld and applies one of the
+// inside-algorithm transforms (see EpiMode) before writing fp32 to HBM.
+//
+// Warp roles (256 threads): w0 = TMA producer, w1 = MMA issuer,
+// w2 = TMEM allocator, w4..w7 = epilogue (TMEM lane quadrant = warp % 4).
+#pragma once
+#include "fi_ptx.cuh"
+
+namespace fi {
+
+enum EpiMode : int {
+  EPI_FWD = 0,     // [a | b] = x + log(acc)                      (inside.py:203-213)
+  EPI_DGRAD = 1,   // lq = log|acc| - x  (= log|go| - o)           (inside.py:433-447)
+  EPI_DUNARY = 2,  // dunary = acc * exp(unary - x)  (width-1 go)  (inside.py:420-423)
+  EPI_WGRAD = 3,   // d{L,R} = exp({L,R}) * acc                    (inside.py:446)
+  EPI_STORE = 4,   // plain C = acc (GEMM unit tests)
+};
+
+struct GemmShape {
+  int M, N, K;    // logical problem; rows >= M are masked in the epilogue
+  int a_row0;     // K-major A: first row coordinate inside the tensor map
+  int num_m, num_n, num_k;
+};
+
+struct GemmEpi {
+  int M;              // valid output rows
+  long long row0;     // global chart row of output row 0 (X / chart indexing)
+  const float* X;     // per-row log shift x† (indexed by global row)
+  // EPI_FWD
+  float* outA;
+  float* outB;
+  int Np;             // padded nonterminal count == row stride of chart arrays
+  // EPI_DGRAD
+  float* LQ;
+  const int* lengths;
+  int width;
+  int n_w;
+  // EPI_DUNARY
+  float* dunary;
+  const float* unary;
+  int P;
+  int lmax;
+  // EPI_WGRAD
+  const float* Lsrc;
+  const float* Rsrc;
+  float* dL;
+  float* dR;
+  int n_nt;
+  int ld_lr;          // row stride of L/R/dL/dR (= N + P)
+  int col_off;        // 0 for the NN block, N for the NP block
+  int valid_cols;     // N or P
+  // EPI_STORE
+  float* C;
+  int ldc;
+};
+
+template <typename T, int BN>
+struct GemmCfg {
+  static constexpr int BM = 128;
+  static constexpr int kElt = static_cast<int>(sizeof(T));
+  static constexpr int BK = 128 / kElt;            // one 128-B swizzle row of K
+  static constexpr int UK = 32 / kElt;             // K per tcgen05.mma
+  static constexpr int ATOM = 128 / kElt;          // MN elements per 128-B atom
+  static constexpr int A_BYTES = BM * 128;
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (200 * 1024 / STAGE_BYTES) > 8 ? 8 : (200 * 1024 / STAGE_BYTES);
+  static constexpr int TMEM_COLS = 2 * BN;         // double-buffered accumulator
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr bool TF32 = (kElt == 4);
+};
+
+// Row-wise epilogue for one 32-column chunk of one accumulator row.
+template <int EPI>
+__device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int lrow, long long grow, int col,
+                                          const float (&v)[32], float xv, bool row_ok,
+                                          float* rowptr, int aux) {
+  if (!row_ok) return;
+  if constexpr (EPI == EPI_FWD) {
+    float4* dst = reinterpret_cast<float4*>(rowptr + col);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float4 o;
+      o.x = xv + __logf(v[4 * q + 0]);
+      o.y = xv + __logf(v[4 * q + 1]);
+      o.z = xv + __logf(v[4 * q + 2]);
+      o.w = xv + __logf(v[4 * q + 3]);
+      dst[q] = o;
+    }
+  } else if constexpr (EPI == EPI_DGRAD) {
+    float4* dst = reinterpret_cast<float4*>(rowptr + col);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float4 o;
+      o.x = __logf(fabsf(v[4 * q + 0])) - xv;
+      o.y = __logf(fabsf(v[4 * q + 1])) - xv;
+      o.z = __logf(fabsf(v[4 * q + 2])) - xv;
+      o.w = __logf(fabsf(v[4 * q + 3])) - xv;
+      dst[q] = o;
+    }
+  } else if constexpr (EPI == EPI_DUNARY) {
+    // rowptr = dunary row, aux = 1 if the token position is inside the sentence
+    const float* un = ep.unary + static_cast<long long>(lrow) * ep.P;
+#pragma unroll 8
+    for (int t = 0; t < 32; ++t) {
+      int c = col + t;
+      if (c < ep.P) rowptr[c] = aux ? v[t] * __expf(un[c] - xv) : 0.f;
+    }
+  } else if constexpr (EPI == EPI_WGRAD) {
+    // rowptr = d{L,R} row start; aux selects the right table; lrow = table row
+#pragma unroll 8
+    for (int t = 0; t < 32; ++t) {
+      int c = col + t;
+      if (c < ep.valid_cols) {
+        long long off = static_cast<long long>(ep.col_off + c);
+        const float* lr = (aux ? ep.Rsrc : ep.Lsrc) + static_cast<long long>(lrow) * ep.ld_lr;
+        rowptr[off] = expf(lr[off]) * v[t];
+      }
+    }
+  } else {  // EPI_STORE
+#pragma unroll
+    for (int t = 0; t < 32; ++t) rowptr[col + t] = v[t];
+  }
+}
+
+// SPLIT (fp32 mode, bf16x3): each operand is stored as hi + lo bf16 planes
+// (x = hi + lo to ~2^-17 relative) and the K loop runs three passes,
+// hi*hi + lo*hi + hi*lo, accumulating into the same TMEM tile.
+template <typename T, int BN, bool A_MN, bool B_MN, int EPI, bool SPLIT>
+__global__ void __launch_bounds__(256, 1)
+    k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+           const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
+           GemmShape sh, GemmEpi ep) {
+  using C = GemmCfg<T, BN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smB + C::STAGES * C::B_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_tiles = sh.num_m * sh.num_n;
+  const int k_iters = SPLIT ? 3 * sh.num_k : sh.num_k;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    if constexpr (SPLIT) {
+      tma_prefetch_desc(&tmA2);
+      tma_prefetch_desc(&tmB2);
+    }
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<C::TMEM_COLS>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m_blk = tile % sh.num_m;
+        const int n_blk = tile / sh.num_m;
+        for (int it = 0; it < k_iters; ++it) {
+          const int pass = SPLIT ? it / sh.num_k : 0;
+          const int kb = SPLIT ? it - pass * sh.num_k : it;
+          const CUtensorMap* ma = (SPLIT && pass == 1) ? &tmA2 : &tmA;
+          const CUtensorMap* mb = (SPLIT && pass == 2) ? &tmB2 : &tmB;
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+          uint8_t* a_dst = smA + stage * C::A_BYTES;
+          uint8_t* b_dst = smB + stage * C::B_BYTES;
+          if constexpr (!A_MN) {
+            tma_load_2d(a_dst, ma, &full[stage], kb * C::BK, sh.a_row0 + m_blk * C::BM);
+          } else {
+#pragma unroll
+            for (int j = 0; j < C::BM / C::ATOM; ++j)
+              tma_load_2d(a_dst + j * C::BK * 128, ma, &full[stage], m_blk * C::BM + j * C::ATOM,
+                          kb * C::BK);
+          }
+          if constexpr (!B_MN) {
+            tma_load_2d(b_dst, mb, &full[stage], kb * C::BK, n_blk * BN);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / C::ATOM; ++j)
+              tma_load_2d(b_dst + j * C::BK * 128, mb, &full[stage], n_blk * BN + j * C::ATOM,
+                          kb * C::BK);
+          }
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc = make_idesc<C::TF32>(BN, A_MN, B_MN);
+      constexpr uint32_t a_lbo = A_MN ? C::BK * 128 : 16;
+      constexpr uint32_t b_lbo = B_MN ? C::BK * 128 : 16;
+      // tf32 MN-major operands use the 32B-atom 128B swizzle (4-row groups)
+      constexpr uint32_t a_lay = (A_MN && C::TF32) ? kLayoutSW128Base32B : kLayoutSW128;
+      constexpr uint32_t b_lay = (B_MN && C::TF32) ? kLayoutSW128Base32B : kLayoutSW128;
+      constexpr uint32_t a_sbo = (A_MN && C::TF32) ? 512 : 1024;
+      constexpr uint32_t b_sbo = (B_MN && C::TF32) ? 512 : 1024;
+      constexpr uint32_t a_kstep = A_MN ? C::UK * 128 : C::UK * C::kElt;
+      constexpr uint32_t b_kstep = B_MN ? C::UK * 128 : C::UK * C::kElt;
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+        for (int kb = 0; kb < k_iters; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(smA + stage * C::A_BYTES);
+          const uint32_t b_base = smem_u32(smB + stage * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < C::BK / C::UK; ++k) {
+            uint64_t ad = make_sdesc(a_base + k * a_kstep, a_lbo, a_sbo, a_lay);
+            uint64_t bd = make_sdesc(b_base + k * b_kstep, b_lbo, b_sbo, b_lay);
+            umma<C::TF32>(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // -------------------------------------------------- epilogue
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;  // accumulator row (TMEM lane)
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int m_blk = tile % sh.num_m;
+      const int n_blk = tile / sh.num_m;
+      const int lrow = m_blk * C::BM + r;  // row within this GEMM
+      const long long grow = ep.row0 + lrow;
+      const bool row_ok = lrow < ep.M;
+      float xv = 0.f;
+      float* rowptr = nullptr;
+      int aux = 0;
+      int col_base = n_blk * BN;
+      if (row_ok) {
+        if constexpr (EPI == EPI_FWD) {
+          xv = ep.X[grow];
+          if (col_base < ep.Np) {
+            rowptr = ep.outA + grow * ep.Np;
+          } else {
+            rowptr = ep.outB + grow * ep.Np;
+            col_base -= ep.Np;
+          }
+        } else if constexpr (EPI == EPI_DGRAD) {
+          xv = ep.X[grow];
+          rowptr = ep.LQ + grow * ep.Np;
+        } else if constexpr (EPI == EPI_DUNARY) {
+          xv = ep.X[grow];
+          const int b = lrow / ep.lmax, i = lrow % ep.lmax;
+          aux = i < ep.lengths[b];
+          rowptr = ep.dunary + static_cast<long long>(lrow) * ep.P;
+        } else if constexpr (EPI == EPI_WGRAD) {
+          aux = lrow >= ep.Np;  // 0 -> left table, 1 -> right table
+          const int arow = aux ? lrow - ep.Np : lrow;
+          rowptr = (aux ? ep.dR : ep.dL) + static_cast<long long>(arow) * ep.ld_lr;
+          if (arow >= ep.n_nt) rowptr = nullptr;
+        } else {
+          rowptr = ep.C + static_cast<long long>(lrow) * ep.ldc;
+        }
+      }
+      bool ok = row_ok && rowptr != nullptr;
+      if constexpr (EPI == EPI_DGRAD) {
+        // the seed kernel owns the top span of each sentence (inside.py:400-404)
+        if (ok) {
+          const int b = lrow / ep.n_w, i = lrow % ep.n_w;
+          if (i == 0 && ep.lengths[b] == ep.width) ok = false;
+        }
+      }
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
+                             static_cast<uint32_t>(acc * BN);
+#pragma unroll 1
+      for (int j = 0; j < BN / 32; ++j) {
+        float v[32];
+        tmem_ld32(t_row + j * 32, v);
+        if constexpr (EPI == EPI_WGRAD) {
+          const int arow = aux ? lrow - ep.Np : lrow;
+          epi_chunk<EPI>(ep, arow, grow, col_base + j * 32, v, xv, ok, rowptr, aux);
+        } else {
+          epi_chunk<EPI>(ep, lrow, grow, col_base + j * 32, v, xv, ok, rowptr, aux);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tmem_base);
+}
+
+}  // namespace fi

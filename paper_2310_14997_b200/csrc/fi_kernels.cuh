@@ -1,0 +1,534 @@
+// Bandwidth-bound FlashInside kernels for sm_100a: weight exponentiation,
+// width-1 preparation, the split-point contraction (forward), the seed of
+// the outside pass, and the gather-form split backward.
+//
+// Chart layout in HBM (all fp32 unless noted), one row per span:
+//   n_w        = lmax - w + 1                    spans of width w per sentence
+//   rowbase(w) = B * sum_{v<w} n_v               first row of width w
+//   row(w,b,i) = rowbase(w) + b * n_w + i        span (i, i+w) of sentence b
+// Every chart array has row stride Np (nonterminals padded to a multiple of
+// 256 with -inf / zero-probability dummy symbols).  The arrays are
+//   A, Bc  : left/right projections a[w], b[w]            (inside.py:66-84)
+//   O      : inside scores o[w] over nonterminals (optional; parity/marginals)
+//   X      : per-span shift x† = max_s o[w][i, s]          (inside.py:205-206)
+//   E      : exp(o - x†) in the GEMM operand type (bf16 or tf32)
+//   LQ     : log|go| - o, the outside weight in log space (backward only)
+//   G      : [ga·exp(x†-a) | gb·exp(x†-b)] per span, 2*Np wide (backward)
+#pragma once
+#include <cooperative_groups.h>
+#include "fi_ptx.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace fi {
+
+constexpr float kNegInf = -__builtin_huge_valf();
+constexpr float kLowInit = -1.0e30f;  // finite "minus infinity" for online LSE
+
+__host__ __device__ __forceinline__ long long rowbase(int w, int B, int lmax) {
+  const long long k = w - 1;
+  return static_cast<long long>(B) * (k * (lmax + 1) - k * (k + 1) / 2);
+}
+__host__ __device__ __forceinline__ long long chart_row(int w, int b, int i, int B, int lmax) {
+  return rowbase(w, B, lmax) + static_cast<long long>(b) * (lmax - w + 1) + i;
+}
+
+__device__ __forceinline__ float to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+template <typename T>
+__device__ __forceinline__ void store4(T* p, float a, float b, float c, float d);
+template <>
+__device__ __forceinline__ void store4<float>(float* p, float a, float b, float c, float d) {
+  *reinterpret_cast<float4*>(p) = make_float4(to_tf32(a), to_tf32(b), to_tf32(c), to_tf32(d));
+}
+template <>
+__device__ __forceinline__ void store4<__nv_bfloat16>(__nv_bfloat16* p, float a, float b, float c,
+                                                      float d) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(a, b);
+  __nv_bfloat162 hi = __floats2bfloat162_rn(c, d);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&lo);
+  u.y = *reinterpret_cast<uint32_t*>(&hi);
+  *reinterpret_cast<uint2*>(p) = u;
+}
+template <typename T>
+__device__ __forceinline__ T cvt1(float x);
+template <>
+__device__ __forceinline__ float cvt1<float>(float x) {
+  return to_tf32(x);
+}
+template <>
+__device__ __forceinline__ __nv_bfloat16 cvt1<__nv_bfloat16>(float x) {
+  return __float2bfloat16_rn(x);
+}
+
+// Split-precision stores: with lo != 0 (fp32 mode, bf16x3) a second plane
+// at element offset `lo` receives the bf16 residual x - bf16(x).
+template <typename T>
+__device__ __forceinline__ void store4s(T* p, long long lo, float a, float b, float c, float d) {
+  if constexpr (sizeof(T) == 2) {
+    store4<T>(p, a, b, c, d);
+    if (lo) {
+      const float ha = __bfloat162float(__float2bfloat16_rn(a));
+      const float hb = __bfloat162float(__float2bfloat16_rn(b));
+      const float hc = __bfloat162float(__float2bfloat16_rn(c));
+      const float hd = __bfloat162float(__float2bfloat16_rn(d));
+      store4<T>(p + lo, a - ha, b - hb, c - hc, d - hd);
+    }
+  } else {
+    store4<T>(p, a, b, c, d);
+  }
+}
+template <typename T>
+__device__ __forceinline__ void store1s(T* p, long long lo, float x) {
+  const T h = cvt1<T>(x);
+  *p = h;
+  if constexpr (sizeof(T) == 2) {
+    if (lo) p[lo] = cvt1<T>(x - __bfloat162float(h));
+  }
+}
+
+__device__ __forceinline__ float4 ldg4(const float* p) {
+  return __ldg(reinterpret_cast<const float4*>(p));
+}
+
+// Block-wide reduction; result valid in every thread.  `red` holds >= 33 floats.
+template <bool kMax>
+__device__ __forceinline__ float block_reduce(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    float t = __shfl_xor_sync(0xffffffffu, v, o);
+    v = kMax ? fmaxf(v, t) : v + t;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    float u = lane < nw ? red[lane] : (kMax ? kNegInf : 0.f);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      float t = __shfl_xor_sync(0xffffffffu, u, o);
+      u = kMax ? fmaxf(u, t) : u + t;
+    }
+    if (lane == 0) red[32] = u;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+// Reduce a block-uniform value over the CTAs of the cluster through DSMEM.
+template <bool kMax>
+__device__ __forceinline__ float cluster_reduce(float v, float* slot, float* bcast) {
+  cg::cluster_group cl = cg::this_cluster();
+  if (threadIdx.x == 0) *slot = v;
+  cl.sync();
+  if (threadIdx.x == 0) {
+    float r = kMax ? kNegInf : 0.f;
+    for (unsigned k = 0; k < cl.num_blocks(); ++k) {
+      float t = *cl.map_shared_rank(slot, k);
+      r = kMax ? fmaxf(r, t) : r + t;
+    }
+    *bcast = r;
+  }
+  cl.sync();
+  return *bcast;
+}
+
+// ---------------------------------------------------------------------------
+// K1: W_NN = exp([L_NN ; R_NN]) (2Np x Np), W_NP = exp([L_NP ; R_NP]) (2Np x Pp).
+// Once per step, not per sentence (inside.py:194-200 recomputes it per call).
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_prep_weights(const float* __restrict__ L, const float* __restrict__ R,
+                               T* __restrict__ wnn, T* __restrict__ wnp, int N, int P, int Np,
+                               int Pp, long long wnn_lo, long long wnp_lo) {
+  const int row = blockIdx.y;  // 0 .. 2Np-1
+  const bool right = row >= Np;
+  const int a = right ? row - Np : row;
+  const float* src = (right ? R : L) + static_cast<long long>(a) * (N + P);
+  const int total = Np + Pp;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < total; c += gridDim.x * blockDim.x) {
+    if (c < Np) {
+      float v = (a < N && c < N) ? expf(src[c]) : 0.f;
+      store1s<T>(wnn + static_cast<long long>(row) * Np + c, wnn_lo, v);
+    } else {
+      const int t = c - Np;
+      float v = (a < N && t < P) ? expf(src[N + t]) : 0.f;
+      store1s<T>(wnp + static_cast<long long>(row) * Pp + t, wnp_lo, v);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Width 1: o[1] = unary (inside.py:296-298); x† = max; E1 = exp(unary - x†).
+// One CTA per (sentence, position).  Padded positions get E1 = 0.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) k_prep_width1(const float* __restrict__ unary,
+                                                     const int* __restrict__ lengths,
+                                                     T* __restrict__ e1, float* __restrict__ X,
+                                                     int lmax, int P, int Pp, long long e1_lo) {
+  __shared__ float red[33];
+  const int r = blockIdx.x;  // = b * lmax + i = chart_row(1, b, i)
+  const int b = r / lmax, i = r % lmax;
+  const bool ok = i < lengths[b];
+  const float* u = unary + static_cast<long long>(r) * P;
+  float mx = kNegInf;
+  if (ok)
+    for (int t = threadIdx.x; t < P; t += blockDim.x) mx = fmaxf(mx, u[t]);
+  mx = block_reduce<true>(mx, red);
+  const float xs = (mx == kNegInf) ? 0.f : mx;
+  T* dst = e1 + static_cast<long long>(r) * Pp;
+  for (int t = threadIdx.x; t < Pp; t += blockDim.x)
+    store1s<T>(dst + t, e1_lo, (ok && t < P) ? __expf(u[t] - xs) : 0.f);
+  if (threadIdx.x == 0) X[r] = xs;
+}
+
+// ---------------------------------------------------------------------------
+// K4/K5: split-point contraction for width w (inside.py:313-332) + logZ
+// (inside.py:124-129).  One cluster of C CTAs per span row; each CTA owns a
+// contiguous chunk of Np/C nonterminal columns, each thread V float4s of it.
+// Online log-sum-exp over the w-1 split points with one exp per element;
+// the row max x† is reduced across the cluster through DSMEM, then E is
+// written in the GEMM operand type.  No (w-1, n, N) stack is materialised.
+// ---------------------------------------------------------------------------
+struct SplitArgs {
+  const float* A;
+  const float* Bc;
+  float* O;        // nullable
+  void* E;         // T*, row stride Np (nullable at w == lmax)
+  long long e_lo;  // element offset of the lo plane (fp32 mode), else 0
+  float* X;
+  float* TOP;      // B x Np : root + o at the top span (for d_root)
+  float* logZ;
+  const float* root;
+  const int* lengths;
+  int B, lmax, N, Np, w, cols_per_cta;
+};
+
+__device__ __forceinline__ void lse_push(float& M, float& S, float v) {
+  const float d = v - M;
+  const float e = __expf(-fabsf(d));  // d = -inf -> 0
+  const bool gt = d > 0.f;
+  S = gt ? fmaf(S, e, 1.f) : S + e;
+  M = gt ? v : M;
+}
+
+template <typename T, int V>
+__global__ void __launch_bounds__(256) k_split_fwd(SplitArgs a) {
+  __shared__ float red[33];
+  __shared__ float cl_slot, cl_bcast;
+  const int w = a.w;
+  const int n_w = a.lmax - w + 1;
+  const int local = blockIdx.y;
+  const int b = local / n_w, i = local % n_w;
+  const int len = a.lengths[b];
+  const long long row = rowbase(w, a.B, a.lmax) + local;
+  const int nthr = blockDim.x;
+  const int col0 = blockIdx.x * a.cols_per_cta + threadIdx.x * 4;
+  T* E = reinterpret_cast<T*>(a.E);
+
+  if (i + w > len) {  // span outside the sentence: never feeds a valid span
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int c = col0 + v * nthr * 4;
+      if (a.O) *reinterpret_cast<float4*>(a.O + row * a.Np + c) =
+          make_float4(kNegInf, kNegInf, kNegInf, kNegInf);
+      if (E) store4s<T>(E + row * a.Np + c, a.e_lo, 0.f, 0.f, 0.f, 0.f);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.X[row] = 0.f;
+    return;  // uniform across the cluster (same row)
+  }
+
+  float M[4 * V], S[4 * V];
+#pragma unroll
+  for (int k = 0; k < 4 * V; ++k) {
+    M[k] = kLowInit;
+    S[k] = 0.f;
+  }
+  // split m of span (i, i+w) pairs a[m][i] with b[w-m][i+m]   (inside.py:317-319)
+  int m = 1;
+  for (; m + 3 < w; m += 4) {
+    float4 va[4][V], vb[4][V];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int mm = m + u;
+      const float* pa = a.A + chart_row(mm, b, i, a.B, a.lmax) * a.Np;
+      const float* pb = a.Bc + chart_row(w - mm, b, i + mm, a.B, a.lmax) * a.Np;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        va[u][v] = ldg4(pa + col0 + v * nthr * 4);
+        vb[u][v] = ldg4(pb + col0 + v * nthr * 4);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        lse_push(M[4 * v + 0], S[4 * v + 0], va[u][v].x + vb[u][v].x);
+        lse_push(M[4 * v + 1], S[4 * v + 1], va[u][v].y + vb[u][v].y);
+        lse_push(M[4 * v + 2], S[4 * v + 2], va[u][v].z + vb[u][v].z);
+        lse_push(M[4 * v + 3], S[4 * v + 3], va[u][v].w + vb[u][v].w);
+      }
+  }
+  for (; m < w; ++m) {
+    const float* pa = a.A + chart_row(m, b, i, a.B, a.lmax) * a.Np;
+    const float* pb = a.Bc + chart_row(w - m, b, i + m, a.B, a.lmax) * a.Np;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      float4 x = ldg4(pa + col0 + v * nthr * 4);
+      float4 y = ldg4(pb + col0 + v * nthr * 4);
+      lse_push(M[4 * v + 0], S[4 * v + 0], x.x + y.x);
+      lse_push(M[4 * v + 1], S[4 * v + 1], x.y + y.y);
+      lse_push(M[4 * v + 2], S[4 * v + 2], x.z + y.z);
+      lse_push(M[4 * v + 3], S[4 * v + 3], x.w + y.w);
+    }
+  }
+  float o[4 * V];
+  float mx = kNegInf;
+#pragma unroll
+  for (int k = 0; k < 4 * V; ++k) {
+    o[k] = S[k] > 0.f ? M[k] + __logf(S[k]) : kNegInf;
+    mx = fmaxf(mx, o[k]);
+  }
+  if (a.O) {
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+      *reinterpret_cast<float4*>(a.O + row * a.Np + col0 + v * nthr * 4) =
+          make_float4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+  }
+  // row max over all Np columns: block, then cluster (DSMEM)
+  mx = block_reduce<true>(mx, red);
+  mx = cluster_reduce<true>(mx, &cl_slot, &cl_bcast);
+  const float xs = (mx == kNegInf) ? 0.f : mx;  // inside.py:324-326
+  if (E) {
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+      store4s<T>(E + row * a.Np + col0 + v * nthr * 4, a.e_lo, __expf(o[4 * v] - xs),
+                __expf(o[4 * v + 1] - xs), __expf(o[4 * v + 2] - xs), __expf(o[4 * v + 3] - xs));
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.X[row] = xs;
+
+  if (i == 0 && w == len) {  // top span: logZ = LSE_A(root[A] + o[A])  (inside.py:124-129)
+    float sc[4 * V];
+    float smx = kNegInf;
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int c = col0 + v * nthr * 4 + k;
+        sc[4 * v + k] = c < a.N ? a.root[c] + o[4 * v + k] : kNegInf;
+        a.TOP[static_cast<long long>(b) * a.Np + c] = sc[4 * v + k];
+        smx = fmaxf(smx, sc[4 * v + k]);
+      }
+    smx = block_reduce<true>(smx, red);
+    smx = cluster_reduce<true>(smx, &cl_slot, &cl_bcast);
+    float s = 0.f;
+    if (smx != kNegInf) {
+#pragma unroll
+      for (int k = 0; k < 4 * V; ++k) s += expf(sc[k] - smx);
+    }
+    s = block_reduce<false>(s, red);
+    s = cluster_reduce<false>(s, &cl_slot, &cl_bcast);
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.logZ[b] = smx == kNegInf ? kNegInf : smx + logf(s);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Backward seed (inside.py:400-404): the root posterior
+//   post[A] = exp(root[A] + o[len][0, A] - logZ)
+// seeds the outside pass at each sentence's top span, stored in log form
+// lq = log|g·post| - o = root - logZ + log|g|, and is itself d_root.
+// One thread per nonterminal column; loops over sentences.
+// ---------------------------------------------------------------------------
+__global__ void k_seed_bwd(const float* __restrict__ root, const float* __restrict__ TOP,
+                           const float* __restrict__ logZ, const float* __restrict__ g,
+                           const int* __restrict__ lengths, float* __restrict__ LQ,
+                           float* __restrict__ droot, int* __restrict__ flag, int B, int lmax,
+                           int N, int Np) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= Np) return;
+  float acc = 0.f;
+  for (int b = 0; b < B; ++b) {
+    const float lz = logZ[b];
+    const float gb = g[b];
+    const bool finite = isfinite(lz);
+    if (!finite && c == 0) atomicOr(flag, 1);
+    float lq = kNegInf;
+    if (finite && gb != 0.f && c < N) {
+      lq = root[c] - lz + logf(fabsf(gb));
+      acc += gb * expf(TOP[static_cast<long long>(b) * Np + c] - lz);
+    }
+    LQ[chart_row(lengths[b], b, 0, B, lmax) * Np + c] = lq;
+  }
+  if (c < N) droot[c] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// K7: gather-form split backward for child width m (inside.py:406-417).
+// For span (i, i+m) of sentence b, with Q_w = log|go_w| - o_w (LQ):
+//   G_L = [a != -inf] * sum_{w>m}  exp(x†_m + b[w-m][i+m] + LQ[w][i])
+//   G_R = [b != -inf] * sum_{s<i}  exp(x†_m + a[i-s][s]   + LQ[i+m-s][s])
+// which equals ga·exp(x† - a) (resp. gb·exp(x† - b)) of the reference, the
+// row of the dgrad/wgrad GEMM operand; the a (resp. b) factor cancels.
+// Each accumulator is written once: deterministic, no atomics.
+// ---------------------------------------------------------------------------
+struct GatherArgs {
+  const float* A;
+  const float* Bc;
+  const float* LQ;
+  const float* X;
+  void* G;  // T*, row stride 2*Np
+  long long g_lo;
+  const int* lengths;
+  const float* g;
+  int B, lmax, Np, m, cols_per_cta;
+};
+
+template <typename T, int V>
+__global__ void __launch_bounds__(256) k_gather_bwd(GatherArgs a) {
+  const int m = a.m;
+  const int n_m = a.lmax - m + 1;
+  const int local = blockIdx.y;
+  const int b = local / n_m, i = local % n_m;
+  const int len = a.lengths[b];
+  const long long row = rowbase(m, a.B, a.lmax) + local;
+  const int nthr = blockDim.x;
+  const int col0 = blockIdx.x * a.cols_per_cta + threadIdx.x * 4;
+  T* G = reinterpret_cast<T*>(a.G) + row * (2LL * a.Np);
+
+  if (i + m > len) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int c = col0 + v * nthr * 4;
+      store4s<T>(G + c, a.g_lo, 0.f, 0.f, 0.f, 0.f);
+      store4s<T>(G + a.Np + c, a.g_lo, 0.f, 0.f, 0.f, 0.f);
+    }
+    return;
+  }
+  const float xm = a.X[row];
+  float gl[4 * V], gr[4 * V];
+#pragma unroll
+  for (int k = 0; k < 4 * V; ++k) gl[k] = gr[k] = 0.f;
+
+  // left child (i, i+m) of parent (i, i+w): right sibling b[w-m][i+m]
+  const int wmax = len - i;
+  int w = m + 1;
+  for (; w + 1 <= wmax; w += 2) {
+    float4 vb[2][V], vq[2][V];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const float* pb = a.Bc + chart_row(w + u - m, b, i + m, a.B, a.lmax) * a.Np;
+      const float* pq = a.LQ + chart_row(w + u, b, i, a.B, a.lmax) * a.Np;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        vb[u][v] = ldg4(pb + col0 + v * nthr * 4);
+        vq[u][v] = ldg4(pq + col0 + v * nthr * 4);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        gl[4 * v + 0] += __expf(xm + vb[u][v].x + vq[u][v].x);
+        gl[4 * v + 1] += __expf(xm + vb[u][v].y + vq[u][v].y);
+        gl[4 * v + 2] += __expf(xm + vb[u][v].z + vq[u][v].z);
+        gl[4 * v + 3] += __expf(xm + vb[u][v].w + vq[u][v].w);
+      }
+  }
+  for (; w <= wmax; ++w) {
+    const float* pb = a.Bc + chart_row(w - m, b, i + m, a.B, a.lmax) * a.Np;
+    const float* pq = a.LQ + chart_row(w, b, i, a.B, a.lmax) * a.Np;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      float4 x = ldg4(pb + col0 + v * nthr * 4);
+      float4 q = ldg4(pq + col0 + v * nthr * 4);
+      gl[4 * v + 0] += __expf(xm + x.x + q.x);
+      gl[4 * v + 1] += __expf(xm + x.y + q.y);
+      gl[4 * v + 2] += __expf(xm + x.z + q.z);
+      gl[4 * v + 3] += __expf(xm + x.w + q.w);
+    }
+  }
+  // right child (i, i+m) of parent (s, i+m): left sibling a[i-s][s]
+  int s = 0;
+  for (; s + 1 < i; s += 2) {
+    float4 va[2][V], vq[2][V];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int ss = s + u;
+      const float* pa = a.A + chart_row(i - ss, b, ss, a.B, a.lmax) * a.Np;
+      const float* pq = a.LQ + chart_row(i + m - ss, b, ss, a.B, a.lmax) * a.Np;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        va[u][v] = ldg4(pa + col0 + v * nthr * 4);
+        vq[u][v] = ldg4(pq + col0 + v * nthr * 4);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        gr[4 * v + 0] += __expf(xm + va[u][v].x + vq[u][v].x);
+        gr[4 * v + 1] += __expf(xm + va[u][v].y + vq[u][v].y);
+        gr[4 * v + 2] += __expf(xm + va[u][v].z + vq[u][v].z);
+        gr[4 * v + 3] += __expf(xm + va[u][v].w + vq[u][v].w);
+      }
+  }
+  for (; s < i; ++s) {
+    const float* pa = a.A + chart_row(i - s, b, s, a.B, a.lmax) * a.Np;
+    const float* pq = a.LQ + chart_row(i + m - s, b, s, a.B, a.lmax) * a.Np;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      float4 x = ldg4(pa + col0 + v * nthr * 4);
+      float4 q = ldg4(pq + col0 + v * nthr * 4);
+      gr[4 * v + 0] += __expf(xm + x.x + q.x);
+      gr[4 * v + 1] += __expf(xm + x.y + q.y);
+      gr[4 * v + 2] += __expf(xm + x.z + q.z);
+      gr[4 * v + 3] += __expf(xm + x.w + q.w);
+    }
+  }
+  // zero-mass projections carry no gradient (inside.py:441-443 NaN guard)
+  const float sg = a.g[b] < 0.f ? -1.f : 1.f;
+  const float* pam = a.A + row * a.Np;
+  const float* pbm = a.Bc + row * a.Np;
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int c = col0 + v * nthr * 4;
+    float4 am = ldg4(pam + c), bm = ldg4(pbm + c);
+    store4s<T>(G + c, a.g_lo, am.x == kNegInf ? 0.f : sg * gl[4 * v + 0],
+              am.y == kNegInf ? 0.f : sg * gl[4 * v + 1], am.z == kNegInf ? 0.f : sg * gl[4 * v + 2],
+              am.w == kNegInf ? 0.f : sg * gl[4 * v + 3]);
+    store4s<T>(G + a.Np + c, a.g_lo, bm.x == kNegInf ? 0.f : sg * gr[4 * v + 0],
+              bm.y == kNegInf ? 0.f : sg * gr[4 * v + 1], bm.z == kNegInf ? 0.f : sg * gr[4 * v + 2],
+              bm.w == kNegInf ? 0.f : sg * gr[4 * v + 3]);
+  }
+}
+
+// Span marginals mu_sym[w][i, A] = go / |g| = exp(LQ + o - log|g|)  (inside.py:425-430)
+__global__ void k_marginals(const float* __restrict__ LQ, const float* __restrict__ O,
+                            const float* __restrict__ g, const int* __restrict__ lengths,
+                            float* __restrict__ mu, int B, int lmax, int Np, int N) {
+  const long long row = rowbase(2, B, lmax) + blockIdx.x;  // rows of widths >= 2
+  // recover (w, b, i) from the row index
+  long long r = row;
+  int w = 2;
+  while (w < lmax && r >= rowbase(w + 1, B, lmax)) ++w;
+  const int n_w = lmax - w + 1;
+  const long long local = r - rowbase(w, B, lmax);
+  const int b = static_cast<int>(local / n_w), i = static_cast<int>(local % n_w);
+  const bool ok = i + w <= lengths[b] && g[b] != 0.f;
+  const float lg = ok ? logf(fabsf(g[b])) : 0.f;
+  for (int c = threadIdx.x; c < N; c += blockDim.x) {
+    float v = 0.f;
+    if (ok) v = __expf(LQ[row * Np + c] + O[row * Np + c] - lg);
+    mu[(row - rowbase(2, B, lmax)) * N + c] = v;
+  }
+}
+
+}  // namespace fi
