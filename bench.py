@@ -1,0 +1,443 @@
+"""Benchmark: inside fwd+bwd sentences/s at |N|=4096, length 40, batch 64
+(BASELINE.json config 3) on 1..8 B200s, with the roofline of the dominant
+kernel and the CPU oracle timed on the same host.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+One step = forward + backward of the inside op over one batch of B sentences
+per GPU (weak scaling: B per rank, the batch is sharded across ranks), plus
+one NCCL all-reduce of the grammar gradients [dL | dR | droot] when N > 1.
+Rank 0 prints ONE JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {  # BASELINE.json configs (N = P = |N|)
+    1: dict(n=64, batch=8, length=20),
+    2: dict(n=1024, batch=32, length=30),
+    3: dict(n=4096, batch=64, length=40),
+    5: dict(n=8192, batch=128, length=40),
+}
+METRIC = "inside fwd+bwd sentences/sec @|N|=4096,len40 (1/2/4/8 B200) vs CPU; % roofline"
+VOCAB = 64
+
+
+# ---------------------------------------------------------------- helpers
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clock / throttle-reason sampling during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.gpu)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(smax)) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+# ------------------------------------------------------- algorithmic work
+def algorithmic_work(n: int, p: int, batch: int, length: int, gemm_esz: int, store_o: bool):
+    """Per-class algorithmic flops / bytes of one fwd+bwd step.
+
+    GEMM flops count only the live blocks: width 1 contracts over P, widths
+    2..l-1 over N; dgrad and wgrad repeat the forward count.  Split bytes are
+    the compulsory HBM bytes of the fp32 chart vectors each kernel must read
+    plus the vectors it writes, with no cross-launch reuse assumed."""
+    l = length
+    rows_w1 = batch * l
+    rows_mid = batch * (l * (l - 1) // 2 - 1)          # widths 2..l-1
+    f_fwd = 2.0 * rows_w1 * (2 * n) * p + 2.0 * rows_mid * (2 * n) * n
+    s = 4.0  # fp32 chart element
+    pairs = batch * math.comb(l + 1, 3)                # (span, split) pairs
+    spans_ge2 = batch * (l * (l - 1) // 2)             # widths 2..l
+    split_bytes = (2 * pairs * n * s                   # a[m] + b[w-m] reads
+                   + spans_ge2 * n * (s if store_o else 0)
+                   + rows_mid * n * gemm_esz)          # E write (operand)
+    # gather backward: each (span, split) pair is visited twice (as left child
+    # and as right child), reading the sibling and the parent's LQ each time;
+    # plus a, b of the row itself and the 2N-wide G row written.
+    rows_bwd = batch * (l * (l + 1) // 2 - 1)          # widths 1..l-1
+    gather_bytes = 4 * pairs * n * s + rows_bwd * (2 * n * s + 2 * n * gemm_esz)
+    return {
+        "gemm_fwd": ("tensor", f_fwd),
+        "gemm_dgrad": ("tensor", f_fwd),
+        "gemm_wgrad": ("tensor", f_fwd),
+        "split_fwd": ("hbm", split_bytes),
+        "gather_bwd": ("hbm", gather_bytes),
+    }
+
+
+# -------------------------------------------------------------- our arm
+def run_ours(args, world, rank, local):
+    import torch
+    import torch.distributed as dist
+    from paper_2310_14997_b200 import _lib
+    from paper_2310_14997_b200.grammar import GrammarDims, random_grammar
+    from paper_2310_14997_b200.ops import inside
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS[args.config]
+    n, length = cfg["n"], cfg["length"]
+    batch = args.batch or cfg["batch"]
+    if args.scaling == "strong":
+        if batch % world:
+            raise SystemExit(f"strong scaling needs batch % gpus == 0 ({batch} % {world})")
+        batch //= world
+
+    g = random_grammar(GrammarDims(n, n, VOCAB), seed=0)
+    rng = np.random.default_rng(1 + rank)
+    tokens = rng.integers(0, VOCAB, size=(batch, length))
+    L = torch.tensor(g.log_left, dtype=torch.float32, device=dev)
+    R = torch.tensor(g.log_right, dtype=torch.float32, device=dev)
+    root = torch.tensor(g.log_root, dtype=torch.float32, device=dev)
+    emit = torch.tensor(g.log_emit, dtype=torch.float32, device=dev)
+    tok_d = torch.as_tensor(tokens, device=dev)
+    unary = emit.t()[tok_d].contiguous()
+    lengths = torch.full((batch,), length, dtype=torch.int32, device=dev)
+    for t in (L, R, root, unary):
+        t.requires_grad_(True)
+    lib = _lib.load()
+
+    def allreduce(dL, dR, droot):
+        if world == 1:
+            return
+        flat = torch.cat([dL.view(-1), dR.view(-1), droot.view(-1)])
+        dist.all_reduce(flat)
+        k = dL.numel()
+        dL.copy_(flat[:k].view_as(dL))
+        dR.copy_(flat[k:2 * k].view_as(dR))
+        droot.copy_(flat[2 * k:].view_as(droot))
+
+    def step(Li, Ri, rooti, unaryi):
+        log_z = inside(Li, Ri, rooti, unaryi, lengths, gemm_dtype=args.gemm_dtype)
+        loss = -log_z.mean()                          # train.py:218: d loss = -1/B
+        dL, dR, droot, dun = torch.autograd.grad(loss, [Li, Ri, rooti, unaryi])
+        allreduce(dL, dR, droot)
+        return log_z, loss, dL, dR, droot, dun
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-resident timed region
+    for _ in range(args.warmup):
+        step(L, R, root, unary)
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    _lib.profile_enable(True)
+    launch0 = lib.fi_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record()
+    for _ in range(args.steps):
+        _, loss, *_ = step(L, R, root, unary)
+    e1.record()
+    barrier()
+    _lib.profile_enable(False)
+    prof = _lib.profile_collect()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    gpu_launches = int(lib.fi_launch_count() - launch0)
+    loss_val = float(loss.item())
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * batch / (ms / 1e3)
+
+    # ---- end-to-end through host buffers (reference-facing call pattern)
+    e2e = None
+    if not args.no_e2e:
+        pin = dict(pin_memory=True)
+        Lh = torch.tensor(g.log_left, dtype=torch.float32).pin_memory()
+        Rh = torch.tensor(g.log_right, dtype=torch.float32).pin_memory()
+        rooth = torch.tensor(g.log_root, dtype=torch.float32).pin_memory()
+        emith = torch.tensor(g.log_emit, dtype=torch.float32).pin_memory()
+        tokh = torch.as_tensor(tokens).pin_memory()
+        outs = [torch.empty(g.log_left.shape, dtype=torch.float32, **pin),
+                torch.empty(g.log_right.shape, dtype=torch.float32, **pin),
+                torch.empty(g.log_root.shape, dtype=torch.float32, **pin),
+                torch.empty(g.log_emit.shape, dtype=torch.float32, **pin),
+                torch.empty(batch, dtype=torch.float32, **pin)]
+        h2d = sum(t.numel() * t.element_size() for t in (Lh, Rh, rooth, emith, tokh))
+        d2h = sum(t.numel() * t.element_size() for t in outs)
+
+        def e2e_step():
+            Ld = Lh.to(dev, non_blocking=True).requires_grad_(True)
+            Rd = Rh.to(dev, non_blocking=True).requires_grad_(True)
+            rd = rooth.to(dev, non_blocking=True).requires_grad_(True)
+            ed = emith.to(dev, non_blocking=True)
+            td = tokh.to(dev, non_blocking=True)
+            un = ed.t()[td].contiguous().requires_grad_(True)
+            log_z, loss, dL, dR, droot, dun = step(Ld, Rd, rd, un)
+            d_emit = torch.zeros(VOCAB, n, device=dev).index_add_(
+                0, td.view(-1), dun.reshape(-1, n))           # inside.py:420-423
+            for dst, src in zip(outs, (dL, dR, droot, d_emit.t(), log_z.detach())):
+                dst.copy_(src, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        barrier()
+        ems = (time.perf_counter() - t0) * 1e3 / args.steps
+        if world > 1:
+            t = torch.tensor([ems], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": world * batch / (ems / 1e3), "unit": "sentences/s",
+               "ms_per_step": ems, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h),
+               "path": "pinned host grammar+tokens -> H2D -> op fwd+bwd -> D2H log_z+GrammarGrad"}
+
+    # ---- roofline of the dominant kernel class
+    peaks = measured_peaks()
+    esz = 4 if args.gemm_dtype == "tf32" else 2
+    work = algorithmic_work(n, n, batch, length, esz, store_o=False)
+    per_class = {}
+    for name, (tot_ms, cnt) in prof.items():
+        if cnt:
+            per_class[name] = {"ms_per_step": tot_ms / args.steps,
+                               "launches_per_step": cnt // args.steps}
+    dominant = max((k for k in per_class if k in work), key=lambda k: per_class[k]["ms_per_step"])
+    bound, amount = work[dominant]
+    k_ms = per_class[dominant]["ms_per_step"]
+    if bound == "hbm":
+        achieved = amount / (k_ms / 1e3) / 1e9
+        peak = peaks["hbm_gbs"]
+        unit = "GB/s"
+    else:
+        achieved = amount / (k_ms / 1e3) / 1e12
+        peak = peaks["bf16_tflops_sustained"]
+        unit = "TFLOP/s"
+    for name, d in per_class.items():
+        if name in work:
+            b, amt = work[name]
+            d["achieved"] = amt / (d["ms_per_step"] / 1e3) / (1e9 if b == "hbm" else 1e12)
+            d["unit"] = "GB/s" if b == "hbm" else "TFLOP/s"
+            d["frac"] = d["achieved"] / (peaks["hbm_gbs"] if b == "hbm"
+                                         else peaks["bf16_tflops_sustained"])
+    traffic = None
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get(dominant)
+    roofline = {"kernel": dominant, "bound": bound, "achieved": achieved, "peak": peak,
+                "unit": unit, "frac": achieved / peak, "traffic": traffic,
+                "peak_source": peaks["source"] + (" sustained" if bound == "tensor" else ""),
+                "per_class": per_class}
+
+    # ---- CPU baseline (oracle port) on rank 0, N = 1 only
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(g, tokens[:1], length)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "sentences/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+            "dtype": "fp32 chart, " + {"bf16": "bf16", "tf32": "tf32",
+                                       "fp32": "bf16x3 (fp32-accurate)"}[args.gemm_dtype]
+                     + " GEMM operands, fp32 accumulate",
+            "data": "synthetic: random_grammar(GrammarDims(N,N,64), seed=0) Dirichlet(1) rows; "
+                    "uniform tokens default_rng(1+rank)",
+            "config": {"workload": f"config {args.config}: SimplePCFG |N|={n} (N=P={n}), "
+                                   f"length {length}, batch {batch} per GPU, fwd+bwd",
+                       "n_nt": n, "n_pt": n, "length": length, "batch_per_gpu": batch,
+                       "global_batch": batch * world, "gemm_dtype": args.gemm_dtype,
+                       "parallelism": f"dp{world}",
+                       "l2": "working set ~4 GB chart per step >> 126 MB L2 (no flush needed)"},
+            "clocks": clk,
+            "e2e": e2e,
+            "gpu_launches": gpu_launches,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "loss": loss_val,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline_sample(g, tokens, length):
+    """Time the CPU oracle (float64 NumPy port of the reference path) on a
+    bounded sample: one sentence of the workload, forward + backward."""
+    from oracle import flashinside_oracle as O
+    try:
+        import threadpoolctl
+        threadpoolctl.threadpool_limits(_cpu_threads())
+    except ImportError:
+        pass
+    un = O.unary_from_tokens(np.asarray(g.log_emit), tokens, length)
+    t0 = time.perf_counter()
+    O.inside_batch(g.log_left, g.log_right, g.log_root, un, np.array([length]))
+    dt = time.perf_counter() - t0
+    return {"value": tokens.shape[0] / dt, "unit": "sentences/s", "cores": _cpu_threads(),
+            "kind": "port", "seconds": dt,
+            "sample": f"{tokens.shape[0]} sentence (l={length}) of the workload, fwd + "
+                      "GEMM-form bwd, float64 NumPy/OpenBLAS, all host threads"}
+
+
+# --------------------------------------------------------- reference arm
+def run_reference(args, world, rank):
+    """The reference's CPU path (oracle port: the reference is Python and does
+    not travel to the GPU box) on this host's cores, rank 0 only."""
+    if rank != 0:
+        return
+    from paper_2310_14997_b200.grammar import GrammarDims, random_grammar
+    from oracle import flashinside_oracle as O
+    try:
+        import threadpoolctl
+        threadpoolctl.threadpool_limits(_cpu_threads())
+    except ImportError:
+        pass
+    cfg = CONFIGS[args.config]
+    n, length = cfg["n"], cfg["length"]
+    g = random_grammar(GrammarDims(n, n, VOCAB), seed=0)
+    rng = np.random.default_rng(1)
+    sample = 1  # sentences per step: a bounded sample of the batch
+    tok = rng.integers(0, VOCAB, size=(args.steps + args.warmup, length))
+    un_all = O.unary_from_tokens(np.asarray(g.log_emit), tok, length)
+    for k in range(args.warmup):
+        O.inside_batch(g.log_left, g.log_right, g.log_root, un_all[k:k + 1], np.array([length]))
+    t0 = time.perf_counter()
+    for k in range(args.warmup, args.warmup + args.steps):
+        O.inside_batch(g.log_left, g.log_right, g.log_root, un_all[k:k + 1], np.array([length]))
+    dt = (time.perf_counter() - t0) / args.steps
+    value = sample / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "sentences/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (same grammar/tokens generator as our arm)",
+        "config": {"workload": f"config {args.config}: SimplePCFG |N|={n}, length {length}, "
+                               f"{sample} sentence per step (bounded sample), fwd+bwd",
+                   "n_nt": n, "length": length, "parallelism": "cpu"},
+        "cpu_baseline": {"value": value, "unit": "sentences/s", "cores": _cpu_threads(),
+                         "kind": "port",
+                         "sample": f"{sample} sentence per step; float64 NumPy port of "
+                                   "inside_flash + inside_backward (GEMM form)"},
+        "e2e": {"value": value, "unit": "sentences/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, choices=sorted(CONFIGS), default=3)
+    ap.add_argument("--batch", type=int, default=None, help="sentences per GPU (weak) / "
+                    "global (strong); default: the config's batch")
+    ap.add_argument("--gemm-dtype", choices=["bf16", "tf32", "fp32"], default="bf16")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    world, rank, local = dist_env()
+    if world != args.gpus and not (world == 1 and args.gpus == 1):
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -66,7 +66,11 @@ typedef struct fi_shape {
 /* Byte offsets of the chart arrays inside the workspace, for chart export.
  * Row r of an array with row stride `np` lives at offset + 4*r*np.
  *   row(w, b, i) = rowbase(w) + b*(l-w+1) + i,
- *   rowbase(w)   = B * ((w-1)*(l+1) - (w-1)*w/2). */
+ *   rowbase(w)   = B * ((w-1)*(l+1) - (w-1)*w/2).
+ * Storage is base-2 and shifted: the natural-log value of a chart entry is
+ *   ln2 * (x[row] + stored[row, A])
+ * with x[row] the fp64 per-span shift (off_x) and the stored fp32 offsets
+ * a^, b^, o^ (o^ <= 0) and, after a backward, lq^ = log2|go| - log2 o + x. */
 typedef struct fi_chart_layout {
   int64_t np;       /* padded N (row stride, floats)          */
   int64_t pp;       /* padded P                               */
@@ -74,7 +78,7 @@ typedef struct fi_chart_layout {
   int64_t off_a;    /* a[w]  fp32, widths 1..l-1              */
   int64_t off_b;    /* b[w]  fp32, widths 1..l-1              */
   int64_t off_o;    /* o[w]  fp32, widths 2..l (-1 if absent) */
-  int64_t off_x;    /* x†    fp32 per row                     */
+  int64_t off_x;    /* x†    fp64 per row (log2 units)        */
   int64_t off_lq;   /* log|go|-o, widths 2..l (after backward)*/
   int64_t off_flag; /* int32 error flags (bit0: non-finite logZ in backward) */
 } fi_chart_layout;
@@ -110,8 +114,24 @@ int fi_marginals(const fi_shape* shape, const int32_t* lengths, const float* gra
 int fi_test_gemm(int32_t dtype, int32_t a_mn, int32_t b_mn, int32_t M, int32_t N, int32_t K,
                  const void* A, const void* B, float* C, void* stream);
 
-/* Number of kernels the last forward/backward call enqueued (for bench accounting). */
-int32_t fi_last_launch_count(void);
+/* Cumulative number of kernels this library has enqueued in the process
+ * (bench accounting: difference before/after the timed region). */
+int64_t fi_launch_count(void);
+
+/* Optional per-kernel-class timing with CUDA events recorded on the launch
+ * stream around every launch of this thread (bench.py roofline).  Collect
+ * synchronizes on the recorded events, returns total ms and launch counts per
+ * class (arrays of n >= FI_PROF_NCLASS) and clears the record. */
+#define FI_PROF_PREP 0       /* exp of [L|R], width-1 prep (and test GEMMs) */
+#define FI_PROF_SPLIT 1      /* k_split_fwd: split-point contraction         */
+#define FI_PROF_GEMM_FWD 2   /* projection GEMM, EPI_FWD                      */
+#define FI_PROF_SEED 3       /* k_seed_bwd                                    */
+#define FI_PROF_GATHER 4     /* k_gather_bwd: split backward                  */
+#define FI_PROF_GEMM_DGRAD 5 /* dgrad GEMMs (EPI_DGRAD, EPI_DUNARY)           */
+#define FI_PROF_GEMM_WGRAD 6 /* wgrad GEMMs (EPI_WGRAD)                       */
+#define FI_PROF_NCLASS 7
+void fi_profile_enable(int32_t on);
+int fi_profile_collect(float* ms, int32_t* counts, int32_t n);
 
 const char* fi_last_error(void);
 int32_t fi_version(void);

@@ -20,6 +20,9 @@ FI_GEMM_BF16 = 0
 FI_GEMM_TF32 = 1
 FI_GEMM_FP32 = 2
 
+PROF_CLASSES = ("prep", "split_fwd", "gemm_fwd", "seed", "gather_bwd", "gemm_dgrad",
+                "gemm_wgrad")
+
 GEMM_DTYPES = {"bf16": FI_GEMM_BF16, "tf32": FI_GEMM_TF32, "fp32": FI_GEMM_FP32}
 
 
@@ -64,7 +67,9 @@ SIGNATURES = [
     ("fi_test_gemm", c_int32,
      [c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p,
       c_void_p]),
-    ("fi_last_launch_count", c_int32, []),
+    ("fi_launch_count", c_int64, []),
+    ("fi_profile_enable", None, [c_int32]),
+    ("fi_profile_collect", c_int32, [POINTER(c_float), POINTER(c_int32), c_int32]),
     ("fi_last_error", c_char_p, []),
     ("fi_version", c_int32, []),
 ]
@@ -124,3 +129,16 @@ def chart_layout(s: FiShape) -> FiChartLayout:
     out = FiChartLayout()
     check(load().fi_get_chart_layout(ctypes.byref(s), ctypes.byref(out)))
     return out
+
+
+def profile_enable(on: bool) -> None:
+    load().fi_profile_enable(1 if on else 0)
+
+
+def profile_collect() -> dict:
+    """{class: (total_ms, launches)} since the last collect (synchronizes)."""
+    n = len(PROF_CLASSES)
+    ms = (c_float * n)()
+    cnt = (c_int32 * n)()
+    check(load().fi_profile_collect(ms, cnt, n))
+    return {name: (float(ms[i]), int(cnt[i])) for i, name in enumerate(PROF_CLASSES)}

@@ -16,6 +16,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
+#include <mutex>
+#include <vector>
 #include <cudaTypedefs.h>
 
 #include "../../include/flashinside.h"
@@ -27,7 +30,52 @@ using namespace fi;
 namespace {
 
 thread_local char g_err[512] = "";
-thread_local int g_launches = 0;
+// Process-wide count of kernels this library enqueued (autograd runs the
+// backward on its own thread, so nothing here is thread-local).
+std::atomic<long long> g_launches{0};
+
+// ---------------------------------------------------------------- profiler
+// Optional per-kernel-class CUDA-event timing (bench.py roofline): when
+// enabled, every launch is bracketed by two events on its own stream.
+struct ProfRec {
+  int cls;
+  cudaEvent_t a, b;
+};
+std::atomic<bool> g_prof_on{false};
+std::mutex g_prof_mu;
+std::vector<ProfRec> g_prof;
+std::vector<cudaEvent_t> g_prof_pool;
+
+cudaEvent_t prof_event() {  // caller holds g_prof_mu
+  if (!g_prof_pool.empty()) {
+    cudaEvent_t e = g_prof_pool.back();
+    g_prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct ProfScope {
+  cudaStream_t st;
+  ProfRec rec;
+  bool on;
+  ProfScope(int cls, cudaStream_t s) : st(s), on(g_prof_on.load()) {
+    if (!on) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    rec.cls = cls;
+    rec.a = prof_event();
+    rec.b = prof_event();
+    cudaEventRecord(rec.a, st);
+  }
+  ~ProfScope() {
+    if (!on) return;
+    cudaEventRecord(rec.b, st);
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof.push_back(rec);
+  }
+};
 
 int set_err(int code, const char* fmt, ...) {
   va_list ap;
@@ -55,7 +103,7 @@ int set_err(int code, const char* fmt, ...) {
 struct Plan {
   int N, P, B, l, Np, Pp, esz, clusters, v, threads, cols_per_cta;
   long long rows;
-  size_t wnn, wnp, e1, eall, gall, a, b, o, lq, x, top, flag, total;
+  size_t wnn, wnp, e1, eall, gall, a, b, o, lq, x, top, topz, flag, total;
   // element offsets of the lo planes of the GEMM operands (fp32 mode only)
   long long wnn_lo, wnp_lo, e1_lo, eall_lo, gall_lo;
   bool store_o, tf32, split;
@@ -119,8 +167,9 @@ int make_plan(const fi_shape* s, Plan* p) {
   p->b = take(4ull * rows * p->Np);
   p->o = p->store_o ? take(4ull * rows * p->Np) : static_cast<size_t>(-1);
   p->lq = take(4ull * rows * p->Np);
-  p->x = take(4ull * rows);
+  p->x = take(8ull * rows);  // fp64 row shifts
   p->top = take(4ull * p->B * p->Np);
+  p->topz = take(4ull * p->B);
   p->flag = take(256);
   p->total = off;
   return FI_OK;
@@ -184,7 +233,7 @@ int num_sms() {
   return cached[dev] > 0 ? cached[dev] : 148;
 }
 
-template <typename T, int BN, bool AMN, bool BMN, int EPI, bool SPLIT>
+template <typename T, int BN, bool AMN, bool BMN, int EPI, bool SPLIT, int CHUNK>
 int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_row0,
                 const GemmEpi& ep, cudaStream_t st) {
   using Cf = GemmCfg<T, BN>;
@@ -211,7 +260,7 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
   sh.num_m = (M + Cf::BM - 1) / Cf::BM;
   sh.num_n = N / BN;
   sh.num_k = (K + Cf::BK - 1) / Cf::BK;
-  auto kern = k_gemm<T, BN, AMN, BMN, EPI, SPLIT>;
+  auto kern = k_gemm<T, BN, AMN, BMN, EPI, SPLIT, CHUNK>;
   static bool attr_done[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -223,6 +272,9 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
   const int tiles = sh.num_m * sh.num_n;
   const int grid = tiles < num_sms() ? tiles : num_sms();
   if (grid <= 0) return FI_OK;
+  ProfScope prof(EPI == EPI_FWD ? FI_PROF_GEMM_FWD
+                 : EPI == EPI_WGRAD ? FI_PROF_GEMM_WGRAD
+                 : EPI == EPI_STORE ? FI_PROF_PREP : FI_PROF_GEMM_DGRAD, st);
   kern<<<grid, 256, Cf::SMEM_BYTES, st>>>(ta, tb, ta2, tb2, sh, ep);
   ++g_launches;
   FI_CUDA(cudaGetLastError());
@@ -236,11 +288,22 @@ int run_gemm_s(const Operand& A, const Operand& B, int M, int N, int K, int a_ro
   if (M <= 0 || N <= 0) return FI_OK;
   const long long mt = (M + 127) / 128;
   const int sms = num_sms();
-  if (N % 256 == 0 && mt * (N / 256) >= sms)
-    return launch_gemm<T, 256, AMN, BMN, EPI, SPLIT>(A, B, M, N, K, a_row0, ep, st);
-  if (N % 128 == 0 && mt * (N / 128) >= sms)
-    return launch_gemm<T, 128, AMN, BMN, EPI, SPLIT>(A, B, M, N, K, a_row0, ep, st);
-  if (N % 64 == 0) return launch_gemm<T, 64, AMN, BMN, EPI, SPLIT>(A, B, M, N, K, a_row0, ep, st);
+  if constexpr (SPLIT) {
+    // fp32 mode: chunked round-to-nearest accumulation (8 K-iterations per
+    // TMEM chunk) to bound the tensor-core truncation bias; BN <= 128.
+    constexpr int kChunk = 8;
+    if (N % 128 == 0 && mt * (N / 128) >= sms)
+      return launch_gemm<T, 128, AMN, BMN, EPI, SPLIT, kChunk>(A, B, M, N, K, a_row0, ep, st);
+    if (N % 64 == 0)
+      return launch_gemm<T, 64, AMN, BMN, EPI, SPLIT, kChunk>(A, B, M, N, K, a_row0, ep, st);
+  } else {
+    if (N % 256 == 0 && mt * (N / 256) >= sms)
+      return launch_gemm<T, 256, AMN, BMN, EPI, SPLIT, 0>(A, B, M, N, K, a_row0, ep, st);
+    if (N % 128 == 0 && mt * (N / 128) >= sms)
+      return launch_gemm<T, 128, AMN, BMN, EPI, SPLIT, 0>(A, B, M, N, K, a_row0, ep, st);
+    if (N % 64 == 0)
+      return launch_gemm<T, 64, AMN, BMN, EPI, SPLIT, 0>(A, B, M, N, K, a_row0, ep, st);
+  }
   return set_err(FI_ERR_ARG, "GEMM N=%d must be a multiple of 64", N);
 }
 
@@ -291,19 +354,24 @@ int forward_impl(const Plan& p, const float* L, const float* R, const float* roo
   float* A = at<float>(ws, p.a);
   float* Bc = at<float>(ws, p.b);
   float* O = p.store_o ? at<float>(ws, p.o) : nullptr;
-  float* X = at<float>(ws, p.x);
+  double* X = at<double>(ws, p.x);
   float* TOP = at<float>(ws, p.top);
+  float* TOPZ = at<float>(ws, p.topz);
 
   {  // K1: exp of the child tables, once per call
+    ProfScope prof(FI_PROF_PREP, st);
     dim3 grid((p.Np + p.Pp + 255) / 256, 2 * p.Np);
     k_prep_weights<T><<<grid, 256, 0, st>>>(L, R, wnn, wnp, p.N, p.P, p.Np, p.Pp, p.wnn_lo,
                                             p.wnp_lo);
     ++g_launches;
     FI_CUDA(cudaGetLastError());
   }
+  {
+  ProfScope prof(FI_PROF_PREP, st);
   k_prep_width1<T><<<p.B * p.l, 256, 0, st>>>(unary, lengths, e1, X, p.l, p.P, p.Pp, p.e1_lo);
   ++g_launches;
   FI_CUDA(cudaGetLastError());
+  }
 
   const Operand opWnn{wnn, p.Np, 2LL * p.Np, p.Np, false, p.wnn_lo};
   const Operand opWnp{wnp, p.Pp, 2LL * p.Np, p.Pp, false, p.wnp_lo};
@@ -329,6 +397,7 @@ int forward_impl(const Plan& p, const float* L, const float* R, const float* roo
     sa.e_lo = p.eall_lo;
     sa.X = X;
     sa.TOP = TOP;
+    sa.TOPZ = TOPZ;
     sa.logZ = logZ;
     sa.root = root;
     sa.lengths = lengths;
@@ -339,10 +408,13 @@ int forward_impl(const Plan& p, const float* L, const float* R, const float* roo
     sa.w = w;
     sa.cols_per_cta = p.cols_per_cta;
     const dim3 grid(p.clusters, p.B * n_w);
-    if (p.v == 1)
-      FI_TRY(launch_cluster(k_split_fwd<T, 1>, p.clusters, grid, dim3(p.threads), st, sa));
-    else
-      FI_TRY(launch_cluster(k_split_fwd<T, 2>, p.clusters, grid, dim3(p.threads), st, sa));
+    {
+      ProfScope prof(FI_PROF_SPLIT, st);
+      if (p.v == 1)
+        FI_TRY(launch_cluster(k_split_fwd<T, 1>, p.clusters, grid, dim3(p.threads), st, sa));
+      else
+        FI_TRY(launch_cluster(k_split_fwd<T, 2>, p.clusters, grid, dim3(p.threads), st, sa));
+    }
     if (w < p.l) {
       ep.M = p.B * n_w;
       ep.row0 = rowbase(w, p.B, p.l);
@@ -366,15 +438,20 @@ int backward_impl(const Plan& p, const float* L, const float* R, const float* ro
   float* A = at<float>(ws, p.a);
   float* Bc = at<float>(ws, p.b);
   float* LQ = at<float>(ws, p.lq);
-  float* X = at<float>(ws, p.x);
+  double* X = at<double>(ws, p.x);
   float* TOP = at<float>(ws, p.top);
+  float* TOPZ = at<float>(ws, p.topz);
   int* flag = at<int>(ws, p.flag);
 
   FI_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
-  k_seed_bwd<<<(p.Np + 255) / 256, 256, 0, st>>>(root, TOP, logZ, g, lengths, LQ, droot, flag,
+  {
+  ProfScope prof(FI_PROF_SEED, st);
+  (void)logZ;  // the fp64-consistent log2 Z - x† (TOPZ) is used instead
+  k_seed_bwd<<<(p.Np + 255) / 256, 256, 0, st>>>(root, TOP, TOPZ, g, lengths, LQ, droot, flag,
                                                  p.B, p.l, p.N, p.Np);
   ++g_launches;
   FI_CUDA(cudaGetLastError());
+  }
 
   const Operand opWnnMN{wnn, p.Np, 2LL * p.Np, p.Np, true, p.wnn_lo};  // K = 2Np, N = Np
   const Operand opWnpMN{wnp, p.Pp, 2LL * p.Np, p.Pp, true, p.wnp_lo};
@@ -397,10 +474,13 @@ int backward_impl(const Plan& p, const float* L, const float* R, const float* ro
     ga.m = m;
     ga.cols_per_cta = p.cols_per_cta;
     const dim3 grid(p.clusters, p.B * n_m);
-    if (p.v == 1)
-      k_gather_bwd<T, 1><<<grid, p.threads, 0, st>>>(ga);
-    else
-      k_gather_bwd<T, 2><<<grid, p.threads, 0, st>>>(ga);
+    {
+      ProfScope prof(FI_PROF_GATHER, st);
+      if (p.v == 1)
+        k_gather_bwd<T, 1><<<grid, p.threads, 0, st>>>(ga);
+      else
+        k_gather_bwd<T, 2><<<grid, p.threads, 0, st>>>(ga);
+    }
     ++g_launches;
     FI_CUDA(cudaGetLastError());
 
@@ -491,7 +571,6 @@ int fi_get_chart_layout(const fi_shape* shape, fi_chart_layout* out) {
 int fi_inside_forward(const fi_shape* shape, const float* L, const float* R, const float* root,
                       const float* unary, const int32_t* lengths, float* log_z, void* ws,
                       void* stream) {
-  g_launches = 0;
   Plan p;
   FI_TRY(make_plan(shape, &p));
   FI_TRY(check_ptrs({L, R, root, unary, lengths, log_z, ws}));
@@ -505,7 +584,6 @@ int fi_inside_backward(const fi_shape* shape, const float* L, const float* R, co
                        const float* unary, const int32_t* lengths, const float* log_z,
                        const float* grad_log_z, float* dL, float* dR, float* droot,
                        float* dunary, void* ws, void* stream) {
-  g_launches = 0;
   Plan p;
   FI_TRY(make_plan(shape, &p));
   FI_TRY(check_ptrs({L, R, root, unary, lengths, log_z, grad_log_z, dL, dR, droot, dunary, ws}));
@@ -561,7 +639,32 @@ int fi_test_gemm(int32_t dtype, int32_t a_mn, int32_t b_mn, int32_t M, int32_t N
   return set_err(FI_ERR_ARG, "unsupported majorness combination (A MN-major needs B MN-major)");
 }
 
-int32_t fi_last_launch_count(void) { return g_launches; }
+int64_t fi_launch_count(void) { return g_launches.load(); }
+
+void fi_profile_enable(int32_t on) { g_prof_on = on != 0; }
+
+int fi_profile_collect(float* ms, int32_t* counts, int32_t n) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (int c = 0; c < n; ++c) {
+    if (ms) ms[c] = 0.f;
+    if (counts) counts[c] = 0;
+  }
+  int rc = FI_OK;
+  for (const ProfRec& r : g_prof) {
+    float t = 0.f;
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&t, r.a, r.b);
+    if (e != cudaSuccess) rc = set_err(FI_ERR_CUDA, "profile event: %s", cudaGetErrorString(e));
+    if (r.cls >= 0 && r.cls < n) {
+      if (ms) ms[r.cls] += t;
+      if (counts) counts[r.cls] += 1;
+    }
+    g_prof_pool.push_back(r.a);
+    g_prof_pool.push_back(r.b);
+  }
+  g_prof.clear();
+  return rc;
+}
 const char* fi_last_error(void) { return g_err; }
 int32_t fi_version(void) { return 1; }
 

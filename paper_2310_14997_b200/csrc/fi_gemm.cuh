@@ -18,10 +18,12 @@
 
 namespace fi {
 
+// All log values are base 2 and stored as fp32 offsets from the span row's
+// fp64 shift x† (see fi_kernels.cuh), so the epilogues below need no x†.
 enum EpiMode : int {
-  EPI_FWD = 0,     // [a | b] = x + log(acc)                      (inside.py:203-213)
-  EPI_DGRAD = 1,   // lq = log|acc| - x  (= log|go| - o)           (inside.py:433-447)
-  EPI_DUNARY = 2,  // dunary = acc * exp(unary - x)  (width-1 go)  (inside.py:420-423)
+  EPI_FWD = 0,     // [a | b] - x† = log2(acc)                     (inside.py:203-213)
+  EPI_DGRAD = 1,   // LQ^ = log2|acc| (= log2|go| - o + x†)        (inside.py:433-447)
+  EPI_DUNARY = 2,  // dunary = acc * exp(unary - x†) (width-1 go)  (inside.py:420-423)
   EPI_WGRAD = 3,   // d{L,R} = exp({L,R}) * acc                    (inside.py:446)
   EPI_STORE = 4,   // plain C = acc (GEMM unit tests)
 };
@@ -35,7 +37,7 @@ struct GemmShape {
 struct GemmEpi {
   int M;              // valid output rows
   long long row0;     // global chart row of output row 0 (X / chart indexing)
-  const float* X;     // per-row log shift x† (indexed by global row)
+  const double* X;    // per-row log2 shift x† (indexed by global row)
   // EPI_FWD
   float* outA;
   float* outB;
@@ -91,10 +93,10 @@ __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int lrow, long long
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       float4 o;
-      o.x = xv + __logf(v[4 * q + 0]);
-      o.y = xv + __logf(v[4 * q + 1]);
-      o.z = xv + __logf(v[4 * q + 2]);
-      o.w = xv + __logf(v[4 * q + 3]);
+      o.x = lg2(v[4 * q + 0]);
+      o.y = lg2(v[4 * q + 1]);
+      o.z = lg2(v[4 * q + 2]);
+      o.w = lg2(v[4 * q + 3]);
       dst[q] = o;
     }
   } else if constexpr (EPI == EPI_DGRAD) {
@@ -102,23 +104,23 @@ __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int lrow, long long
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       float4 o;
-      o.x = __logf(fabsf(v[4 * q + 0])) - xv;
-      o.y = __logf(fabsf(v[4 * q + 1])) - xv;
-      o.z = __logf(fabsf(v[4 * q + 2])) - xv;
-      o.w = __logf(fabsf(v[4 * q + 3])) - xv;
+      o.x = lg2(fabsf(v[4 * q + 0]));
+      o.y = lg2(fabsf(v[4 * q + 1]));
+      o.z = lg2(fabsf(v[4 * q + 2]));
+      o.w = lg2(fabsf(v[4 * q + 3]));
       dst[q] = o;
     }
   } else if constexpr (EPI == EPI_DUNARY) {
     // rowptr = dunary row, aux = 1 if the token position is inside the sentence
     const float* un = ep.unary + static_cast<long long>(lrow) * ep.P;
-#pragma unroll 8
+#pragma unroll
     for (int t = 0; t < 32; ++t) {
       int c = col + t;
-      if (c < ep.P) rowptr[c] = aux ? v[t] * __expf(un[c] - xv) : 0.f;
+      if (c < ep.P) rowptr[c] = aux ? v[t] * ex2(fmaf(un[c], 1.4426950408889634f, -xv)) : 0.f;
     }
   } else if constexpr (EPI == EPI_WGRAD) {
     // rowptr = d{L,R} row start; aux selects the right table; lrow = table row
-#pragma unroll 8
+#pragma unroll
     for (int t = 0; t < 32; ++t) {
       int c = col + t;
       if (c < ep.valid_cols) {
@@ -135,8 +137,16 @@ __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int lrow, long long
 
 // SPLIT (fp32 mode, bf16x3): each operand is stored as hi + lo bf16 planes
 // (x = hi + lo to ~2^-17 relative) and the K loop runs three passes,
-// hi*hi + lo*hi + hi*lo, accumulating into the same TMEM tile.
-template <typename T, int BN, bool A_MN, bool B_MN, int EPI, bool SPLIT>
+// lo*hi, hi*lo, then hi*hi (small terms first), into the same accumulator.
+//
+// CHUNK > 0: the tensor core accumulates in fp32 with truncation, a
+// downward bias that grows with the number of MMA steps into one
+// accumulator (~1.5e-5 relative at K = 8192) and compounds through the 40
+// levels of the outside pass.  With CHUNK, every CHUNK K-iterations the
+// accumulator is handed to the epilogue warps, which add it into a
+// round-to-nearest fp32 register sum and hand it back (double-buffered), so
+// the bias is bounded by the chunk length whatever K is.  Requires BN <= 128.
+template <typename T, int BN, bool A_MN, bool B_MN, int EPI, bool SPLIT, int CHUNK>
 __global__ void __launch_bounds__(256, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
@@ -192,8 +202,8 @@ __global__ void __launch_bounds__(256, 1)
         for (int it = 0; it < k_iters; ++it) {
           const int pass = SPLIT ? it / sh.num_k : 0;
           const int kb = SPLIT ? it - pass * sh.num_k : it;
-          const CUtensorMap* ma = (SPLIT && pass == 1) ? &tmA2 : &tmA;
-          const CUtensorMap* mb = (SPLIT && pass == 2) ? &tmB2 : &tmB;
+          const CUtensorMap* ma = (SPLIT && pass == 0) ? &tmA2 : &tmA;
+          const CUtensorMap* mb = (SPLIT && pass == 1) ? &tmB2 : &tmB;
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], C::STAGE_BYTES);
           uint8_t* a_dst = smA + stage * C::A_BYTES;
@@ -238,11 +248,16 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      const int cl = CHUNK > 0 ? CHUNK : k_iters;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+        uint32_t d_tmem = tmem_base;
         for (int kb = 0; kb < k_iters; ++kb) {
+          const int kc = kb % cl;
+          if (kc == 0) {  // start a chunk in a drained accumulator
+            mbar_wait(&tempty[acc], acc_phase ^ 1);
+            tc_fence_after();
+            d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+          }
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_base = smem_u32(smA + stage * C::A_BYTES);
@@ -251,17 +266,19 @@ __global__ void __launch_bounds__(256, 1)
           for (int k = 0; k < C::BK / C::UK; ++k) {
             uint64_t ad = make_sdesc(a_base + k * a_kstep, a_lbo, a_sbo, a_lay);
             uint64_t bd = make_sdesc(b_base + k * b_kstep, b_lbo, b_sbo, b_lay);
-            umma<C::TF32>(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+            umma<C::TF32>(d_tmem, ad, bd, idesc, (kc | k) != 0 ? 1u : 0u);
           }
           umma_commit(&empty[stage]);
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
+          if (kc == cl - 1 || kb == k_iters - 1) {
+            umma_commit(&tfull[acc]);
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+          }
         }
-        umma_commit(&tfull[acc]);
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
       }
     }
   } else if (warp >= 4) {
@@ -282,7 +299,6 @@ __global__ void __launch_bounds__(256, 1)
       int col_base = n_blk * BN;
       if (row_ok) {
         if constexpr (EPI == EPI_FWD) {
-          xv = ep.X[grow];
           if (col_base < ep.Np) {
             rowptr = ep.outA + grow * ep.Np;
           } else {
@@ -290,10 +306,9 @@ __global__ void __launch_bounds__(256, 1)
             col_base -= ep.Np;
           }
         } else if constexpr (EPI == EPI_DGRAD) {
-          xv = ep.X[grow];
           rowptr = ep.LQ + grow * ep.Np;
         } else if constexpr (EPI == EPI_DUNARY) {
-          xv = ep.X[grow];
+          xv = static_cast<float>(ep.X[grow]);
           const int b = lrow / ep.lmax, i = lrow % ep.lmax;
           aux = i < ep.lengths[b];
           rowptr = ep.dunary + static_cast<long long>(lrow) * ep.P;
@@ -314,26 +329,52 @@ __global__ void __launch_bounds__(256, 1)
           if (i == 0 && ep.lengths[b] == ep.width) ok = false;
         }
       }
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
-                             static_cast<uint32_t>(acc * BN);
+      const int erow = (EPI == EPI_WGRAD && aux) ? lrow - ep.Np : lrow;
+      const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
+      if constexpr (CHUNK == 0) {
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        const uint32_t t_row = t_lane + static_cast<uint32_t>(acc * BN);
 #pragma unroll 1
-      for (int j = 0; j < BN / 32; ++j) {
-        float v[32];
-        tmem_ld32(t_row + j * 32, v);
-        if constexpr (EPI == EPI_WGRAD) {
-          const int arow = aux ? lrow - ep.Np : lrow;
-          epi_chunk<EPI>(ep, arow, grow, col_base + j * 32, v, xv, ok, rowptr, aux);
-        } else {
-          epi_chunk<EPI>(ep, lrow, grow, col_base + j * 32, v, xv, ok, rowptr, aux);
+        for (int j = 0; j < BN / 32; ++j) {
+          float v[32];
+          tmem_ld32(t_row + j * 32, v);
+          epi_chunk<EPI>(ep, erow, grow, col_base + j * 32, v, xv, ok, rowptr, aux);
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      } else {
+        static_assert(BN <= 128, "chunked accumulation keeps BN fp32 sums per thread");
+        float sum[BN / 32][32];
+#pragma unroll
+        for (int j = 0; j < BN / 32; ++j)
+#pragma unroll
+          for (int t = 0; t < 32; ++t) sum[j][t] = 0.f;
+        const int nchunks = (k_iters + CHUNK - 1) / CHUNK;
+        for (int c = 0; c < nchunks; ++c) {
+          mbar_wait(&tfull[acc], acc_phase);
+          tc_fence_after();
+          const uint32_t t_row = t_lane + static_cast<uint32_t>(acc * BN);
+#pragma unroll
+          for (int j = 0; j < BN / 32; ++j) {
+            float v[32];
+            tmem_ld32(t_row + j * 32, v);
+#pragma unroll
+            for (int t = 0; t < 32; ++t) sum[j][t] += v[t];
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+          acc ^= 1;
+          if (acc == 0) acc_phase ^= 1;
+        }
+#pragma unroll
+        for (int j = 0; j < BN / 32; ++j)
+          epi_chunk<EPI>(ep, erow, grow, col_base + j * 32, sum[j], xv, ok, rowptr, aux);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
     }
   }
 

@@ -2,18 +2,25 @@
 // width-1 preparation, the split-point contraction (forward), the seed of
 // the outside pass, and the gather-form split backward.
 //
-// Chart layout in HBM (all fp32 unless noted), one row per span:
+// Chart layout in HBM, one row per span:
 //   n_w        = lmax - w + 1                    spans of width w per sentence
 //   rowbase(w) = B * sum_{v<w} n_v               first row of width w
 //   row(w,b,i) = rowbase(w) + b * n_w + i        span (i, i+w) of sentence b
-// Every chart array has row stride Np (nonterminals padded to a multiple of
-// 256 with -inf / zero-probability dummy symbols).  The arrays are
-//   A, Bc  : left/right projections a[w], b[w]            (inside.py:66-84)
-//   O      : inside scores o[w] over nonterminals (optional; parity/marginals)
-//   X      : per-span shift x† = max_s o[w][i, s]          (inside.py:205-206)
-//   E      : exp(o - x†) in the GEMM operand type (bf16 or tf32)
-//   LQ     : log|go| - o, the outside weight in log space (backward only)
-//   G      : [ga·exp(x†-a) | gb·exp(x†-b)] per span, 2*Np wide (backward)
+// Every per-symbol array has row stride Np (nonterminals padded to a multiple
+// of 256 with -inf / zero-probability dummy symbols).
+//
+// Numerics: all log values are base 2 (log2 = ln * log2(e)), so every
+// exp/log is one MUFU op, and every span row carries its large magnitude in
+// ONE fp64 scalar X[row] = x†, the row max of the inside score
+// (inside.py:205-206).  Per-symbol arrays hold small fp32 offsets from it:
+//   A^, B^ : a[w] - x†, b[w] - x†   = log2(E W^T)       (inside.py:203-213)
+//   O^     : o[w] - x† <= 0          (optional: chart export / marginals)
+//   E      : exp2(O^) in the GEMM operand type (bf16, tf32, or bf16 hi+lo)
+//   LQ^    : log2|go| - o + x†  = log2|G W|  (outside weight, backward)
+//   G      : [ga*exp(x†-a) | gb*exp(x†-b)] per span, 2*Np wide (backward)
+// Sums such as a[m][i] + b[w-m][i+m] - o[w][i] are then formed as
+// (fp64 scalar difference, rounded once) + (two O(10) fp32 offsets), so no
+// fp32 operation ever cancels two O(100) log values.
 #pragma once
 #include <cooperative_groups.h>
 #include "fi_ptx.cuh"
@@ -24,6 +31,9 @@ namespace fi {
 
 constexpr float kNegInf = -__builtin_huge_valf();
 constexpr float kLowInit = -1.0e30f;  // finite "minus infinity" for online LSE
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr double kLn2d = 0.6931471805599453;
+
 
 __host__ __device__ __forceinline__ long long rowbase(int w, int B, int lmax) {
   const long long k = w - 1;
@@ -142,7 +152,7 @@ __device__ __forceinline__ float cluster_reduce(float v, float* slot, float* bca
 
 // ---------------------------------------------------------------------------
 // K1: W_NN = exp([L_NN ; R_NN]) (2Np x Np), W_NP = exp([L_NP ; R_NP]) (2Np x Pp).
-// Once per step, not per sentence (inside.py:194-200 recomputes it per call).
+// Once per call, not per sentence (inside.py:194-200 recomputes it per call).
 // ---------------------------------------------------------------------------
 template <typename T>
 __global__ void k_prep_weights(const float* __restrict__ L, const float* __restrict__ R,
@@ -167,12 +177,12 @@ __global__ void k_prep_weights(const float* __restrict__ L, const float* __restr
 
 // ---------------------------------------------------------------------------
 // Width 1: o[1] = unary (inside.py:296-298); x† = max; E1 = exp(unary - x†).
-// One CTA per (sentence, position).  Padded positions get E1 = 0.
+// One CTA per (sentence, position).  Padded positions get E1 = 0, x† = 0.
 // ---------------------------------------------------------------------------
 template <typename T>
 __global__ void __launch_bounds__(256) k_prep_width1(const float* __restrict__ unary,
                                                      const int* __restrict__ lengths,
-                                                     T* __restrict__ e1, float* __restrict__ X,
+                                                     T* __restrict__ e1, double* __restrict__ X,
                                                      int lmax, int P, int Pp, long long e1_lo) {
   __shared__ float red[33];
   const int r = blockIdx.x;  // = b * lmax + i = chart_row(1, b, i)
@@ -181,12 +191,12 @@ __global__ void __launch_bounds__(256) k_prep_width1(const float* __restrict__ u
   const float* u = unary + static_cast<long long>(r) * P;
   float mx = kNegInf;
   if (ok)
-    for (int t = threadIdx.x; t < P; t += blockDim.x) mx = fmaxf(mx, u[t]);
+    for (int t = threadIdx.x; t < P; t += blockDim.x) mx = fmaxf(mx, u[t] * kLog2e);
   mx = block_reduce<true>(mx, red);
   const float xs = (mx == kNegInf) ? 0.f : mx;
   T* dst = e1 + static_cast<long long>(r) * Pp;
   for (int t = threadIdx.x; t < Pp; t += blockDim.x)
-    store1s<T>(dst + t, e1_lo, (ok && t < P) ? __expf(u[t] - xs) : 0.f);
+    store1s<T>(dst + t, e1_lo, (ok && t < P) ? ex2(fmaf(u[t], kLog2e, -xs)) : 0.f);
   if (threadIdx.x == 0) X[r] = xs;
 }
 
@@ -194,19 +204,20 @@ __global__ void __launch_bounds__(256) k_prep_width1(const float* __restrict__ u
 // K4/K5: split-point contraction for width w (inside.py:313-332) + logZ
 // (inside.py:124-129).  One cluster of C CTAs per span row; each CTA owns a
 // contiguous chunk of Np/C nonterminal columns, each thread V float4s of it.
-// Online log-sum-exp over the w-1 split points with one exp per element;
+// Online log-sum-exp over the w-1 split points with one exp2 per element;
 // the row max x† is reduced across the cluster through DSMEM, then E is
 // written in the GEMM operand type.  No (w-1, n, N) stack is materialised.
 // ---------------------------------------------------------------------------
 struct SplitArgs {
-  const float* A;
-  const float* Bc;
-  float* O;        // nullable
-  void* E;         // T*, row stride Np (nullable at w == lmax)
-  long long e_lo;  // element offset of the lo plane (fp32 mode), else 0
-  float* X;
-  float* TOP;      // B x Np : root + o at the top span (for d_root)
-  float* logZ;
+  const float* A;    // A^
+  const float* Bc;   // B^
+  float* O;          // O^ (nullable)
+  void* E;           // T*, row stride Np (nullable at w == lmax)
+  long long e_lo;    // element offset of the lo plane (fp32 mode), else 0
+  double* X;
+  float* TOP;        // B x Np : log2 root + O^ at the top span (for d_root)
+  float* TOPZ;       // B      : log2 Z - x†_top
+  float* logZ;       // B      : natural-log partition (output)
   const float* root;
   const int* lengths;
   int B, lmax, N, Np, w, cols_per_cta;
@@ -214,7 +225,7 @@ struct SplitArgs {
 
 __device__ __forceinline__ void lse_push(float& M, float& S, float v) {
   const float d = v - M;
-  const float e = __expf(-fabsf(d));  // d = -inf -> 0
+  const float e = ex2(-fabsf(d));  // d = -inf -> 0
   const bool gt = d > 0.f;
   S = gt ? fmaf(S, e, 1.f) : S + e;
   M = gt ? v : M;
@@ -234,6 +245,12 @@ __global__ void __launch_bounds__(256) k_split_fwd(SplitArgs a) {
   const int col0 = blockIdx.x * a.cols_per_cta + threadIdx.x * 4;
   T* E = reinterpret_cast<T*>(a.E);
 
+  // split m of span (i, i+w) pairs a[m][i] with b[w-m][i+m]   (inside.py:317-319)
+  // row(m, b, i) advances by B*n_m; row(w-m, b, i+m) retreats by B*n_{w-m+1} - 1
+  long long ra = chart_row(1, b, i, a.B, a.lmax);
+  long long rb = chart_row(w - 1, b, i + 1, a.B, a.lmax);
+  const double ref = a.X[ra] + a.X[rb];  // c_1: the row's reference offset
+
   if (i + w > len) {  // span outside the sentence: never feeds a valid span
 #pragma unroll
     for (int v = 0; v < V; ++v) {
@@ -242,7 +259,7 @@ __global__ void __launch_bounds__(256) k_split_fwd(SplitArgs a) {
           make_float4(kNegInf, kNegInf, kNegInf, kNegInf);
       if (E) store4s<T>(E + row * a.Np + c, a.e_lo, 0.f, 0.f, 0.f, 0.f);
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.X[row] = 0.f;
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.X[row] = ref;
     return;  // uniform across the cluster (same row)
   }
 
@@ -252,15 +269,18 @@ __global__ void __launch_bounds__(256) k_split_fwd(SplitArgs a) {
     M[k] = kLowInit;
     S[k] = 0.f;
   }
-  // split m of span (i, i+w) pairs a[m][i] with b[w-m][i+m]   (inside.py:317-319)
   int m = 1;
   for (; m + 3 < w; m += 4) {
     float4 va[4][V], vb[4][V];
+    float dl[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int mm = m + u;
-      const float* pa = a.A + chart_row(mm, b, i, a.B, a.lmax) * a.Np;
-      const float* pb = a.Bc + chart_row(w - mm, b, i + mm, a.B, a.lmax) * a.Np;
+      const long long r1 = chart_row(mm, b, i, a.B, a.lmax);
+      const long long r2 = chart_row(w - mm, b, i + mm, a.B, a.lmax);
+      dl[u] = static_cast<float>(__ldg(a.X + r1) + __ldg(a.X + r2) - ref);
+      const float* pa = a.A + r1 * a.Np;
+      const float* pb = a.Bc + r2 * a.Np;
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         va[u][v] = ldg4(pa + col0 + v * nthr * 4);
@@ -271,49 +291,55 @@ __global__ void __launch_bounds__(256) k_split_fwd(SplitArgs a) {
     for (int u = 0; u < 4; ++u)
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        lse_push(M[4 * v + 0], S[4 * v + 0], va[u][v].x + vb[u][v].x);
-        lse_push(M[4 * v + 1], S[4 * v + 1], va[u][v].y + vb[u][v].y);
-        lse_push(M[4 * v + 2], S[4 * v + 2], va[u][v].z + vb[u][v].z);
-        lse_push(M[4 * v + 3], S[4 * v + 3], va[u][v].w + vb[u][v].w);
+        lse_push(M[4 * v + 0], S[4 * v + 0], va[u][v].x + vb[u][v].x + dl[u]);
+        lse_push(M[4 * v + 1], S[4 * v + 1], va[u][v].y + vb[u][v].y + dl[u]);
+        lse_push(M[4 * v + 2], S[4 * v + 2], va[u][v].z + vb[u][v].z + dl[u]);
+        lse_push(M[4 * v + 3], S[4 * v + 3], va[u][v].w + vb[u][v].w + dl[u]);
       }
   }
   for (; m < w; ++m) {
-    const float* pa = a.A + chart_row(m, b, i, a.B, a.lmax) * a.Np;
-    const float* pb = a.Bc + chart_row(w - m, b, i + m, a.B, a.lmax) * a.Np;
+    const long long r1 = chart_row(m, b, i, a.B, a.lmax);
+    const long long r2 = chart_row(w - m, b, i + m, a.B, a.lmax);
+    const float dl = static_cast<float>(__ldg(a.X + r1) + __ldg(a.X + r2) - ref);
+    const float* pa = a.A + r1 * a.Np;
+    const float* pb = a.Bc + r2 * a.Np;
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       float4 x = ldg4(pa + col0 + v * nthr * 4);
       float4 y = ldg4(pb + col0 + v * nthr * 4);
-      lse_push(M[4 * v + 0], S[4 * v + 0], x.x + y.x);
-      lse_push(M[4 * v + 1], S[4 * v + 1], x.y + y.y);
-      lse_push(M[4 * v + 2], S[4 * v + 2], x.z + y.z);
-      lse_push(M[4 * v + 3], S[4 * v + 3], x.w + y.w);
+      lse_push(M[4 * v + 0], S[4 * v + 0], x.x + y.x + dl);
+      lse_push(M[4 * v + 1], S[4 * v + 1], x.y + y.y + dl);
+      lse_push(M[4 * v + 2], S[4 * v + 2], x.z + y.z + dl);
+      lse_push(M[4 * v + 3], S[4 * v + 3], x.w + y.w + dl);
     }
   }
-  float o[4 * V];
+  float o[4 * V];  // o - ref
   float mx = kNegInf;
 #pragma unroll
   for (int k = 0; k < 4 * V; ++k) {
-    o[k] = S[k] > 0.f ? M[k] + __logf(S[k]) : kNegInf;
+    o[k] = S[k] > 0.f ? M[k] + lg2(S[k]) : kNegInf;
     mx = fmaxf(mx, o[k]);
   }
+  // row max over all Np columns: block, then cluster (DSMEM)
+  mx = block_reduce<true>(mx, red);
+  mx = cluster_reduce<true>(mx, &cl_slot, &cl_bcast);
+  const float xs = (mx == kNegInf) ? 0.f : mx;  // inside.py:324-326
+#pragma unroll
+  for (int k = 0; k < 4 * V; ++k) o[k] -= xs;    // O^ = o - x†  (<= 0)
   if (a.O) {
 #pragma unroll
     for (int v = 0; v < V; ++v)
       *reinterpret_cast<float4*>(a.O + row * a.Np + col0 + v * nthr * 4) =
           make_float4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
   }
-  // row max over all Np columns: block, then cluster (DSMEM)
-  mx = block_reduce<true>(mx, red);
-  mx = cluster_reduce<true>(mx, &cl_slot, &cl_bcast);
-  const float xs = (mx == kNegInf) ? 0.f : mx;  // inside.py:324-326
   if (E) {
 #pragma unroll
     for (int v = 0; v < V; ++v)
-      store4s<T>(E + row * a.Np + col0 + v * nthr * 4, a.e_lo, __expf(o[4 * v] - xs),
-                __expf(o[4 * v + 1] - xs), __expf(o[4 * v + 2] - xs), __expf(o[4 * v + 3] - xs));
+      store4s<T>(E + row * a.Np + col0 + v * nthr * 4, a.e_lo, ex2(o[4 * v]), ex2(o[4 * v + 1]),
+                 ex2(o[4 * v + 2]), ex2(o[4 * v + 3]));
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) a.X[row] = xs;
+  const double xrow = ref + static_cast<double>(xs);
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.X[row] = xrow;
 
   if (i == 0 && w == len) {  // top span: logZ = LSE_A(root[A] + o[A])  (inside.py:124-129)
     float sc[4 * V];
@@ -323,7 +349,7 @@ __global__ void __launch_bounds__(256) k_split_fwd(SplitArgs a) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int c = col0 + v * nthr * 4 + k;
-        sc[4 * v + k] = c < a.N ? a.root[c] + o[4 * v + k] : kNegInf;
+        sc[4 * v + k] = c < a.N ? fmaf(a.root[c], kLog2e, o[4 * v + k]) : kNegInf;
         a.TOP[static_cast<long long>(b) * a.Np + c] = sc[4 * v + k];
         smx = fmaxf(smx, sc[4 * v + k]);
       }
@@ -332,23 +358,27 @@ __global__ void __launch_bounds__(256) k_split_fwd(SplitArgs a) {
     float s = 0.f;
     if (smx != kNegInf) {
 #pragma unroll
-      for (int k = 0; k < 4 * V; ++k) s += expf(sc[k] - smx);
+      for (int k = 0; k < 4 * V; ++k) s += exp2f(sc[k] - smx);
     }
     s = block_reduce<false>(s, red);
     s = cluster_reduce<false>(s, &cl_slot, &cl_bcast);
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.logZ[b] = smx == kNegInf ? kNegInf : smx + logf(s);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      const float z = smx == kNegInf ? kNegInf : smx + log2f(s);  // log2 Z - x†
+      a.TOPZ[b] = z;
+      a.logZ[b] = z == kNegInf ? kNegInf : static_cast<float>((xrow + z) * kLn2d);
+    }
   }
 }
 
 // ---------------------------------------------------------------------------
 // Backward seed (inside.py:400-404): the root posterior
 //   post[A] = exp(root[A] + o[len][0, A] - logZ)
-// seeds the outside pass at each sentence's top span, stored in log form
-// lq = log|g·post| - o = root - logZ + log|g|, and is itself d_root.
-// One thread per nonterminal column; loops over sentences.
+// seeds the outside pass at each sentence's top span as
+//   LQ^ = log2|g post| - o + x† = log2 root - (log2 Z - x†) + log2|g|
+// and is itself d_root (times g).  One thread per column; loops sentences.
 // ---------------------------------------------------------------------------
 __global__ void k_seed_bwd(const float* __restrict__ root, const float* __restrict__ TOP,
-                           const float* __restrict__ logZ, const float* __restrict__ g,
+                           const float* __restrict__ TOPZ, const float* __restrict__ g,
                            const int* __restrict__ lengths, float* __restrict__ LQ,
                            float* __restrict__ droot, int* __restrict__ flag, int B, int lmax,
                            int N, int Np) {
@@ -356,14 +386,14 @@ __global__ void k_seed_bwd(const float* __restrict__ root, const float* __restri
   if (c >= Np) return;
   float acc = 0.f;
   for (int b = 0; b < B; ++b) {
-    const float lz = logZ[b];
+    const float z = TOPZ[b];
     const float gb = g[b];
-    const bool finite = isfinite(lz);
+    const bool finite = isfinite(z);
     if (!finite && c == 0) atomicOr(flag, 1);
     float lq = kNegInf;
     if (finite && gb != 0.f && c < N) {
-      lq = root[c] - lz + logf(fabsf(gb));
-      acc += gb * expf(TOP[static_cast<long long>(b) * Np + c] - lz);
+      lq = fmaf(root[c], kLog2e, -z) + log2f(fabsf(gb));
+      acc += gb * exp2f(TOP[static_cast<long long>(b) * Np + c] - z);
     }
     LQ[chart_row(lengths[b], b, 0, B, lmax) * Np + c] = lq;
   }
@@ -372,18 +402,21 @@ __global__ void k_seed_bwd(const float* __restrict__ root, const float* __restri
 
 // ---------------------------------------------------------------------------
 // K7: gather-form split backward for child width m (inside.py:406-417).
-// For span (i, i+m) of sentence b, with Q_w = log|go_w| - o_w (LQ):
-//   G_L = [a != -inf] * sum_{w>m}  exp(x†_m + b[w-m][i+m] + LQ[w][i])
-//   G_R = [b != -inf] * sum_{s<i}  exp(x†_m + a[i-s][s]   + LQ[i+m-s][s])
-// which equals ga·exp(x† - a) (resp. gb·exp(x† - b)) of the reference, the
-// row of the dgrad/wgrad GEMM operand; the a (resp. b) factor cancels.
+// For span (i, i+m) of sentence b (row r), with the outside weight
+// LQ = log2|go| - o of each parent:
+//   G_L = [a != -inf] * sum_{w>m}  2^(x†_r + b[w-m][i+m] + LQ[w][i])
+//   G_R = [b != -inf] * sum_{s<i}  2^(x†_r + a[i-s][s]   + LQ[i+m-s][s])
+// which is ga*exp(x† - a) (resp. gb*exp(x† - b)) of the reference -- the row
+// of the dgrad/wgrad GEMM operand -- because the a (resp. b) factor of the
+// split softmax exp(a + b - o) cancels against exp(-a).  With the shifted
+// storage each term is 2^(d + B^ + LQ^), d an fp64 per-term scalar.
 // Each accumulator is written once: deterministic, no atomics.
 // ---------------------------------------------------------------------------
 struct GatherArgs {
   const float* A;
   const float* Bc;
   const float* LQ;
-  const float* X;
+  const double* X;
   void* G;  // T*, row stride 2*Np
   long long g_lo;
   const int* lengths;
@@ -412,7 +445,7 @@ __global__ void __launch_bounds__(256) k_gather_bwd(GatherArgs a) {
     }
     return;
   }
-  const float xm = a.X[row];
+  const double xm = a.X[row];
   float gl[4 * V], gr[4 * V];
 #pragma unroll
   for (int k = 0; k < 4 * V; ++k) gl[k] = gr[k] = 0.f;
@@ -422,10 +455,14 @@ __global__ void __launch_bounds__(256) k_gather_bwd(GatherArgs a) {
   int w = m + 1;
   for (; w + 1 <= wmax; w += 2) {
     float4 vb[2][V], vq[2][V];
+    float d[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
-      const float* pb = a.Bc + chart_row(w + u - m, b, i + m, a.B, a.lmax) * a.Np;
-      const float* pq = a.LQ + chart_row(w + u, b, i, a.B, a.lmax) * a.Np;
+      const long long rs = chart_row(w + u - m, b, i + m, a.B, a.lmax);
+      const long long rp = chart_row(w + u, b, i, a.B, a.lmax);
+      d[u] = static_cast<float>(xm + __ldg(a.X + rs) - __ldg(a.X + rp));
+      const float* pb = a.Bc + rs * a.Np;
+      const float* pq = a.LQ + rp * a.Np;
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         vb[u][v] = ldg4(pb + col0 + v * nthr * 4);
@@ -436,34 +473,41 @@ __global__ void __launch_bounds__(256) k_gather_bwd(GatherArgs a) {
     for (int u = 0; u < 2; ++u)
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        gl[4 * v + 0] += __expf(xm + vb[u][v].x + vq[u][v].x);
-        gl[4 * v + 1] += __expf(xm + vb[u][v].y + vq[u][v].y);
-        gl[4 * v + 2] += __expf(xm + vb[u][v].z + vq[u][v].z);
-        gl[4 * v + 3] += __expf(xm + vb[u][v].w + vq[u][v].w);
+        gl[4 * v + 0] += ex2(vb[u][v].x + vq[u][v].x + d[u]);
+        gl[4 * v + 1] += ex2(vb[u][v].y + vq[u][v].y + d[u]);
+        gl[4 * v + 2] += ex2(vb[u][v].z + vq[u][v].z + d[u]);
+        gl[4 * v + 3] += ex2(vb[u][v].w + vq[u][v].w + d[u]);
       }
   }
   for (; w <= wmax; ++w) {
-    const float* pb = a.Bc + chart_row(w - m, b, i + m, a.B, a.lmax) * a.Np;
-    const float* pq = a.LQ + chart_row(w, b, i, a.B, a.lmax) * a.Np;
+    const long long rs = chart_row(w - m, b, i + m, a.B, a.lmax);
+    const long long rp = chart_row(w, b, i, a.B, a.lmax);
+    const float d = static_cast<float>(xm + __ldg(a.X + rs) - __ldg(a.X + rp));
+    const float* pb = a.Bc + rs * a.Np;
+    const float* pq = a.LQ + rp * a.Np;
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       float4 x = ldg4(pb + col0 + v * nthr * 4);
       float4 q = ldg4(pq + col0 + v * nthr * 4);
-      gl[4 * v + 0] += __expf(xm + x.x + q.x);
-      gl[4 * v + 1] += __expf(xm + x.y + q.y);
-      gl[4 * v + 2] += __expf(xm + x.z + q.z);
-      gl[4 * v + 3] += __expf(xm + x.w + q.w);
+      gl[4 * v + 0] += ex2(x.x + q.x + d);
+      gl[4 * v + 1] += ex2(x.y + q.y + d);
+      gl[4 * v + 2] += ex2(x.z + q.z + d);
+      gl[4 * v + 3] += ex2(x.w + q.w + d);
     }
   }
   // right child (i, i+m) of parent (s, i+m): left sibling a[i-s][s]
   int s = 0;
   for (; s + 1 < i; s += 2) {
     float4 va[2][V], vq[2][V];
+    float d[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int ss = s + u;
-      const float* pa = a.A + chart_row(i - ss, b, ss, a.B, a.lmax) * a.Np;
-      const float* pq = a.LQ + chart_row(i + m - ss, b, ss, a.B, a.lmax) * a.Np;
+      const long long rs = chart_row(i - ss, b, ss, a.B, a.lmax);
+      const long long rp = chart_row(i + m - ss, b, ss, a.B, a.lmax);
+      d[u] = static_cast<float>(xm + __ldg(a.X + rs) - __ldg(a.X + rp));
+      const float* pa = a.A + rs * a.Np;
+      const float* pq = a.LQ + rp * a.Np;
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         va[u][v] = ldg4(pa + col0 + v * nthr * 4);
@@ -474,23 +518,26 @@ __global__ void __launch_bounds__(256) k_gather_bwd(GatherArgs a) {
     for (int u = 0; u < 2; ++u)
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        gr[4 * v + 0] += __expf(xm + va[u][v].x + vq[u][v].x);
-        gr[4 * v + 1] += __expf(xm + va[u][v].y + vq[u][v].y);
-        gr[4 * v + 2] += __expf(xm + va[u][v].z + vq[u][v].z);
-        gr[4 * v + 3] += __expf(xm + va[u][v].w + vq[u][v].w);
+        gr[4 * v + 0] += ex2(va[u][v].x + vq[u][v].x + d[u]);
+        gr[4 * v + 1] += ex2(va[u][v].y + vq[u][v].y + d[u]);
+        gr[4 * v + 2] += ex2(va[u][v].z + vq[u][v].z + d[u]);
+        gr[4 * v + 3] += ex2(va[u][v].w + vq[u][v].w + d[u]);
       }
   }
   for (; s < i; ++s) {
-    const float* pa = a.A + chart_row(i - s, b, s, a.B, a.lmax) * a.Np;
-    const float* pq = a.LQ + chart_row(i + m - s, b, s, a.B, a.lmax) * a.Np;
+    const long long rs = chart_row(i - s, b, s, a.B, a.lmax);
+    const long long rp = chart_row(i + m - s, b, s, a.B, a.lmax);
+    const float d = static_cast<float>(xm + __ldg(a.X + rs) - __ldg(a.X + rp));
+    const float* pa = a.A + rs * a.Np;
+    const float* pq = a.LQ + rp * a.Np;
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       float4 x = ldg4(pa + col0 + v * nthr * 4);
       float4 q = ldg4(pq + col0 + v * nthr * 4);
-      gr[4 * v + 0] += __expf(xm + x.x + q.x);
-      gr[4 * v + 1] += __expf(xm + x.y + q.y);
-      gr[4 * v + 2] += __expf(xm + x.z + q.z);
-      gr[4 * v + 3] += __expf(xm + x.w + q.w);
+      gr[4 * v + 0] += ex2(x.x + q.x + d);
+      gr[4 * v + 1] += ex2(x.y + q.y + d);
+      gr[4 * v + 2] += ex2(x.z + q.z + d);
+      gr[4 * v + 3] += ex2(x.w + q.w + d);
     }
   }
   // zero-mass projections carry no gradient (inside.py:441-443 NaN guard)
@@ -502,31 +549,29 @@ __global__ void __launch_bounds__(256) k_gather_bwd(GatherArgs a) {
     const int c = col0 + v * nthr * 4;
     float4 am = ldg4(pam + c), bm = ldg4(pbm + c);
     store4s<T>(G + c, a.g_lo, am.x == kNegInf ? 0.f : sg * gl[4 * v + 0],
-              am.y == kNegInf ? 0.f : sg * gl[4 * v + 1], am.z == kNegInf ? 0.f : sg * gl[4 * v + 2],
-              am.w == kNegInf ? 0.f : sg * gl[4 * v + 3]);
+               am.y == kNegInf ? 0.f : sg * gl[4 * v + 1], am.z == kNegInf ? 0.f : sg * gl[4 * v + 2],
+               am.w == kNegInf ? 0.f : sg * gl[4 * v + 3]);
     store4s<T>(G + a.Np + c, a.g_lo, bm.x == kNegInf ? 0.f : sg * gr[4 * v + 0],
-              bm.y == kNegInf ? 0.f : sg * gr[4 * v + 1], bm.z == kNegInf ? 0.f : sg * gr[4 * v + 2],
-              bm.w == kNegInf ? 0.f : sg * gr[4 * v + 3]);
+               bm.y == kNegInf ? 0.f : sg * gr[4 * v + 1], bm.z == kNegInf ? 0.f : sg * gr[4 * v + 2],
+               bm.w == kNegInf ? 0.f : sg * gr[4 * v + 3]);
   }
 }
 
-// Span marginals mu_sym[w][i, A] = go / |g| = exp(LQ + o - log|g|)  (inside.py:425-430)
+// Span marginals mu_sym[w][i, A] = go / |g| = 2^(LQ^ + O^ - log2|g|)  (inside.py:425-430)
 __global__ void k_marginals(const float* __restrict__ LQ, const float* __restrict__ O,
                             const float* __restrict__ g, const int* __restrict__ lengths,
                             float* __restrict__ mu, int B, int lmax, int Np, int N) {
   const long long row = rowbase(2, B, lmax) + blockIdx.x;  // rows of widths >= 2
-  // recover (w, b, i) from the row index
-  long long r = row;
   int w = 2;
-  while (w < lmax && r >= rowbase(w + 1, B, lmax)) ++w;
+  while (w < lmax && row >= rowbase(w + 1, B, lmax)) ++w;
   const int n_w = lmax - w + 1;
-  const long long local = r - rowbase(w, B, lmax);
+  const long long local = row - rowbase(w, B, lmax);
   const int b = static_cast<int>(local / n_w), i = static_cast<int>(local % n_w);
   const bool ok = i + w <= lengths[b] && g[b] != 0.f;
-  const float lg = ok ? logf(fabsf(g[b])) : 0.f;
+  const float lg = ok ? log2f(fabsf(g[b])) : 0.f;
   for (int c = threadIdx.x; c < N; c += blockDim.x) {
     float v = 0.f;
-    if (ok) v = __expf(LQ[row * Np + c] + O[row * Np + c] - lg);
+    if (ok) v = exp2f(LQ[row * Np + c] + O[row * Np + c] - lg);
     mu[(row - rowbase(2, B, lmax)) * N + c] = v;
   }
 }

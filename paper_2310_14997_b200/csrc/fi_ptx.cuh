@@ -156,6 +156,17 @@ __host__ __device__ constexpr uint32_t make_idesc(int n, bool a_mn_major, bool b
 }
 
 // ------------------------------------------------------------ misc device
+__device__ __forceinline__ float ex2(float x) {  // 2^x, MUFU.EX2 (-inf -> 0; subnormals kept)
+  float y;
+  asm("ex2.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float lg2(float x) {  // log2 x, MUFU.LG2 (0 -> -inf)
+  float y;
+  asm("lg2.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ float4 ldg_nc_f4(const float* p) {
   float4 r;
   asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];"

@@ -112,6 +112,7 @@ def _setup_context(ctx, inputs, output):
     L, R, root, unary, lengths, gemm_dtype, store_chart = inputs
     log_z, ws = output
     ctx.save_for_backward(L, R, root, unary, lengths, log_z, ws)
+    ctx.set_materialize_grads(False)  # never zero-fill a grad for the workspace output
     ctx.gemm_dtype = gemm_dtype
     ctx.store_chart = store_chart
 

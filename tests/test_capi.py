@@ -1,0 +1,101 @@
+"""The C-ABI library: loads, exports every symbol include/flashinside.h
+declares, and its host-side planning/validation behaves without a GPU."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+from paper_2310_14997_b200 import _build, _lib
+
+HEADER = Path(__file__).resolve().parent.parent / "include" / "flashinside.h"
+
+
+def declared_functions():
+    text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    names = re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(fi_[a-z_0-9]+)\s*\(", text, re.M)
+    return sorted(set(names))
+
+
+def test_header_declares_the_engine_entry_points():
+    names = declared_functions()
+    for must in ("fi_workspace_bytes", "fi_inside_forward", "fi_inside_backward",
+                 "fi_marginals", "fi_last_error", "fi_get_chart_layout"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    for name in declared_functions():
+        assert hasattr(lib, name), f"{name} declared in flashinside.h but not exported"
+    # and the ctypes binding covers exactly the header
+    bound = {n for n, _, _ in _lib.SIGNATURES}
+    assert bound == set(declared_functions())
+
+
+def test_library_is_sm100a():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_build.LIB_PATH)],
+                         capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def rowbase(w, B, l):
+    return B * ((w - 1) * (l + 1) - (w - 1) * w // 2)
+
+
+@pytest.mark.parametrize("n,p,b,l,dt", [(4096, 4096, 64, 40, "bf16"), (1, 1, 1, 2, "fp32"),
+                                        (100, 60, 5, 9, "tf32"), (1024, 1024, 32, 30, "bf16")])
+def test_chart_layout_rows_and_padding(n, p, b, l, dt):
+    s = _lib.shape(n, p, b, l, dt, store_chart=True)
+    lay = _lib.chart_layout(s)
+    assert lay.rows == rowbase(l, b, l) + b == b * l * (l + 1) // 2
+    assert lay.np % 256 == 0 and lay.np >= n and lay.pp % 256 == 0 and lay.pp >= p
+    assert lay.off_o >= 0
+    nbytes = _lib.workspace_bytes(s)
+    for off in (lay.off_a, lay.off_b, lay.off_o, lay.off_x, lay.off_lq, lay.off_flag):
+        assert 0 <= off < nbytes and off % 1024 == 0
+    # chart arrays do not overlap
+    span = 4 * lay.rows * lay.np
+    offs = sorted([lay.off_a, lay.off_b, lay.off_o, lay.off_lq])
+    assert all(offs[k] + span <= offs[k + 1] for k in range(3))
+
+
+def test_workspace_scales_and_store_chart_costs_a_chart():
+    s0 = _lib.shape(1024, 1024, 8, 20, "bf16", False)
+    s1 = _lib.shape(1024, 1024, 8, 20, "bf16", True)
+    s2 = _lib.shape(1024, 1024, 8, 20, "fp32", False)
+    assert _lib.workspace_bytes(s1) > _lib.workspace_bytes(s0)
+    assert _lib.workspace_bytes(s2) > _lib.workspace_bytes(s0)   # hi + lo operand planes
+
+
+@pytest.mark.parametrize("bad", [dict(n_nt=0), dict(n_pt=0), dict(batch=0), dict(max_len=1),
+                                 dict(gemm_dtype=7)])
+def test_invalid_shapes_are_rejected(bad):
+    kw = dict(n_nt=8, n_pt=8, batch=2, max_len=5, gemm_dtype=0, store_chart=0)
+    kw.update(bad)
+    s = _lib.FiShape(**kw)
+    lib = _lib.load()
+    assert lib.fi_workspace_bytes(ctypes.byref(s)) == 0
+    rc = lib.fi_inside_forward(ctypes.byref(s), *([None] * 7), None)
+    assert rc == _lib.FI_ERR_ARG
+    assert lib.fi_last_error()
+
+
+def test_null_pointers_are_rejected_before_touching_the_gpu():
+    s = _lib.shape(8, 8, 2, 5)
+    lib = _lib.load()
+    rc = lib.fi_inside_forward(ctypes.byref(s), *([None] * 7), None)
+    assert rc == _lib.FI_ERR_ARG
+    assert b"null pointer" in lib.fi_last_error()
+    with pytest.raises(_lib.EngineError):
+        _lib.check(rc)
+
+
+def test_version_and_launch_counter():
+    lib = _lib.load()
+    assert lib.fi_version() >= 1
+    assert lib.fi_launch_count() >= 0
