@@ -103,7 +103,7 @@ int set_err(int code, const char* fmt, ...) {
 struct Plan {
   int N, P, B, l, Np, Pp, esz, clusters, v, threads, cols_per_cta;
   long long rows;
-  size_t wnn, wnp, e1, eall, gall, a, b, o, lq, x, top, topz, flag, total;
+  size_t wnn, wnp, e1, eall, gall, a, b, o, lq, x, top, topz, wsum, flag, total;
   // element offsets of the lo planes of the GEMM operands (fp32 mode only)
   long long wnn_lo, wnp_lo, e1_lo, eall_lo, gall_lo;
   bool store_o, tf32, split;
@@ -123,6 +123,8 @@ int make_plan(const fi_shape* s, Plan* p) {
     return set_err(FI_ERR_ARG, "unknown gemm_dtype %d", s->gemm_dtype);
   if (s->n_nt > 16384 || s->n_pt > 16384)
     return set_err(FI_ERR_UNSUPPORTED, "symbol counts above 16384 are not supported");
+  if (s->max_len > 1024)  // per-span term tables live in shared memory
+    return set_err(FI_ERR_UNSUPPORTED, "sentences longer than 1024 tokens are not supported");
   p->N = s->n_nt;
   p->P = s->n_pt;
   p->B = s->batch;
@@ -170,6 +172,7 @@ int make_plan(const fi_shape* s, Plan* p) {
   p->x = take(8ull * rows);  // fp64 row shifts
   p->top = take(4ull * p->B * p->Np);
   p->topz = take(4ull * p->B);
+  p->wsum = take(16);
   p->flag = take(256);
   p->total = off;
   return FI_OK;
@@ -318,11 +321,12 @@ int run_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_row0
 }
 
 template <typename K, typename... Args>
-int launch_cluster(K kern, int cluster, dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+int launch_cluster(K kern, int cluster, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                   Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -358,11 +362,12 @@ int forward_impl(const Plan& p, const float* L, const float* R, const float* roo
   float* TOP = at<float>(ws, p.top);
   float* TOPZ = at<float>(ws, p.topz);
 
+  float* wsum = at<float>(ws, p.wsum);
   {  // K1: exp of the child tables, once per call
     ProfScope prof(FI_PROF_PREP, st);
-    dim3 grid((p.Np + p.Pp + 255) / 256, 2 * p.Np);
-    k_prep_weights<T><<<grid, 256, 0, st>>>(L, R, wnn, wnp, p.N, p.P, p.Np, p.Pp, p.wnn_lo,
-                                            p.wnp_lo);
+    FI_CUDA(cudaMemsetAsync(wsum, 0, 16, st));
+    k_prep_weights<T><<<2 * p.Np, 256, 0, st>>>(L, R, wnn, wnp, wsum, p.N, p.P, p.Np, p.Pp,
+                                                p.wnn_lo, p.wnp_lo);
     ++g_launches;
     FI_CUDA(cudaGetLastError());
   }
@@ -396,6 +401,7 @@ int forward_impl(const Plan& p, const float* L, const float* R, const float* roo
     sa.E = w < p.l ? static_cast<void*>(eall) : nullptr;
     sa.e_lo = p.eall_lo;
     sa.X = X;
+    sa.wsum = wsum;
     sa.TOP = TOP;
     sa.TOPZ = TOPZ;
     sa.logZ = logZ;
@@ -410,10 +416,11 @@ int forward_impl(const Plan& p, const float* L, const float* R, const float* roo
     const dim3 grid(p.clusters, p.B * n_w);
     {
       ProfScope prof(FI_PROF_SPLIT, st);
+      const size_t smem = sizeof(SplitTerm) * (w - 1);
       if (p.v == 1)
-        FI_TRY(launch_cluster(k_split_fwd<T, 1>, p.clusters, grid, dim3(p.threads), st, sa));
+        FI_TRY(launch_cluster(k_split_fwd<T, 1>, p.clusters, grid, dim3(p.threads), smem, st, sa));
       else
-        FI_TRY(launch_cluster(k_split_fwd<T, 2>, p.clusters, grid, dim3(p.threads), st, sa));
+        FI_TRY(launch_cluster(k_split_fwd<T, 2>, p.clusters, grid, dim3(p.threads), smem, st, sa));
     }
     if (w < p.l) {
       ep.M = p.B * n_w;
@@ -476,10 +483,11 @@ int backward_impl(const Plan& p, const float* L, const float* R, const float* ro
     const dim3 grid(p.clusters, p.B * n_m);
     {
       ProfScope prof(FI_PROF_GATHER, st);
+      const size_t smem = sizeof(GatherTerm) * p.l;
       if (p.v == 1)
-        k_gather_bwd<T, 1><<<grid, p.threads, 0, st>>>(ga);
+        k_gather_bwd<T, 1><<<grid, p.threads, smem, st>>>(ga);
       else
-        k_gather_bwd<T, 2><<<grid, p.threads, 0, st>>>(ga);
+        k_gather_bwd<T, 2><<<grid, p.threads, smem, st>>>(ga);
     }
     ++g_launches;
     FI_CUDA(cudaGetLastError());

@@ -153,25 +153,36 @@ __device__ __forceinline__ float cluster_reduce(float v, float* slot, float* bca
 // ---------------------------------------------------------------------------
 // K1: W_NN = exp([L_NN ; R_NN]) (2Np x Np), W_NP = exp([L_NP ; R_NP]) (2Np x Pp).
 // Once per call, not per sentence (inside.py:194-200 recomputes it per call).
+// One CTA per row; it also reduces the row's block sums into
+// wsum = {max_A sum W_L,NN, max sum W_R,NN, max sum W_L,NP, max sum W_R,NP},
+// the bounds that let the split contraction use a fixed per-span shift.
 // ---------------------------------------------------------------------------
 template <typename T>
-__global__ void k_prep_weights(const float* __restrict__ L, const float* __restrict__ R,
-                               T* __restrict__ wnn, T* __restrict__ wnp, int N, int P, int Np,
-                               int Pp, long long wnn_lo, long long wnp_lo) {
-  const int row = blockIdx.y;  // 0 .. 2Np-1
+__global__ void __launch_bounds__(256) k_prep_weights(
+    const float* __restrict__ L, const float* __restrict__ R, T* __restrict__ wnn,
+    T* __restrict__ wnp, float* __restrict__ wsum, int N, int P, int Np, int Pp,
+    long long wnn_lo, long long wnp_lo) {
+  __shared__ float red[33];
+  const int row = blockIdx.x;  // 0 .. 2Np-1
   const bool right = row >= Np;
   const int a = right ? row - Np : row;
   const float* src = (right ? R : L) + static_cast<long long>(a) * (N + P);
-  const int total = Np + Pp;
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < total; c += gridDim.x * blockDim.x) {
-    if (c < Np) {
-      float v = (a < N && c < N) ? expf(src[c]) : 0.f;
-      store1s<T>(wnn + static_cast<long long>(row) * Np + c, wnn_lo, v);
-    } else {
-      const int t = c - Np;
-      float v = (a < N && t < P) ? expf(src[N + t]) : 0.f;
-      store1s<T>(wnp + static_cast<long long>(row) * Pp + t, wnp_lo, v);
-    }
+  float snn = 0.f, snp = 0.f;
+  for (int c = threadIdx.x; c < Np; c += blockDim.x) {
+    const float v = (a < N && c < N) ? expf(src[c]) : 0.f;
+    snn += v;
+    store1s<T>(wnn + static_cast<long long>(row) * Np + c, wnn_lo, v);
+  }
+  for (int t = threadIdx.x; t < Pp; t += blockDim.x) {
+    const float v = (a < N && t < P) ? expf(src[N + t]) : 0.f;
+    snp += v;
+    store1s<T>(wnp + static_cast<long long>(row) * Pp + t, wnp_lo, v);
+  }
+  snn = block_reduce<false>(snn, red);
+  snp = block_reduce<false>(snp, red);
+  if (threadIdx.x == 0) {  // non-negative floats order like their bit patterns
+    atomicMax(reinterpret_cast<int*>(wsum) + (right ? 1 : 0), __float_as_int(snn));
+    atomicMax(reinterpret_cast<int*>(wsum) + (right ? 3 : 2), __float_as_int(snp));
   }
 }
 
@@ -215,6 +226,7 @@ struct SplitArgs {
   void* E;           // T*, row stride Np (nullable at w == lmax)
   long long e_lo;    // element offset of the lo plane (fp32 mode), else 0
   double* X;
+  const float* wsum; // K1 block row-sum bounds
   float* TOP;        // B x Np : log2 root + O^ at the top span (for d_root)
   float* TOPZ;       // B      : log2 Z - x†_top
   float* logZ;       // B      : natural-log partition (output)
@@ -223,18 +235,24 @@ struct SplitArgs {
   int B, lmax, N, Np, w, cols_per_cta;
 };
 
-__device__ __forceinline__ void lse_push(float& M, float& S, float v) {
-  const float d = v - M;
-  const float e = ex2(-fabsf(d));  // d = -inf -> 0
-  const bool gt = d > 0.f;
-  S = gt ? fmaf(S, e, 1.f) : S + e;
-  M = gt ? v : M;
-}
+struct SplitTerm {
+  long long ra, rb;  // chart rows of a[m][i] and b[w-m][i+m]
+  double xs;         // x†(a) + x†(b)
+  float d;           // xs - D, rounded once from fp64
+  float pad;
+};
 
+// Every term a[m][i,A] + b[w-m][i+m,A] is bounded by its two row shifts plus
+// the log2 row-sum bounds of the projection blocks (a^ = log2 sum_B W E with
+// E <= 1), so with D = max_m of those bounds every 2^(term - D) <= 1: the
+// log-sum-exp over splits needs no running max -- one FADD pair, one EX2 and
+// one FADD per element and split.  (inside.py:323-331 computes the max first.)
 template <typename T, int V>
 __global__ void __launch_bounds__(256) k_split_fwd(SplitArgs a) {
+  extern __shared__ SplitTerm terms[];  // w - 1 entries
   __shared__ float red[33];
   __shared__ float cl_slot, cl_bcast;
+  __shared__ double dred[33];
   const int w = a.w;
   const int n_w = a.lmax - w + 1;
   const int local = blockIdx.y;
@@ -246,10 +264,34 @@ __global__ void __launch_bounds__(256) k_split_fwd(SplitArgs a) {
   T* E = reinterpret_cast<T*>(a.E);
 
   // split m of span (i, i+w) pairs a[m][i] with b[w-m][i+m]   (inside.py:317-319)
-  // row(m, b, i) advances by B*n_m; row(w-m, b, i+m) retreats by B*n_{w-m+1} - 1
-  long long ra = chart_row(1, b, i, a.B, a.lmax);
-  long long rb = chart_row(w - 1, b, i + 1, a.B, a.lmax);
-  const double ref = a.X[ra] + a.X[rb];  // c_1: the row's reference offset
+  const float lnn = a.wsum[0] > 0.f ? log2f(a.wsum[0]) : 0.f;
+  const float rnn = a.wsum[1] > 0.f ? log2f(a.wsum[1]) : 0.f;
+  const float lnp = a.wsum[2] > 0.f ? log2f(a.wsum[2]) : 0.f;
+  const float rnp = a.wsum[3] > 0.f ? log2f(a.wsum[3]) : 0.f;
+  double ub = -1.0e300;
+  for (int t = threadIdx.x; t < w - 1; t += nthr) {
+    const int m = t + 1;
+    const long long r1 = chart_row(m, b, i, a.B, a.lmax);
+    const long long r2 = chart_row(w - m, b, i + m, a.B, a.lmax);
+    const double xs = a.X[r1] + a.X[r2];
+    terms[t].ra = r1;
+    terms[t].rb = r2;
+    terms[t].xs = xs;
+    ub = fmax(ub, xs + (m == 1 ? lnp : lnn) + (w - m == 1 ? rnp : rnn));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ub = fmax(ub, __shfl_xor_sync(0xffffffffu, ub, o));
+  if ((threadIdx.x & 31) == 0) dred[threadIdx.x >> 5] = ub;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double d = dred[0];
+    for (int k = 1; k < (nthr + 31) >> 5; ++k) d = fmax(d, dred[k]);
+    dred[32] = d;
+  }
+  __syncthreads();
+  const double D = dred[32];
+  for (int t = threadIdx.x; t < w - 1; t += nthr) terms[t].d = static_cast<float>(terms[t].xs - D);
+  __syncthreads();
 
   if (i + w > len) {  // span outside the sentence: never feeds a valid span
 #pragma unroll
@@ -259,65 +301,58 @@ __global__ void __launch_bounds__(256) k_split_fwd(SplitArgs a) {
           make_float4(kNegInf, kNegInf, kNegInf, kNegInf);
       if (E) store4s<T>(E + row * a.Np + c, a.e_lo, 0.f, 0.f, 0.f, 0.f);
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.X[row] = ref;
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.X[row] = D;
     return;  // uniform across the cluster (same row)
   }
 
-  float M[4 * V], S[4 * V];
+  float S[4 * V];
 #pragma unroll
-  for (int k = 0; k < 4 * V; ++k) {
-    M[k] = kLowInit;
-    S[k] = 0.f;
-  }
-  int m = 1;
-  for (; m + 3 < w; m += 4) {
+  for (int k = 0; k < 4 * V; ++k) S[k] = 0.f;
+  int m = 0;
+  for (; m + 3 < w - 1; m += 4) {
     float4 va[4][V], vb[4][V];
     float dl[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int mm = m + u;
-      const long long r1 = chart_row(mm, b, i, a.B, a.lmax);
-      const long long r2 = chart_row(w - mm, b, i + mm, a.B, a.lmax);
-      dl[u] = static_cast<float>(__ldg(a.X + r1) + __ldg(a.X + r2) - ref);
-      const float* pa = a.A + r1 * a.Np;
-      const float* pb = a.Bc + r2 * a.Np;
+      const SplitTerm tm = terms[m + u];
+      dl[u] = tm.d;
+      const float* pa = a.A + tm.ra * a.Np + col0;
+      const float* pb = a.Bc + tm.rb * a.Np + col0;
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        va[u][v] = ldg4(pa + col0 + v * nthr * 4);
-        vb[u][v] = ldg4(pb + col0 + v * nthr * 4);
+        va[u][v] = ldg4(pa + v * nthr * 4);
+        vb[u][v] = ldg4(pb + v * nthr * 4);
       }
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        lse_push(M[4 * v + 0], S[4 * v + 0], va[u][v].x + vb[u][v].x + dl[u]);
-        lse_push(M[4 * v + 1], S[4 * v + 1], va[u][v].y + vb[u][v].y + dl[u]);
-        lse_push(M[4 * v + 2], S[4 * v + 2], va[u][v].z + vb[u][v].z + dl[u]);
-        lse_push(M[4 * v + 3], S[4 * v + 3], va[u][v].w + vb[u][v].w + dl[u]);
+        S[4 * v + 0] += ex2(va[u][v].x + vb[u][v].x + dl[u]);
+        S[4 * v + 1] += ex2(va[u][v].y + vb[u][v].y + dl[u]);
+        S[4 * v + 2] += ex2(va[u][v].z + vb[u][v].z + dl[u]);
+        S[4 * v + 3] += ex2(va[u][v].w + vb[u][v].w + dl[u]);
       }
   }
-  for (; m < w; ++m) {
-    const long long r1 = chart_row(m, b, i, a.B, a.lmax);
-    const long long r2 = chart_row(w - m, b, i + m, a.B, a.lmax);
-    const float dl = static_cast<float>(__ldg(a.X + r1) + __ldg(a.X + r2) - ref);
-    const float* pa = a.A + r1 * a.Np;
-    const float* pb = a.Bc + r2 * a.Np;
+  for (; m < w - 1; ++m) {
+    const SplitTerm tm = terms[m];
+    const float* pa = a.A + tm.ra * a.Np + col0;
+    const float* pb = a.Bc + tm.rb * a.Np + col0;
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      float4 x = ldg4(pa + col0 + v * nthr * 4);
-      float4 y = ldg4(pb + col0 + v * nthr * 4);
-      lse_push(M[4 * v + 0], S[4 * v + 0], x.x + y.x + dl);
-      lse_push(M[4 * v + 1], S[4 * v + 1], x.y + y.y + dl);
-      lse_push(M[4 * v + 2], S[4 * v + 2], x.z + y.z + dl);
-      lse_push(M[4 * v + 3], S[4 * v + 3], x.w + y.w + dl);
+      float4 x = ldg4(pa + v * nthr * 4);
+      float4 y = ldg4(pb + v * nthr * 4);
+      S[4 * v + 0] += ex2(x.x + y.x + tm.d);
+      S[4 * v + 1] += ex2(x.y + y.y + tm.d);
+      S[4 * v + 2] += ex2(x.z + y.z + tm.d);
+      S[4 * v + 3] += ex2(x.w + y.w + tm.d);
     }
   }
-  float o[4 * V];  // o - ref
+  float o[4 * V];  // o - D
   float mx = kNegInf;
 #pragma unroll
   for (int k = 0; k < 4 * V; ++k) {
-    o[k] = S[k] > 0.f ? M[k] + lg2(S[k]) : kNegInf;
+    o[k] = lg2(S[k]);  // S = 0 -> -inf
     mx = fmaxf(mx, o[k]);
   }
   // row max over all Np columns: block, then cluster (DSMEM)
@@ -338,7 +373,7 @@ __global__ void __launch_bounds__(256) k_split_fwd(SplitArgs a) {
       store4s<T>(E + row * a.Np + col0 + v * nthr * 4, a.e_lo, ex2(o[4 * v]), ex2(o[4 * v + 1]),
                  ex2(o[4 * v + 2]), ex2(o[4 * v + 3]));
   }
-  const double xrow = ref + static_cast<double>(xs);
+  const double xrow = D + static_cast<double>(xs);
   if (blockIdx.x == 0 && threadIdx.x == 0) a.X[row] = xrow;
 
   if (i == 0 && w == len) {  // top span: logZ = LSE_A(root[A] + o[A])  (inside.py:124-129)
@@ -424,8 +459,15 @@ struct GatherArgs {
   int B, lmax, Np, m, cols_per_cta;
 };
 
+struct GatherTerm {
+  long long rs, rp;  // chart rows of the sibling and of the parent
+  float d;           // x†(child) + x†(sibling) - x†(parent), rounded from fp64
+  float pad;
+};
+
 template <typename T, int V>
 __global__ void __launch_bounds__(256) k_gather_bwd(GatherArgs a) {
+  extern __shared__ GatherTerm gterms[];  // <= lmax entries: G_L terms then G_R terms
   const int m = a.m;
   const int n_m = a.lmax - m + 1;
   const int local = blockIdx.y;
@@ -445,101 +487,77 @@ __global__ void __launch_bounds__(256) k_gather_bwd(GatherArgs a) {
     }
     return;
   }
+  // left child (i, i+m) of parent (i, i+w), w = m+1..len-i: sibling b[w-m][i+m]
+  // right child (i, i+m) of parent (s, i+m), s = 0..i-1:    sibling a[i-s][s]
+  const int n_left = len - i - m;
+  const int n_all = n_left + i;
   const double xm = a.X[row];
+  for (int t = threadIdx.x; t < n_all; t += nthr) {
+    long long rs, rp;
+    if (t < n_left) {
+      const int w = m + 1 + t;
+      rs = chart_row(w - m, b, i + m, a.B, a.lmax);
+      rp = chart_row(w, b, i, a.B, a.lmax);
+    } else {
+      const int sidx = t - n_left;
+      rs = chart_row(i - sidx, b, sidx, a.B, a.lmax);
+      rp = chart_row(i + m - sidx, b, sidx, a.B, a.lmax);
+    }
+    gterms[t].rs = rs;
+    gterms[t].rp = rp;
+    gterms[t].d = static_cast<float>(xm + a.X[rs] - a.X[rp]);
+  }
+  __syncthreads();
+
   float gl[4 * V], gr[4 * V];
 #pragma unroll
   for (int k = 0; k < 4 * V; ++k) gl[k] = gr[k] = 0.f;
+  // one pass over both term lists; each term is 2^(d + sibling^ + LQ^)
+  auto run = [&](const float* sib, int t0, int t1, float (&acc)[4 * V]) {
+    int t = t0;
+    for (; t + 1 < t1; t += 2) {
+      float4 vs[2][V], vq[2][V];
+      float d[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const GatherTerm tm = gterms[t + u];
+        d[u] = tm.d;
+        const float* ps = sib + tm.rs * a.Np + col0;
+        const float* pq = a.LQ + tm.rp * a.Np + col0;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          vs[u][v] = ldg4(ps + v * nthr * 4);
+          vq[u][v] = ldg4(pq + v * nthr * 4);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          acc[4 * v + 0] += ex2(vs[u][v].x + vq[u][v].x + d[u]);
+          acc[4 * v + 1] += ex2(vs[u][v].y + vq[u][v].y + d[u]);
+          acc[4 * v + 2] += ex2(vs[u][v].z + vq[u][v].z + d[u]);
+          acc[4 * v + 3] += ex2(vs[u][v].w + vq[u][v].w + d[u]);
+        }
+    }
+    for (; t < t1; ++t) {
+      const GatherTerm tm = gterms[t];
+      const float* ps = sib + tm.rs * a.Np + col0;
+      const float* pq = a.LQ + tm.rp * a.Np + col0;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        float4 x = ldg4(ps + v * nthr * 4);
+        float4 q = ldg4(pq + v * nthr * 4);
+        acc[4 * v + 0] += ex2(x.x + q.x + tm.d);
+        acc[4 * v + 1] += ex2(x.y + q.y + tm.d);
+        acc[4 * v + 2] += ex2(x.z + q.z + tm.d);
+        acc[4 * v + 3] += ex2(x.w + q.w + tm.d);
+      }
+    }
+  };
+  run(a.Bc, 0, n_left, gl);
+  run(a.A, n_left, n_all, gr);
 
-  // left child (i, i+m) of parent (i, i+w): right sibling b[w-m][i+m]
-  const int wmax = len - i;
-  int w = m + 1;
-  for (; w + 1 <= wmax; w += 2) {
-    float4 vb[2][V], vq[2][V];
-    float d[2];
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const long long rs = chart_row(w + u - m, b, i + m, a.B, a.lmax);
-      const long long rp = chart_row(w + u, b, i, a.B, a.lmax);
-      d[u] = static_cast<float>(xm + __ldg(a.X + rs) - __ldg(a.X + rp));
-      const float* pb = a.Bc + rs * a.Np;
-      const float* pq = a.LQ + rp * a.Np;
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        vb[u][v] = ldg4(pb + col0 + v * nthr * 4);
-        vq[u][v] = ldg4(pq + col0 + v * nthr * 4);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 2; ++u)
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        gl[4 * v + 0] += ex2(vb[u][v].x + vq[u][v].x + d[u]);
-        gl[4 * v + 1] += ex2(vb[u][v].y + vq[u][v].y + d[u]);
-        gl[4 * v + 2] += ex2(vb[u][v].z + vq[u][v].z + d[u]);
-        gl[4 * v + 3] += ex2(vb[u][v].w + vq[u][v].w + d[u]);
-      }
-  }
-  for (; w <= wmax; ++w) {
-    const long long rs = chart_row(w - m, b, i + m, a.B, a.lmax);
-    const long long rp = chart_row(w, b, i, a.B, a.lmax);
-    const float d = static_cast<float>(xm + __ldg(a.X + rs) - __ldg(a.X + rp));
-    const float* pb = a.Bc + rs * a.Np;
-    const float* pq = a.LQ + rp * a.Np;
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      float4 x = ldg4(pb + col0 + v * nthr * 4);
-      float4 q = ldg4(pq + col0 + v * nthr * 4);
-      gl[4 * v + 0] += ex2(x.x + q.x + d);
-      gl[4 * v + 1] += ex2(x.y + q.y + d);
-      gl[4 * v + 2] += ex2(x.z + q.z + d);
-      gl[4 * v + 3] += ex2(x.w + q.w + d);
-    }
-  }
-  // right child (i, i+m) of parent (s, i+m): left sibling a[i-s][s]
-  int s = 0;
-  for (; s + 1 < i; s += 2) {
-    float4 va[2][V], vq[2][V];
-    float d[2];
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int ss = s + u;
-      const long long rs = chart_row(i - ss, b, ss, a.B, a.lmax);
-      const long long rp = chart_row(i + m - ss, b, ss, a.B, a.lmax);
-      d[u] = static_cast<float>(xm + __ldg(a.X + rs) - __ldg(a.X + rp));
-      const float* pa = a.A + rs * a.Np;
-      const float* pq = a.LQ + rp * a.Np;
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        va[u][v] = ldg4(pa + col0 + v * nthr * 4);
-        vq[u][v] = ldg4(pq + col0 + v * nthr * 4);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 2; ++u)
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        gr[4 * v + 0] += ex2(va[u][v].x + vq[u][v].x + d[u]);
-        gr[4 * v + 1] += ex2(va[u][v].y + vq[u][v].y + d[u]);
-        gr[4 * v + 2] += ex2(va[u][v].z + vq[u][v].z + d[u]);
-        gr[4 * v + 3] += ex2(va[u][v].w + vq[u][v].w + d[u]);
-      }
-  }
-  for (; s < i; ++s) {
-    const long long rs = chart_row(i - s, b, s, a.B, a.lmax);
-    const long long rp = chart_row(i + m - s, b, s, a.B, a.lmax);
-    const float d = static_cast<float>(xm + __ldg(a.X + rs) - __ldg(a.X + rp));
-    const float* pa = a.A + rs * a.Np;
-    const float* pq = a.LQ + rp * a.Np;
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      float4 x = ldg4(pa + col0 + v * nthr * 4);
-      float4 q = ldg4(pq + col0 + v * nthr * 4);
-      gr[4 * v + 0] += ex2(x.x + q.x + d);
-      gr[4 * v + 1] += ex2(x.y + q.y + d);
-      gr[4 * v + 2] += ex2(x.z + q.z + d);
-      gr[4 * v + 3] += ex2(x.w + q.w + d);
-    }
-  }
   // zero-mass projections carry no gradient (inside.py:441-443 NaN guard)
   const float sg = a.g[b] < 0.f ? -1.f : 1.f;
   const float* pam = a.A + row * a.Np;
