@@ -14,9 +14,11 @@
 //            (m = 1: dunary = E1 * (G_1 W_NP)) -> tcgen05 GEMM, EPI_DUNARY
 //   dW = G^T E over all spans, d{L,R} = W*dW   -> tcgen05 GEMM, EPI_WGRAD
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <atomic>
+#include <type_traits>
 #include <mutex>
 #include <vector>
 #include <cudaTypedefs.h>
@@ -100,8 +102,13 @@ int set_err(int code, const char* fmt, ...) {
   } while (0)
 
 // ------------------------------------------------------------------ layout
+struct Decomp {
+  int clusters, threads, v, cols_per_cta, stages;
+};
+
 struct Plan {
-  int N, P, B, l, Np, Pp, esz, clusters, v, threads, cols_per_cta;
+  int N, P, B, l, Np, Pp, esz;
+  Decomp dsplit, dgather;
   long long rows;
   size_t wnn, wnp, e1, eall, gall, a, b, o, lq, x, top, topz, wsum, flag, total;
   // element offsets of the lo planes of the GEMM operands (fp32 mode only)
@@ -110,6 +117,26 @@ struct Plan {
 };
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+int make_decomp(int Np, int c, const char* env_c, const char* env_s, int stages, Decomp* d) {
+  const int want = env_int(env_c, c);
+  if (want >= 1 && want <= 8 && Np % (want * 256) == 0) c = want;
+  const int cols = Np / c;
+  d->clusters = c;
+  d->threads = cols / 4 < 256 ? cols / 4 : 256;
+  d->v = cols / (4 * d->threads);
+  d->cols_per_cta = cols;
+  const int st = env_int(env_s, stages);
+  d->stages = st < 2 ? 2 : (st > 16 ? 16 : st);
+  if (d->v != 1 && d->v != 2 && d->v != 4)
+    return set_err(FI_ERR_UNSUPPORTED, "unsupported column decomposition (Np=%d, C=%d)", Np, c);
+  return FI_OK;
+}
 
 int make_plan(const fi_shape* s, Plan* p) {
   if (!s) return set_err(FI_ERR_ARG, "null shape");
@@ -136,16 +163,14 @@ int make_plan(const fi_shape* s, Plan* p) {
   p->esz = p->tf32 ? 4 : 2;
   const int planes = p->split ? 2 : 1;
   p->store_o = s->store_chart != 0;
-  if (p->Np <= 1024) {
-    p->clusters = 1;
-    p->threads = p->Np / 4;
-    p->v = 1;
-  } else {
-    p->threads = 256;
-    p->clusters = p->Np / 1024 < 8 ? p->Np / 1024 : 8;
-    p->v = p->Np / (p->clusters * 1024);
-  }
-  p->cols_per_cta = p->Np / p->clusters;
+  // column decomposition of a span row for the bandwidth kernels: C CTAs
+  // (a thread-block cluster for the split contraction's row max), each
+  // `threads` consumer threads x V float4 columns.  Measured on B200 at
+  // N = 4096 (bench sweeps): split C = 2 / 4-deep ring, gather C = 4 /
+  // 6-deep ring.  FI_CLUSTER / FI_GCLUSTER / FI_STAGES / FI_GSTAGES override.
+  FI_TRY(make_decomp(p->Np, p->Np <= 1024 ? 1 : 2, "FI_CLUSTER", "FI_STAGES", 4, &p->dsplit));
+  FI_TRY(make_decomp(p->Np, p->Np <= 1024 ? 1 : (p->Np / 1024 < 8 ? p->Np / 1024 : 8),
+                     "FI_GCLUSTER", "FI_GSTAGES", 6, &p->dgather));
   p->rows = rowbase(p->l, p->B, p->l) + p->B;
   const long long rows = p->rows;
   if (static_cast<long long>(p->B) * p->l > 65535 || rows > (1LL << 30))
@@ -320,6 +345,34 @@ int run_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_row0
   return run_gemm_s<T, AMN, BMN, EPI, false>(A, B, M, N, K, a_row0, ep, st);
 }
 
+// Bandwidth-kernel variant: TMA-bulk shared-memory ring (default) or the
+// register-pipelined kernels (FI_BULK=0), and the ring depth (FI_STAGES).
+bool use_bulk() {
+  static int v = [] {
+    const char* e = getenv("FI_BULK");
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0;
+}
+template <int V>
+using VC = std::integral_constant<int, V>;
+template <typename F>
+int dispatch_v(int v, F&& f) {
+  switch (v) {
+    case 1: return f(VC<1>{});
+    case 2: return f(VC<2>{});
+    case 4: return f(VC<4>{});
+  }
+  return set_err(FI_ERR_UNSUPPORTED, "columns per thread %d", v);
+}
+
+template <typename K>
+int set_smem(K kern, size_t bytes) {
+  FI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(bytes < 49152 ? 49152 : bytes)));
+  return FI_OK;
+}
+
 template <typename K, typename... Args>
 int launch_cluster(K kern, int cluster, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                    Args... args) {
@@ -412,15 +465,30 @@ int forward_impl(const Plan& p, const float* L, const float* R, const float* roo
     sa.N = p.N;
     sa.Np = p.Np;
     sa.w = w;
-    sa.cols_per_cta = p.cols_per_cta;
-    const dim3 grid(p.clusters, p.B * n_w);
+    const Decomp& dc = p.dsplit;
+    sa.cols_per_cta = dc.cols_per_cta;
+    const dim3 grid(dc.clusters, p.B * n_w);
     {
       ProfScope prof(FI_PROF_SPLIT, st);
-      const size_t smem = sizeof(SplitTerm) * (w - 1);
-      if (p.v == 1)
-        FI_TRY(launch_cluster(k_split_fwd<T, 1>, p.clusters, grid, dim3(p.threads), smem, st, sa));
-      else
-        FI_TRY(launch_cluster(k_split_fwd<T, 2>, p.clusters, grid, dim3(p.threads), smem, st, sa));
+      if (use_bulk()) {
+        const int stages = dc.stages;
+        const size_t smem = align128(sizeof(SplitTerm) * (w - 1)) +
+                            static_cast<size_t>(stages) * (2 * dc.cols_per_cta * 4 + 16);
+        const dim3 block(32 + dc.threads);
+        FI_TRY(dispatch_v(dc.v, [&](auto vc) {
+          constexpr int V = decltype(vc)::value;
+          FI_TRY(set_smem(k_split_fwd_bulk<T, V>, smem));
+          return launch_cluster(k_split_fwd_bulk<T, V>, dc.clusters, grid, block, smem, st, sa,
+                                stages);
+        }));
+      } else {
+        const size_t smem = sizeof(SplitTerm) * (w - 1);
+        FI_TRY(dispatch_v(dc.v, [&](auto vc) {
+          constexpr int V = decltype(vc)::value;
+          return launch_cluster(k_split_fwd<T, V>, dc.clusters, grid, dim3(dc.threads), smem, st,
+                                sa);
+        }));
+      }
     }
     if (w < p.l) {
       ep.M = p.B * n_w;
@@ -479,15 +547,29 @@ int backward_impl(const Plan& p, const float* L, const float* R, const float* ro
     ga.lmax = p.l;
     ga.Np = p.Np;
     ga.m = m;
-    ga.cols_per_cta = p.cols_per_cta;
-    const dim3 grid(p.clusters, p.B * n_m);
+    const Decomp& dc = p.dgather;
+    ga.cols_per_cta = dc.cols_per_cta;
+    const dim3 grid(dc.clusters, p.B * n_m);
     {
       ProfScope prof(FI_PROF_GATHER, st);
-      const size_t smem = sizeof(GatherTerm) * p.l;
-      if (p.v == 1)
-        k_gather_bwd<T, 1><<<grid, p.threads, smem, st>>>(ga);
-      else
-        k_gather_bwd<T, 2><<<grid, p.threads, smem, st>>>(ga);
+      if (use_bulk()) {
+        const int stages = dc.stages;
+        const size_t smem = align128(sizeof(GatherTerm) * p.l) +
+                            static_cast<size_t>(stages) * (2 * dc.cols_per_cta * 4 + 16);
+        FI_TRY(dispatch_v(dc.v, [&](auto vc) {
+          constexpr int V = decltype(vc)::value;
+          FI_TRY(set_smem(k_gather_bwd_bulk<T, V>, smem));
+          k_gather_bwd_bulk<T, V><<<grid, 32 + dc.threads, smem, st>>>(ga, stages);
+          return FI_OK;
+        }));
+      } else {
+        const size_t smem = sizeof(GatherTerm) * p.l;
+        FI_TRY(dispatch_v(dc.v, [&](auto vc) {
+          constexpr int V = decltype(vc)::value;
+          k_gather_bwd<T, V><<<grid, dc.threads, smem, st>>>(ga);
+          return FI_OK;
+        }));
+      }
     }
     ++g_launches;
     FI_CUDA(cudaGetLastError());

@@ -575,6 +575,322 @@ __global__ void __launch_bounds__(256) k_gather_bwd(GatherArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-bulk pipelined variants of the split contraction and the gather.
+// Both kernels stream, per term, two contiguous row chunks (Np/C floats each)
+// from HBM into a STAGES-deep shared-memory ring with cp.async.bulk
+// (warp 0, one lane: producer) while warps 1.. consume them from shared
+// memory; mbarrier full/empty pairs hand stages back and forth.  This keeps
+// ~STAGES * 8 KB in flight per CTA with almost no registers, so the kernels
+// sit on the HBM roofline instead of the load-latency limit of the
+// register-pipelined versions above.
+// ---------------------------------------------------------------------------
+struct BulkRing {
+  float* buf;       // stages x (2 x cpc) floats
+  uint64_t* full;   // stages
+  uint64_t* empty;  // stages
+  int stages, cpc;
+};
+
+__device__ __forceinline__ BulkRing carve_ring(uint8_t* base, int stages, int cpc) {
+  BulkRing r;
+  r.buf = reinterpret_cast<float*>(base);
+  r.full = reinterpret_cast<uint64_t*>(base + static_cast<size_t>(stages) * 2 * cpc * 4);
+  r.empty = r.full + stages;
+  r.stages = stages;
+  r.cpc = cpc;
+  return r;
+}
+
+__device__ __forceinline__ void ring_init(BulkRing& r, int consumer_warps) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < r.stages; ++s) {
+      mbar_init(&r.full[s], 1);
+      mbar_init(&r.empty[s], consumer_warps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+}
+
+__host__ __device__ __forceinline__ size_t align128(size_t v) { return (v + 127) & ~size_t(127); }
+
+template <typename T, int V>
+__global__ void __launch_bounds__(288) k_split_fwd_bulk(SplitArgs a, int stages) {
+  extern __shared__ __align__(128) uint8_t dsm[];
+  __shared__ float red[33];
+  __shared__ float cl_slot, cl_bcast;
+  __shared__ double dred[33];
+  const int w = a.w;
+  const int nsplit = w - 1;
+  const int n_w = a.lmax - w + 1;
+  const int local = blockIdx.y;
+  const int b = local / n_w, i = local % n_w;
+  const int len = a.lengths[b];
+  const long long row = rowbase(w, a.B, a.lmax) + local;
+  const int nthr = blockDim.x;
+  const int ncons = nthr - 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cpc = a.cols_per_cta;
+  const int chunk0 = blockIdx.x * cpc;
+  const int ci = threadIdx.x - 32;                 // consumer index
+  const int col0 = chunk0 + ci * 4;
+  T* E = reinterpret_cast<T*>(a.E);
+  SplitTerm* terms = reinterpret_cast<SplitTerm*>(dsm);
+  BulkRing ring = carve_ring(dsm + align128(sizeof(SplitTerm) * nsplit), stages, cpc);
+
+  // per-split rows and fixed shift D (see k_split_fwd)
+  const float lnn = a.wsum[0] > 0.f ? log2f(a.wsum[0]) : 0.f;
+  const float rnn = a.wsum[1] > 0.f ? log2f(a.wsum[1]) : 0.f;
+  const float lnp = a.wsum[2] > 0.f ? log2f(a.wsum[2]) : 0.f;
+  const float rnp = a.wsum[3] > 0.f ? log2f(a.wsum[3]) : 0.f;
+  double ub = -1.0e300;
+  for (int t = threadIdx.x; t < nsplit; t += nthr) {
+    const int m = t + 1;
+    const long long r1 = chart_row(m, b, i, a.B, a.lmax);
+    const long long r2 = chart_row(w - m, b, i + m, a.B, a.lmax);
+    const double xs = a.X[r1] + a.X[r2];
+    terms[t].ra = r1;
+    terms[t].rb = r2;
+    terms[t].xs = xs;
+    ub = fmax(ub, xs + (m == 1 ? lnp : lnn) + (w - m == 1 ? rnp : rnn));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ub = fmax(ub, __shfl_xor_sync(0xffffffffu, ub, o));
+  if (lane == 0) dred[warp] = ub;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double d = dred[0];
+    for (int k = 1; k < (nthr + 31) >> 5; ++k) d = fmax(d, dred[k]);
+    dred[32] = d;
+  }
+  __syncthreads();
+  const double D = dred[32];
+  for (int t = threadIdx.x; t < nsplit; t += nthr) terms[t].d = static_cast<float>(terms[t].xs - D);
+
+  if (i + w > len) {  // span outside the sentence: never feeds a valid span
+    if (ci >= 0) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const int c = col0 + v * ncons * 4;
+        if (a.O) *reinterpret_cast<float4*>(a.O + row * a.Np + c) =
+            make_float4(kNegInf, kNegInf, kNegInf, kNegInf);
+        if (E) store4s<T>(E + row * a.Np + c, a.e_lo, 0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.X[row] = D;
+    return;  // uniform across the cluster (same row)
+  }
+  ring_init(ring, ncons >> 5);  // also publishes the term table
+
+  float S[4 * V];
+#pragma unroll
+  for (int k = 0; k < 4 * V; ++k) S[k] = 0.f;
+  if (warp == 0) {
+    if (lane == 0) {  // producer: a[m][i] and b[w-m][i+m] chunks of every split
+      for (int t = 0; t < nsplit; ++t) {
+        const int s = t % stages;
+        const uint32_t ph = (t / stages) & 1;
+        mbar_wait(&ring.empty[s], ph ^ 1);
+        mbar_expect_tx(&ring.full[s], 2u * cpc * 4u);
+        float* dst = ring.buf + static_cast<size_t>(s) * 2 * cpc;
+        bulk_g2s(dst, a.A + terms[t].ra * a.Np + chunk0, cpc * 4u, &ring.full[s]);
+        bulk_g2s(dst + cpc, a.Bc + terms[t].rb * a.Np + chunk0, cpc * 4u, &ring.full[s]);
+      }
+    }
+  } else {
+    for (int t = 0; t < nsplit; ++t) {
+      const int s = t % stages;
+      const uint32_t ph = (t / stages) & 1;
+      mbar_wait(&ring.full[s], ph);
+      const float dl = terms[t].d;
+      const float* src = ring.buf + static_cast<size_t>(s) * 2 * cpc + ci * 4;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const float4 x = *reinterpret_cast<const float4*>(src + v * ncons * 4);
+        const float4 y = *reinterpret_cast<const float4*>(src + cpc + v * ncons * 4);
+        S[4 * v + 0] += ex2(x.x + y.x + dl);
+        S[4 * v + 1] += ex2(x.y + y.y + dl);
+        S[4 * v + 2] += ex2(x.z + y.z + dl);
+        S[4 * v + 3] += ex2(x.w + y.w + dl);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ring.empty[s]);
+    }
+  }
+  float o[4 * V];  // o - D
+  float mx = kNegInf;
+#pragma unroll
+  for (int k = 0; k < 4 * V; ++k) {
+    o[k] = warp == 0 ? kNegInf : lg2(S[k]);  // S = 0 -> -inf
+    mx = fmaxf(mx, o[k]);
+  }
+  mx = block_reduce<true>(mx, red);
+  mx = cluster_reduce<true>(mx, &cl_slot, &cl_bcast);
+  const float xs = (mx == kNegInf) ? 0.f : mx;  // inside.py:324-326
+#pragma unroll
+  for (int k = 0; k < 4 * V; ++k) o[k] -= xs;    // O^ = o - x†  (<= 0)
+  if (ci >= 0) {
+    if (a.O) {
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        *reinterpret_cast<float4*>(a.O + row * a.Np + col0 + v * ncons * 4) =
+            make_float4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+    }
+    if (E) {
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        store4s<T>(E + row * a.Np + col0 + v * ncons * 4, a.e_lo, ex2(o[4 * v]),
+                   ex2(o[4 * v + 1]), ex2(o[4 * v + 2]), ex2(o[4 * v + 3]));
+    }
+  }
+  const double xrow = D + static_cast<double>(xs);
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.X[row] = xrow;
+
+  if (i == 0 && w == len) {  // top span: logZ = LSE_A(root[A] + o[A])  (inside.py:124-129)
+    float sc[4 * V];
+    float smx = kNegInf;
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int c = col0 + v * ncons * 4 + k;
+        sc[4 * v + k] = (ci >= 0 && c < a.N) ? fmaf(a.root[c], kLog2e, o[4 * v + k]) : kNegInf;
+        if (ci >= 0) a.TOP[static_cast<long long>(b) * a.Np + c] = sc[4 * v + k];
+        smx = fmaxf(smx, sc[4 * v + k]);
+      }
+    smx = block_reduce<true>(smx, red);
+    smx = cluster_reduce<true>(smx, &cl_slot, &cl_bcast);
+    float sum = 0.f;
+    if (smx != kNegInf) {
+#pragma unroll
+      for (int k = 0; k < 4 * V; ++k) sum += exp2f(sc[k] - smx);
+    }
+    sum = block_reduce<false>(sum, red);
+    sum = cluster_reduce<false>(sum, &cl_slot, &cl_bcast);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      const float z = smx == kNegInf ? kNegInf : smx + log2f(sum);  // log2 Z - x†
+      a.TOPZ[b] = z;
+      a.logZ[b] = z == kNegInf ? kNegInf : static_cast<float>((xrow + z) * kLn2d);
+    }
+  }
+}
+
+template <typename T, int V>
+__global__ void __launch_bounds__(288) k_gather_bwd_bulk(GatherArgs a, int stages) {
+  extern __shared__ __align__(128) uint8_t dsm[];
+  const int m = a.m;
+  const int n_m = a.lmax - m + 1;
+  const int local = blockIdx.y;
+  const int b = local / n_m, i = local % n_m;
+  const int len = a.lengths[b];
+  const long long row = rowbase(m, a.B, a.lmax) + local;
+  const int nthr = blockDim.x;
+  const int ncons = nthr - 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cpc = a.cols_per_cta;
+  const int chunk0 = blockIdx.x * cpc;
+  const int ci = threadIdx.x - 32;
+  const int col0 = chunk0 + ci * 4;
+  T* G = reinterpret_cast<T*>(a.G) + row * (2LL * a.Np);
+
+  if (i + m > len) {
+    if (ci >= 0) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const int c = col0 + v * ncons * 4;
+        store4s<T>(G + c, a.g_lo, 0.f, 0.f, 0.f, 0.f);
+        store4s<T>(G + a.Np + c, a.g_lo, 0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    return;
+  }
+  const int n_left = len - i - m;
+  const int n_all = n_left + i;
+  GatherTerm* gterms = reinterpret_cast<GatherTerm*>(dsm);
+  BulkRing ring = carve_ring(dsm + align128(sizeof(GatherTerm) * a.lmax), stages, cpc);
+  const double xm = a.X[row];
+  for (int t = threadIdx.x; t < n_all; t += nthr) {
+    long long rs, rp;
+    if (t < n_left) {  // left child (i, i+m) of parent (i, i+w): sibling b[w-m][i+m]
+      const int w = m + 1 + t;
+      rs = chart_row(w - m, b, i + m, a.B, a.lmax);
+      rp = chart_row(w, b, i, a.B, a.lmax);
+    } else {           // right child of parent (s, i+m): sibling a[i-s][s]
+      const int sidx = t - n_left;
+      rs = chart_row(i - sidx, b, sidx, a.B, a.lmax);
+      rp = chart_row(i + m - sidx, b, sidx, a.B, a.lmax);
+    }
+    gterms[t].rs = rs;
+    gterms[t].rp = rp;
+    gterms[t].d = static_cast<float>(xm + a.X[rs] - a.X[rp]);
+  }
+  ring_init(ring, ncons >> 5);
+
+  float gl[4 * V], gr[4 * V];
+#pragma unroll
+  for (int k = 0; k < 4 * V; ++k) gl[k] = gr[k] = 0.f;
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int t = 0; t < n_all; ++t) {
+        const int s = t % stages;
+        const uint32_t ph = (t / stages) & 1;
+        mbar_wait(&ring.empty[s], ph ^ 1);
+        mbar_expect_tx(&ring.full[s], 2u * cpc * 4u);
+        float* dst = ring.buf + static_cast<size_t>(s) * 2 * cpc;
+        const float* sib = t < n_left ? a.Bc : a.A;
+        bulk_g2s(dst, sib + gterms[t].rs * a.Np + chunk0, cpc * 4u, &ring.full[s]);
+        bulk_g2s(dst + cpc, a.LQ + gterms[t].rp * a.Np + chunk0, cpc * 4u, &ring.full[s]);
+      }
+    }
+  } else {
+    for (int t = 0; t < n_all; ++t) {
+      const int s = t % stages;
+      const uint32_t ph = (t / stages) & 1;
+      mbar_wait(&ring.full[s], ph);
+      const float d = gterms[t].d;
+      const float* src = ring.buf + static_cast<size_t>(s) * 2 * cpc + ci * 4;
+      float* acc = t < n_left ? gl : gr;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const float4 x = *reinterpret_cast<const float4*>(src + v * ncons * 4);
+        const float4 q = *reinterpret_cast<const float4*>(src + cpc + v * ncons * 4);
+        if (t < n_left) {
+          gl[4 * v + 0] += ex2(x.x + q.x + d);
+          gl[4 * v + 1] += ex2(x.y + q.y + d);
+          gl[4 * v + 2] += ex2(x.z + q.z + d);
+          gl[4 * v + 3] += ex2(x.w + q.w + d);
+        } else {
+          gr[4 * v + 0] += ex2(x.x + q.x + d);
+          gr[4 * v + 1] += ex2(x.y + q.y + d);
+          gr[4 * v + 2] += ex2(x.z + q.z + d);
+          gr[4 * v + 3] += ex2(x.w + q.w + d);
+        }
+      }
+      (void)acc;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ring.empty[s]);
+    }
+    // zero-mass projections carry no gradient (inside.py:441-443 NaN guard)
+    const float sg = a.g[b] < 0.f ? -1.f : 1.f;
+    const float* pam = a.A + row * a.Np;
+    const float* pbm = a.Bc + row * a.Np;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int c = col0 + v * ncons * 4;
+      float4 am = ldg4(pam + c), bm = ldg4(pbm + c);
+      store4s<T>(G + c, a.g_lo, am.x == kNegInf ? 0.f : sg * gl[4 * v + 0],
+                 am.y == kNegInf ? 0.f : sg * gl[4 * v + 1],
+                 am.z == kNegInf ? 0.f : sg * gl[4 * v + 2],
+                 am.w == kNegInf ? 0.f : sg * gl[4 * v + 3]);
+      store4s<T>(G + a.Np + c, a.g_lo, bm.x == kNegInf ? 0.f : sg * gr[4 * v + 0],
+                 bm.y == kNegInf ? 0.f : sg * gr[4 * v + 1],
+                 bm.z == kNegInf ? 0.f : sg * gr[4 * v + 2],
+                 bm.w == kNegInf ? 0.f : sg * gr[4 * v + 3]);
+    }
+  }
+}
+
 // Span marginals mu_sym[w][i, A] = go / |g| = 2^(LQ^ + O^ - log2|g|)  (inside.py:425-430)
 __global__ void k_marginals(const float* __restrict__ LQ, const float* __restrict__ O,
                             const float* __restrict__ g, const int* __restrict__ lengths,
