@@ -1,0 +1,116 @@
+"""Summarise ncu outputs (launch list CSV + --set full reports) into profiles/.
+
+    python scripts/summarize_profiles.py --tag r01 --launches gpurun_out/launches.csv \
+        --reps gpurun_out/prof_*.ncu-rep
+
+Writes profiles/<tag>_launches_summary.md, profiles/<tag>_ncu_kernels.json and
+profiles/ncu_traffic.json (per kernel class: DRAM bytes of the captured
+launch and its algorithmic bytes, read by bench.py for roofline.traffic).
+"""
+
+from __future__ import annotations
+
+import argparse
+import collections
+import csv
+import json
+import re
+import subprocess
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+SCALE = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0,
+         "second": 1e3, "s": 1e3}
+BYTES = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6,
+         "GB": 1e9}
+
+
+def short(name: str) -> str:
+    return re.sub(r"\(.*", "", name).replace("void fi::", "").replace("void ", "")
+
+
+def launches(path: Path, tag: str) -> str:
+    rows = list(csv.reader(path.read_text().splitlines()))
+    hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
+    hdr, data = rows[hi], rows[hi + 1:]
+    ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    ks = [(r[ki], float(r[vi].replace(",", "")) * SCALE[r[ui]]) for r in data if len(r) > vi]
+    step = ks[len(ks) // 2:]  # second of two identical steps (first is warm-up)
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for name, ms in step:
+        agg[short(name)][0] += 1
+        agg[short(name)][1] += ms
+    tot = sum(ms for _, ms in step)
+    out = [f"# {tag} launch list (ncu --metrics gpu__time_duration.sum --clock-control none)",
+           "", "Second of two identical fwd+bwd steps; ncu serialises and cold-starts every",
+           "launch, so compare the SHARES with bench.py's per-class CUDA-event times.",
+           f"Total {tot:.2f} ms over {len(step)} launches.", "",
+           "| kernel | launches | ms | share |", "|---|---|---|---|"]
+    for k, (c, ms) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        out.append(f"| `{k[:90]}` | {c} | {ms:.3f} | {100 * ms / tot:.1f}% |")
+    return "\n".join(out) + "\n"
+
+
+WANT = {
+    "time_ms": "gpu__time_duration.sum",
+    "dram_read": "dram__bytes_read.sum",
+    "dram_write": "dram__bytes_write.sum",
+    "dram_pct_peak": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "tensor_pct": "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "l2_hit_pct": "lts__t_sector_hit_rate.pct",
+    "regs": "launch__registers_per_thread",
+    "warps_active_pct": "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "issue_busy_pct": "sm__inst_issued.avg.pct_of_peak_sustained_active",
+}
+
+
+def report(path: Path) -> list[dict]:
+    out = subprocess.run(["ncu", "-i", str(path), "--page", "raw", "--csv"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    hdr, units = rows[0], rows[1]
+    res = []
+    for r in rows[2:]:
+        d = {"file": path.name, "kernel": short(r[hdr.index("Kernel Name")]),
+             "grid": r[hdr.index("Grid Size")], "block": r[hdr.index("Block Size")]}
+        for key, metric in WANT.items():
+            if metric not in hdr:
+                continue
+            j = hdr.index(metric)
+            try:
+                v = float(r[j].replace(",", ""))
+            except ValueError:
+                continue
+            u = units[j]
+            if key == "time_ms":
+                v *= SCALE.get(u, 1.0)
+            elif key.startswith("dram_") and key != "dram_pct_peak":
+                v *= BYTES.get(u, 1.0)
+            d[key] = v
+        res.append(d)
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--tag", default="r01")
+    ap.add_argument("--launches")
+    ap.add_argument("--reps", nargs="*", default=[])
+    args = ap.parse_args()
+    prof = ROOT / "profiles"
+    prof.mkdir(exist_ok=True)
+    if args.launches:
+        text = launches(Path(args.launches), args.tag)
+        (prof / f"{args.tag}_launches_summary.md").write_text(text)
+        print(text)
+    kernels = []
+    for rp in args.reps:
+        kernels += report(Path(rp))
+    if kernels:
+        (prof / f"{args.tag}_ncu_kernels.json").write_text(json.dumps(kernels, indent=1))
+        for k in kernels:
+            print(json.dumps(k))
+
+
+if __name__ == "__main__":
+    main()
