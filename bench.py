@@ -112,28 +112,47 @@ def measured_peaks() -> dict:
 
 
 # ------------------------------------------------------- algorithmic work
+def gather_launch_bytes(n: int, batch: int, length: int, m: int, gemm_esz: int) -> float:
+    """Compulsory HBM bytes of the gather-backward launch for child width m.
+
+    Child span (i, i+m) reads, per parent, a sibling row and the parent's LQ
+    row.  Over one launch the left siblings b[w-m][i+m], the right siblings
+    a[i-s][s] and the parents (every span wider than m) are each a bijection
+    onto the S_m = (l-m)(l-m+1)/2 spans of width > m (resp. < l-m+1), and
+    every parent row is shared by its left and right child, so the launch
+    must read 3 * S_m distinct fp32 rows; plus the child's own a, b rows
+    (the -inf guard) and its 2N-wide G row written in the operand type."""
+    l = length
+    s_m = (l - m) * (l - m + 1) // 2
+    n_m = l - m + 1
+    return batch * (3 * s_m * n * 4.0 + n_m * (2 * n * 4.0 + 2 * n * gemm_esz))
+
+
+def split_launch_bytes(n: int, batch: int, length: int, w: int, gemm_esz: int) -> float:
+    """Compulsory HBM bytes of the split-contraction launch for width w: every
+    (span, split) pair reads the distinct rows a[m][i] and b[w-m][i+m]; the
+    span's E row is written in the operand type (none at the top width)."""
+    n_w = length - w + 1
+    return batch * n_w * (2 * (w - 1) * n * 4.0 + (n * gemm_esz if w < length else 0))
+
+
 def algorithmic_work(n: int, p: int, batch: int, length: int, gemm_esz: int, store_o: bool):
     """Per-class algorithmic flops / bytes of one fwd+bwd step.
 
     GEMM flops count only the live blocks: width 1 contracts over P, widths
-    2..l-1 over N; dgrad and wgrad repeat the forward count.  Split bytes are
-    the compulsory HBM bytes of the fp32 chart vectors each kernel must read
-    plus the vectors it writes, with no cross-launch reuse assumed."""
+    2..l-1 over N; dgrad and wgrad repeat the forward count.  Bandwidth-kernel
+    bytes are the compulsory HBM bytes of each launch (split_launch_bytes,
+    gather_launch_bytes): distinct chart rows read once per launch plus the
+    rows written; re-reads across launches are counted, re-reads inside a
+    launch are not."""
     l = length
     rows_w1 = batch * l
     rows_mid = batch * (l * (l - 1) // 2 - 1)          # widths 2..l-1
     f_fwd = 2.0 * rows_w1 * (2 * n) * p + 2.0 * rows_mid * (2 * n) * n
-    s = 4.0  # fp32 chart element
-    pairs = batch * math.comb(l + 1, 3)                # (span, split) pairs
     spans_ge2 = batch * (l * (l - 1) // 2)             # widths 2..l
-    split_bytes = (2 * pairs * n * s                   # a[m] + b[w-m] reads
-                   + spans_ge2 * n * (s if store_o else 0)
-                   + rows_mid * n * gemm_esz)          # E write (operand)
-    # gather backward: each (span, split) pair is visited twice (as left child
-    # and as right child), reading the sibling and the parent's LQ each time;
-    # plus a, b of the row itself and the 2N-wide G row written.
-    rows_bwd = batch * (l * (l + 1) // 2 - 1)          # widths 1..l-1
-    gather_bytes = 4 * pairs * n * s + rows_bwd * (2 * n * s + 2 * n * gemm_esz)
+    split_bytes = (sum(split_launch_bytes(n, batch, l, w, gemm_esz) for w in range(2, l + 1))
+                   + spans_ge2 * n * (4.0 if store_o else 0))
+    gather_bytes = sum(gather_launch_bytes(n, batch, l, m, gemm_esz) for m in range(1, l))
     return {
         "gemm_fwd": ("tensor", f_fwd),
         "gemm_dgrad": ("tensor", f_fwd),
@@ -354,12 +373,18 @@ def run_ours(args, world, rank, local):
             d["unit"] = "GB/s" if b == "hbm" else "TFLOP/s"
             d["frac"] = d["achieved"] / (peaks["hbm_gbs"] if b == "hbm"
                                          else peaks["bf16_tflops_sustained"])
-    traffic = None
+    # DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of one launch
+    # of the dominant class from the committed ncu --set full capture, next
+    # to the compulsory bytes of that same launch (scripts/summarize_profiles.py)
+    traffic, traffic_launch = None, None
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
-        traffic = json.loads(tf.read_text()).get(dominant)
+        traffic_launch = json.loads(tf.read_text()).get(dominant)
+        if traffic_launch:
+            traffic = traffic_launch.get("dram_bytes")
     roofline = {"kernel": dominant, "bound": bound, "achieved": achieved, "peak": peak,
                 "unit": unit, "frac": achieved / peak, "traffic": traffic,
+                "traffic_launch": traffic_launch,
                 "method": "algorithmic work per step / CUDA-event time of the class's launches "
                           "(same K steps re-run with per-launch events)",
                 "peak_source": peaks["source"] + (" sustained" if bound == "tensor" else ""),

@@ -91,9 +91,50 @@ def report(path: Path) -> list[dict]:
     return res
 
 
+def classify(k: dict) -> str | None:
+    name = k["kernel"]
+    if "split_fwd" in name:
+        return "split_fwd"
+    if "gather_bwd" in name:
+        return "gather_bwd"
+    m = re.match(r"k_gemm<[^,]+, \d+, \d, \d, (\d)", name)
+    if m:
+        return {"0": "gemm_fwd", "1": "gemm_dgrad", "2": "gemm_dgrad", "3": "gemm_wgrad"}.get(m.group(1))
+    return None
+
+
+def traffic(kernels: list[dict], n: int, batch: int, length: int, esz: int) -> dict:
+    """Per kernel class: DRAM bytes of the captured launch next to the
+    compulsory (algorithmic) bytes of that same launch (bench.py formulas)."""
+    import sys
+    sys.path.insert(0, str(ROOT))
+    import bench
+    out = {}
+    for k in kernels:
+        cls = classify(k)
+        if cls is None or "dram_read" not in k:
+            continue
+        gy = int(k["grid"].strip("()").split(",")[1])
+        d = {"dram_bytes": k["dram_read"] + k["dram_write"], "time_ms": k["time_ms"],
+             "launch": f"{k['file']} grid {k['grid']}"}
+        if cls in ("split_fwd", "gather_bwd"):
+            width = length - gy // batch + 1
+            fn = bench.split_launch_bytes if cls == "split_fwd" else bench.gather_launch_bytes
+            d["width"] = width
+            d["algorithmic_bytes"] = fn(n, batch, length, width, esz)
+            d["dram_over_algorithmic"] = d["dram_bytes"] / d["algorithmic_bytes"]
+            d["achieved_gbs_under_ncu"] = d["algorithmic_bytes"] / (k["time_ms"] * 1e-3) / 1e9
+        out[cls] = d
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--tag", default="r01")
+    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--length", type=int, default=40)
+    ap.add_argument("--esz", type=int, default=2, help="GEMM operand bytes (bf16 2, tf32 4)")
     ap.add_argument("--launches")
     ap.add_argument("--reps", nargs="*", default=[])
     args = ap.parse_args()
@@ -110,6 +151,9 @@ def main():
         (prof / f"{args.tag}_ncu_kernels.json").write_text(json.dumps(kernels, indent=1))
         for k in kernels:
             print(json.dumps(k))
+        tr = traffic(kernels, args.n, args.batch, args.length, args.esz)
+        (prof / "ncu_traffic.json").write_text(json.dumps(tr, indent=1))
+        print(json.dumps(tr, indent=1))
 
 
 if __name__ == "__main__":
