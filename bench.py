@@ -112,7 +112,8 @@ def measured_peaks() -> dict:
 
 
 # ------------------------------------------------------- algorithmic work
-def gather_launch_bytes(n: int, batch: int, length: int, m: int, gemm_esz: int) -> float:
+def gather_launch_bytes(n: int, batch: int, length: int, m: int, gemm_esz: int,
+                        chart_esz: int = 4) -> float:
     """Compulsory HBM bytes of the gather-backward launch for child width m.
 
     Child span (i, i+m) reads, per parent, a sibling row and the parent's LQ
@@ -120,23 +121,27 @@ def gather_launch_bytes(n: int, batch: int, length: int, m: int, gemm_esz: int) 
     a[i-s][s] and the parents (every span wider than m) are each a bijection
     onto the S_m = (l-m)(l-m+1)/2 spans of width > m (resp. < l-m+1), and
     every parent row is shared by its left and right child, so the launch
-    must read 3 * S_m distinct fp32 rows; plus the child's own a, b rows
-    (the -inf guard) and its 2N-wide G row written in the operand type."""
+    must read 2 * S_m distinct a/b rows (chart_esz bytes per element) and
+    S_m fp32 LQ rows; plus the child's own a, b rows (the -inf guard) and its
+    2N-wide G row written in the operand type."""
     l = length
     s_m = (l - m) * (l - m + 1) // 2
     n_m = l - m + 1
-    return batch * (3 * s_m * n * 4.0 + n_m * (2 * n * 4.0 + 2 * n * gemm_esz))
+    return batch * (s_m * n * (2.0 * chart_esz + 4.0)
+                    + n_m * (2 * n * chart_esz + 2 * n * gemm_esz))
 
 
-def split_launch_bytes(n: int, batch: int, length: int, w: int, gemm_esz: int) -> float:
+def split_launch_bytes(n: int, batch: int, length: int, w: int, gemm_esz: int,
+                       chart_esz: int = 4) -> float:
     """Compulsory HBM bytes of the split-contraction launch for width w: every
     (span, split) pair reads the distinct rows a[m][i] and b[w-m][i+m]; the
     span's E row is written in the operand type (none at the top width)."""
     n_w = length - w + 1
-    return batch * n_w * (2 * (w - 1) * n * 4.0 + (n * gemm_esz if w < length else 0))
+    return batch * n_w * (2 * (w - 1) * n * chart_esz + (n * gemm_esz if w < length else 0))
 
 
-def algorithmic_work(n: int, p: int, batch: int, length: int, gemm_esz: int, store_o: bool):
+def algorithmic_work(n: int, p: int, batch: int, length: int, gemm_esz: int, store_o: bool,
+                     chart_esz: int = 4):
     """Per-class algorithmic flops / bytes of one fwd+bwd step.
 
     GEMM flops count only the live blocks: width 1 contracts over P, widths
@@ -150,9 +155,11 @@ def algorithmic_work(n: int, p: int, batch: int, length: int, gemm_esz: int, sto
     rows_mid = batch * (l * (l - 1) // 2 - 1)          # widths 2..l-1
     f_fwd = 2.0 * rows_w1 * (2 * n) * p + 2.0 * rows_mid * (2 * n) * n
     spans_ge2 = batch * (l * (l - 1) // 2)             # widths 2..l
-    split_bytes = (sum(split_launch_bytes(n, batch, l, w, gemm_esz) for w in range(2, l + 1))
+    split_bytes = (sum(split_launch_bytes(n, batch, l, w, gemm_esz, chart_esz)
+                       for w in range(2, l + 1))
                    + spans_ge2 * n * (4.0 if store_o else 0))
-    gather_bytes = sum(gather_launch_bytes(n, batch, l, m, gemm_esz) for m in range(1, l))
+    gather_bytes = sum(gather_launch_bytes(n, batch, l, m, gemm_esz, chart_esz)
+                       for m in range(1, l))
     return {
         "gemm_fwd": ("tensor", f_fwd),
         "gemm_dgrad": ("tensor", f_fwd),
@@ -284,6 +291,8 @@ def run_ours(args, world, rank, local):
     for t in (L, R, root, unary):
         t.requires_grad_(True)
     lib = _lib.load()
+    chart_fmt = int(_lib.chart_layout(_lib.shape(n, n, batch, length, args.gemm_dtype, False,
+                                                 args.chart_dtype)).chart_fmt)
 
     def allreduce(dL, dR, droot):
         if world == 1:
@@ -296,7 +305,8 @@ def run_ours(args, world, rank, local):
         droot.copy_(flat[2 * k:].view_as(droot))
 
     def step(Li, Ri, rooti, unaryi):
-        log_z = inside(Li, Ri, rooti, unaryi, lengths, gemm_dtype=args.gemm_dtype)
+        log_z = inside(Li, Ri, rooti, unaryi, lengths, gemm_dtype=args.gemm_dtype,
+                       chart_dtype=args.chart_dtype)
         loss = -log_z.mean()                          # train.py:218: d loss = -1/B
         dL, dR, droot, dun = torch.autograd.grad(loss, [Li, Ri, rooti, unaryi])
         allreduce(dL, dR, droot)
@@ -349,7 +359,8 @@ def run_ours(args, world, rank, local):
     # ---- roofline of the dominant kernel class
     peaks = measured_peaks()
     esz = 4 if args.gemm_dtype == "tf32" else 2
-    work = algorithmic_work(n, n, batch, length, esz, store_o=False)
+    chart_esz = 2 if chart_fmt == _lib.FI_CHART_F16 else 4
+    work = algorithmic_work(n, n, batch, length, esz, store_o=False, chart_esz=chart_esz)
     per_class = {}
     for name, (tot_ms, cnt) in prof.items():
         if cnt:
@@ -400,8 +411,10 @@ def run_ours(args, world, rank, local):
             "metric": METRIC, "value": value, "unit": "sentences/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
-            "dtype": "fp32 chart, " + {"bf16": "bf16", "tf32": "tf32",
-                                       "fp32": "bf16x3 (fp32-accurate)"}[args.gemm_dtype]
+            "dtype": ("fp16 linear a/b chart (fp32 o, lq, accumulators)" if chart_esz == 2
+                      else "fp32 chart") + ", "
+                     + {"bf16": "bf16", "tf32": "tf32",
+                        "fp32": "bf16x3 (fp32-accurate)"}[args.gemm_dtype]
                      + " GEMM operands, fp32 accumulate",
             "data": "synthetic: random_grammar(GrammarDims(N,N,64), seed=0) Dirichlet(1) rows; "
                     "uniform tokens default_rng(1+rank)",
@@ -409,6 +422,7 @@ def run_ours(args, world, rank, local):
                                    f"length {length}, batch {batch} per GPU, fwd+bwd",
                        "n_nt": n, "n_pt": n, "length": length, "batch_per_gpu": batch,
                        "global_batch": batch * world, "gemm_dtype": args.gemm_dtype,
+                       "chart_dtype": "fp16" if chart_esz == 2 else "fp32",
                        "parallelism": f"dp{world}",
                        "l2": "working set ~4 GB chart per step >> 126 MB L2 (no flush needed)"},
             "clocks": clk,
@@ -504,6 +518,7 @@ def main(argv=None):
     ap.add_argument("--batch", type=int, default=None, help="sentences per GPU (weak) / "
                     "global (strong); default: the config's batch")
     ap.add_argument("--gemm-dtype", choices=["bf16", "tf32", "fp32"], default="bf16")
+    ap.add_argument("--chart-dtype", choices=["auto", "fp32", "fp16"], default="auto")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -54,6 +54,12 @@ extern "C" {
 #define FI_GEMM_FP32 2 /* "fp32 mode": bf16x3 split operands (hi*hi + lo*hi +
                           hi*lo), ~2^-16 relative per product, fp32 accumulate */
 
+/* Storage of the projected chart vectors a[w], b[w] between the projection
+ * GEMM and the bandwidth-bound split kernels (see fi_chart_layout). */
+#define FI_CHART_AUTO 0 /* fp16 linear with bf16/tf32 GEMM operands, fp32 log in fp32 mode */
+#define FI_CHART_F32 1  /* fp32 base-2 log offsets a^ = log2(acc)                         */
+#define FI_CHART_F16 2  /* fp16 linear acc * 2^14 (acc = (E W^T) in [0, 1])               */
+
 typedef struct fi_shape {
   int32_t n_nt;        /* N */
   int32_t n_pt;        /* P */
@@ -61,6 +67,7 @@ typedef struct fi_shape {
   int32_t max_len;     /* l */
   int32_t gemm_dtype;  /* FI_GEMM_BF16 | FI_GEMM_TF32 | FI_GEMM_FP32 */
   int32_t store_chart; /* 1: keep o[w] for every span (chart export, marginals) */
+  int32_t chart_dtype; /* FI_CHART_AUTO | FI_CHART_F32 | FI_CHART_F16 */
 } fi_shape;
 
 /* Byte offsets of the chart arrays inside the workspace, for chart export.
@@ -70,7 +77,9 @@ typedef struct fi_shape {
  * Storage is base-2 and shifted: the natural-log value of a chart entry is
  *   ln2 * (x[row] + stored[row, A])
  * with x[row] the fp64 per-span shift (off_x) and the stored fp32 offsets
- * a^, b^, o^ (o^ <= 0) and, after a backward, lq^ = log2|go| - log2 o + x. */
+ * a^, b^, o^ (o^ <= 0) and, after a backward, lq^ = log2|go| - log2 o + x.
+ * With chart_fmt == FI_CHART_F16 the a/b arrays hold fp16 s = acc * 2^14
+ * (row stride np halves), i.e. a^ = log2(s) - 14. */
 typedef struct fi_chart_layout {
   int64_t np;       /* padded N (row stride, floats)          */
   int64_t pp;       /* padded P                               */
@@ -81,6 +90,7 @@ typedef struct fi_chart_layout {
   int64_t off_x;    /* x†    fp64 per row (log2 units)        */
   int64_t off_lq;   /* log|go|-o, widths 2..l (after backward)*/
   int64_t off_flag; /* int32 error flags (bit0: non-finite logZ in backward) */
+  int64_t chart_fmt; /* FI_CHART_F32 or FI_CHART_F16: storage of a, b     */
 } fi_chart_layout;
 
 /* Workspace bytes needed for `shape` (0 on invalid shape). */
@@ -132,6 +142,9 @@ int64_t fi_launch_count(void);
 #define FI_PROF_NCLASS 7
 void fi_profile_enable(int32_t on);
 int fi_profile_collect(float* ms, int32_t* counts, int32_t n);
+/* Same record, per launch in issue order: ms[k] and class cls[k] for the
+ * first n launches; returns the number of recorded launches and clears. */
+int fi_profile_collect_launches(float* ms, int32_t* cls, int32_t n);
 
 const char* fi_last_error(void);
 int32_t fi_version(void);

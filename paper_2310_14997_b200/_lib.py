@@ -19,11 +19,15 @@ FI_ERR_UNSUPPORTED = 3
 FI_GEMM_BF16 = 0
 FI_GEMM_TF32 = 1
 FI_GEMM_FP32 = 2
+FI_CHART_AUTO = 0
+FI_CHART_F32 = 1
+FI_CHART_F16 = 2
 
 PROF_CLASSES = ("prep", "split_fwd", "gemm_fwd", "seed", "gather_bwd", "gemm_dgrad",
                 "gemm_wgrad")
 
 GEMM_DTYPES = {"bf16": FI_GEMM_BF16, "tf32": FI_GEMM_TF32, "fp32": FI_GEMM_FP32}
+CHART_DTYPES = {"auto": FI_CHART_AUTO, "fp32": FI_CHART_F32, "fp16": FI_CHART_F16}
 
 
 class FiShape(Structure):
@@ -34,6 +38,7 @@ class FiShape(Structure):
         ("max_len", c_int32),
         ("gemm_dtype", c_int32),
         ("store_chart", c_int32),
+        ("chart_dtype", c_int32),
     ]
 
 
@@ -48,6 +53,7 @@ class FiChartLayout(Structure):
         ("off_x", c_int64),
         ("off_lq", c_int64),
         ("off_flag", c_int64),
+        ("chart_fmt", c_int64),
     ]
 
 
@@ -70,6 +76,7 @@ SIGNATURES = [
     ("fi_launch_count", c_int64, []),
     ("fi_profile_enable", None, [c_int32]),
     ("fi_profile_collect", c_int32, [POINTER(c_float), POINTER(c_int32), c_int32]),
+    ("fi_profile_collect_launches", c_int32, [POINTER(c_float), POINTER(c_int32), c_int32]),
     ("fi_last_error", c_char_p, []),
     ("fi_version", c_int32, []),
 ]
@@ -111,11 +118,13 @@ def check(code: int) -> None:
 
 
 def shape(n_nt: int, n_pt: int, batch: int, max_len: int, gemm_dtype: str = "bf16",
-          store_chart: bool = False) -> FiShape:
+          store_chart: bool = False, chart_dtype: str = "auto") -> FiShape:
     if gemm_dtype not in GEMM_DTYPES:
         raise ValueError(f"gemm_dtype must be one of {sorted(GEMM_DTYPES)}, got {gemm_dtype!r}")
+    if chart_dtype not in CHART_DTYPES:
+        raise ValueError(f"chart_dtype must be one of {sorted(CHART_DTYPES)}, got {chart_dtype!r}")
     return FiShape(int(n_nt), int(n_pt), int(batch), int(max_len), GEMM_DTYPES[gemm_dtype],
-                   1 if store_chart else 0)
+                   1 if store_chart else 0, CHART_DTYPES[chart_dtype])
 
 
 def workspace_bytes(s: FiShape) -> int:
@@ -142,3 +151,11 @@ def profile_collect() -> dict:
     cnt = (c_int32 * n)()
     check(load().fi_profile_collect(ms, cnt, n))
     return {name: (float(ms[i]), int(cnt[i])) for i, name in enumerate(PROF_CLASSES)}
+
+
+def profile_collect_launches(max_launches: int = 65536) -> list[tuple[str, float]]:
+    """[(class, ms)] per recorded launch in issue order (synchronizes, clears)."""
+    ms = (c_float * max_launches)()
+    cls = (c_int32 * max_launches)()
+    k = load().fi_profile_collect_launches(ms, cls, max_launches)
+    return [(PROF_CLASSES[cls[i]], float(ms[i])) for i in range(min(k, max_launches))]

@@ -113,7 +113,7 @@ struct Plan {
   size_t wnn, wnp, e1, eall, gall, a, b, o, lq, x, top, topz, wsum, flag, total;
   // element offsets of the lo planes of the GEMM operands (fp32 mode only)
   long long wnn_lo, wnp_lo, e1_lo, eall_lo, gall_lo;
-  bool store_o, tf32, split;
+  bool store_o, tf32, split, half_chart;
 };
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -148,6 +148,9 @@ int make_plan(const fi_shape* s, Plan* p) {
   if (s->gemm_dtype != FI_GEMM_BF16 && s->gemm_dtype != FI_GEMM_TF32 &&
       s->gemm_dtype != FI_GEMM_FP32)
     return set_err(FI_ERR_ARG, "unknown gemm_dtype %d", s->gemm_dtype);
+  if (s->chart_dtype != FI_CHART_AUTO && s->chart_dtype != FI_CHART_F32 &&
+      s->chart_dtype != FI_CHART_F16)
+    return set_err(FI_ERR_ARG, "unknown chart_dtype %d", s->chart_dtype);
   if (s->n_nt > 16384 || s->n_pt > 16384)
     return set_err(FI_ERR_UNSUPPORTED, "symbol counts above 16384 are not supported");
   if (s->max_len > 1024)  // per-span term tables live in shared memory
@@ -161,16 +164,28 @@ int make_plan(const fi_shape* s, Plan* p) {
   p->tf32 = s->gemm_dtype == FI_GEMM_TF32;
   p->split = s->gemm_dtype == FI_GEMM_FP32;
   p->esz = p->tf32 ? 4 : 2;
+  p->half_chart = s->chart_dtype == FI_CHART_F16 ||
+                  (s->chart_dtype == FI_CHART_AUTO && s->gemm_dtype != FI_GEMM_FP32);
   const int planes = p->split ? 2 : 1;
   p->store_o = s->store_chart != 0;
   // column decomposition of a span row for the bandwidth kernels: C CTAs
   // (a thread-block cluster for the split contraction's row max), each
-  // `threads` consumer threads x V float4 columns.  Measured on B200 at
-  // N = 4096 (bench sweeps): split C = 2 / 4-deep ring, gather C = 4 /
-  // 6-deep ring.  FI_CLUSTER / FI_GCLUSTER / FI_STAGES / FI_GSTAGES override.
-  FI_TRY(make_decomp(p->Np, p->Np <= 1024 ? 1 : 2, "FI_CLUSTER", "FI_STAGES", 4, &p->dsplit));
-  FI_TRY(make_decomp(p->Np, p->Np <= 1024 ? 1 : (p->Np / 1024 < 8 ? p->Np / 1024 : 8),
-                     "FI_GCLUSTER", "FI_GSTAGES", 6, &p->dgather));
+  // `threads` consumer threads x V 4-column groups.  C is sized by the bytes
+  // a CTA streams per term: ~8 KB per a/b row chunk in the split contraction,
+  // ~4 KB per sibling chunk in the gather (measured on B200 at N = 4096:
+  // fp32 chart split C = 2 / gather C = 4, fp16 chart split C = 1 / gather
+  // C = 2).  FI_CLUSTER / FI_GCLUSTER / FI_STAGES / FI_GSTAGES override.
+  const int cesz = p->half_chart ? 2 : 4;
+  auto pick_c = [&](int bytes) {
+    int c = p->Np * cesz / bytes;
+    const int cmin = (p->Np + 4095) / 4096;  // V <= 4
+    c = c < cmin ? cmin : c;
+    c = c < 1 ? 1 : (c > 8 ? 8 : c);
+    while (c > 1 && p->Np % (c * 256)) --c;
+    return c;
+  };
+  FI_TRY(make_decomp(p->Np, pick_c(8192), "FI_CLUSTER", "FI_STAGES", 4, &p->dsplit));
+  FI_TRY(make_decomp(p->Np, pick_c(4096), "FI_GCLUSTER", "FI_GSTAGES", 6, &p->dgather));
   p->rows = rowbase(p->l, p->B, p->l) + p->B;
   const long long rows = p->rows;
   if (static_cast<long long>(p->B) * p->l > 65535 || rows > (1LL << 30))
@@ -190,8 +205,9 @@ int make_plan(const fi_shape* s, Plan* p) {
   p->e1 = plane(1LL * p->B * p->l * p->Pp, &p->e1_lo);
   p->eall = plane(rows * p->Np, &p->eall_lo);
   p->gall = plane(2LL * rows * p->Np, &p->gall_lo);
-  p->a = take(4ull * rows * p->Np);
-  p->b = take(4ull * rows * p->Np);
+  const size_t ab_esz = p->half_chart ? 2 : 4;
+  p->a = take(ab_esz * rows * p->Np);
+  p->b = take(ab_esz * rows * p->Np);
   p->o = p->store_o ? take(4ull * rows * p->Np) : static_cast<size_t>(-1);
   p->lq = take(4ull * rows * p->Np);
   p->x = take(8ull * rows);  // fp64 row shifts
@@ -300,7 +316,7 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
   const int tiles = sh.num_m * sh.num_n;
   const int grid = tiles < num_sms() ? tiles : num_sms();
   if (grid <= 0) return FI_OK;
-  ProfScope prof(EPI == EPI_FWD ? FI_PROF_GEMM_FWD
+  ProfScope prof(EPI == EPI_FWD || EPI == EPI_FWD_H ? FI_PROF_GEMM_FWD
                  : EPI == EPI_WGRAD ? FI_PROF_GEMM_WGRAD
                  : EPI == EPI_STORE ? FI_PROF_PREP : FI_PROF_GEMM_DGRAD, st);
   kern<<<grid, 256, Cf::SMEM_BYTES, st>>>(ta, tb, ta2, tb2, sh, ep);
@@ -345,15 +361,6 @@ int run_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_row0
   return run_gemm_s<T, AMN, BMN, EPI, false>(A, B, M, N, K, a_row0, ep, st);
 }
 
-// Bandwidth-kernel variant: TMA-bulk shared-memory ring (default) or the
-// register-pipelined kernels (FI_BULK=0), and the ring depth (FI_STAGES).
-bool use_bulk() {
-  static int v = [] {
-    const char* e = getenv("FI_BULK");
-    return e ? atoi(e) : 1;
-  }();
-  return v != 0;
-}
 template <int V>
 using VC = std::integral_constant<int, V>;
 template <typename F>
@@ -400,15 +407,16 @@ int check_ptrs(std::initializer_list<const void*> ps) {
 }
 
 // ------------------------------------------------------------------ forward
-template <typename T>
+template <typename T, typename CT>
 int forward_impl(const Plan& p, const float* L, const float* R, const float* root,
                  const float* unary, const int* lengths, float* logZ, void* ws,
                  cudaStream_t st) {
+  constexpr int kEpiFwd = sizeof(CT) == 2 ? EPI_FWD_H : EPI_FWD;
   T* wnn = at<T>(ws, p.wnn);
   T* wnp = at<T>(ws, p.wnp);
   T* e1 = at<T>(ws, p.e1);
   T* eall = at<T>(ws, p.eall);
-  float* A = at<float>(ws, p.a);
+  float* A = at<float>(ws, p.a);   // CT storage; GemmEpi / SplitArgs carry it untyped
   float* Bc = at<float>(ws, p.b);
   float* O = p.store_o ? at<float>(ws, p.o) : nullptr;
   double* X = at<double>(ws, p.x);
@@ -443,7 +451,7 @@ int forward_impl(const Plan& p, const float* L, const float* R, const float* roo
   ep.Np = p.Np;
   ep.M = p.B * p.l;
   ep.row0 = 0;
-  FI_TRY((run_gemm<T, false, false, EPI_FWD>(opE1, opWnp, ep.M, 2 * p.Np, p.Pp, 0, ep, st)));
+  FI_TRY((run_gemm<T, false, false, kEpiFwd>(opE1, opWnp, ep.M, 2 * p.Np, p.Pp, 0, ep, st)));
 
   for (int w = 2; w <= p.l; ++w) {
     const int n_w = p.l - w + 1;
@@ -470,30 +478,21 @@ int forward_impl(const Plan& p, const float* L, const float* R, const float* roo
     const dim3 grid(dc.clusters, p.B * n_w);
     {
       ProfScope prof(FI_PROF_SPLIT, st);
-      if (use_bulk()) {
-        const int stages = dc.stages;
-        const size_t smem = align128(sizeof(SplitTerm) * (w - 1)) +
-                            static_cast<size_t>(stages) * (2 * dc.cols_per_cta * 4 + 16);
-        const dim3 block(32 + dc.threads);
-        FI_TRY(dispatch_v(dc.v, [&](auto vc) {
-          constexpr int V = decltype(vc)::value;
-          FI_TRY(set_smem(k_split_fwd_bulk<T, V>, smem));
-          return launch_cluster(k_split_fwd_bulk<T, V>, dc.clusters, grid, block, smem, st, sa,
-                                stages);
-        }));
-      } else {
-        const size_t smem = sizeof(SplitTerm) * (w - 1);
-        FI_TRY(dispatch_v(dc.v, [&](auto vc) {
-          constexpr int V = decltype(vc)::value;
-          return launch_cluster(k_split_fwd<T, V>, dc.clusters, grid, dim3(dc.threads), smem, st,
-                                sa);
-        }));
-      }
+      const int stages = dc.stages;
+      const size_t smem = align128(sizeof(SplitTerm) * (w - 1)) +
+                          static_cast<size_t>(stages) * (2 * dc.cols_per_cta * sizeof(CT) + 16);
+      const dim3 block(32 + dc.threads);
+      FI_TRY(dispatch_v(dc.v, [&](auto vc) {
+        constexpr int V = decltype(vc)::value;
+        FI_TRY(set_smem(k_split_fwd_bulk<T, CT, V>, smem));
+        return launch_cluster(k_split_fwd_bulk<T, CT, V>, dc.clusters, grid, block, smem, st, sa,
+                              stages);
+      }));
     }
     if (w < p.l) {
       ep.M = p.B * n_w;
       ep.row0 = rowbase(w, p.B, p.l);
-      FI_TRY((run_gemm<T, false, false, EPI_FWD>(opEall, opWnn, ep.M, 2 * p.Np, p.Np,
+      FI_TRY((run_gemm<T, false, false, kEpiFwd>(opEall, opWnn, ep.M, 2 * p.Np, p.Np,
                                                   static_cast<int>(ep.row0), ep, st)));
     }
   }
@@ -501,7 +500,7 @@ int forward_impl(const Plan& p, const float* L, const float* R, const float* roo
 }
 
 // ----------------------------------------------------------------- backward
-template <typename T>
+template <typename T, typename CT>
 int backward_impl(const Plan& p, const float* L, const float* R, const float* root,
                   const float* unary, const int* lengths, const float* logZ, const float* g,
                   float* dL, float* dR, float* droot, float* dunary, void* ws, cudaStream_t st) {
@@ -552,24 +551,15 @@ int backward_impl(const Plan& p, const float* L, const float* R, const float* ro
     const dim3 grid(dc.clusters, p.B * n_m);
     {
       ProfScope prof(FI_PROF_GATHER, st);
-      if (use_bulk()) {
-        const int stages = dc.stages;
-        const size_t smem = align128(sizeof(GatherTerm) * p.l) +
-                            static_cast<size_t>(stages) * (2 * dc.cols_per_cta * 4 + 16);
-        FI_TRY(dispatch_v(dc.v, [&](auto vc) {
-          constexpr int V = decltype(vc)::value;
-          FI_TRY(set_smem(k_gather_bwd_bulk<T, V>, smem));
-          k_gather_bwd_bulk<T, V><<<grid, 32 + dc.threads, smem, st>>>(ga, stages);
-          return FI_OK;
-        }));
-      } else {
-        const size_t smem = sizeof(GatherTerm) * p.l;
-        FI_TRY(dispatch_v(dc.v, [&](auto vc) {
-          constexpr int V = decltype(vc)::value;
-          k_gather_bwd<T, V><<<grid, dc.threads, smem, st>>>(ga);
-          return FI_OK;
-        }));
-      }
+      const int stages = dc.stages;
+      const size_t smem = align128(sizeof(GatherTerm) * p.l) +
+                          static_cast<size_t>(stages) * (dc.cols_per_cta * (sizeof(CT) + 4) + 16);
+      FI_TRY(dispatch_v(dc.v, [&](auto vc) {
+        constexpr int V = decltype(vc)::value;
+        FI_TRY(set_smem(k_gather_bwd_bulk<T, CT, V>, smem));
+        k_gather_bwd_bulk<T, CT, V><<<grid, 32 + dc.threads, smem, st>>>(ga, stages);
+        return FI_OK;
+      }));
     }
     ++g_launches;
     FI_CUDA(cudaGetLastError());
@@ -655,6 +645,7 @@ int fi_get_chart_layout(const fi_shape* shape, fi_chart_layout* out) {
   out->off_x = static_cast<int64_t>(p.x);
   out->off_lq = static_cast<int64_t>(p.lq);
   out->off_flag = static_cast<int64_t>(p.flag);
+  out->chart_fmt = p.half_chart ? FI_CHART_F16 : FI_CHART_F32;
   return FI_OK;
 }
 
@@ -666,8 +657,13 @@ int fi_inside_forward(const fi_shape* shape, const float* L, const float* R, con
   FI_TRY(check_ptrs({L, R, root, unary, lengths, log_z, ws}));
   FI_TRY(load_encode());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (p.tf32) return forward_impl<float>(p, L, R, root, unary, lengths, log_z, ws, st);
-  return forward_impl<__nv_bfloat16>(p, L, R, root, unary, lengths, log_z, ws, st);
+  if (p.tf32) {
+    if (p.half_chart) return forward_impl<float, __half>(p, L, R, root, unary, lengths, log_z, ws, st);
+    return forward_impl<float, float>(p, L, R, root, unary, lengths, log_z, ws, st);
+  }
+  if (p.half_chart)
+    return forward_impl<__nv_bfloat16, __half>(p, L, R, root, unary, lengths, log_z, ws, st);
+  return forward_impl<__nv_bfloat16, float>(p, L, R, root, unary, lengths, log_z, ws, st);
 }
 
 int fi_inside_backward(const fi_shape* shape, const float* L, const float* R, const float* root,
@@ -679,11 +675,16 @@ int fi_inside_backward(const fi_shape* shape, const float* L, const float* R, co
   FI_TRY(check_ptrs({L, R, root, unary, lengths, log_z, grad_log_z, dL, dR, droot, dunary, ws}));
   FI_TRY(load_encode());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (p.tf32)
-    return backward_impl<float>(p, L, R, root, unary, lengths, log_z, grad_log_z, dL, dR, droot,
-                                dunary, ws, st);
-  return backward_impl<__nv_bfloat16>(p, L, R, root, unary, lengths, log_z, grad_log_z, dL, dR,
-                                      droot, dunary, ws, st);
+#define FI_BWD(T, CT)                                                                      \
+  return backward_impl<T, CT>(p, L, R, root, unary, lengths, log_z, grad_log_z, dL, dR, droot, \
+                              dunary, ws, st)
+  if (p.tf32) {
+    if (p.half_chart) FI_BWD(float, __half);
+    FI_BWD(float, float);
+  }
+  if (p.half_chart) FI_BWD(__nv_bfloat16, __half);
+  FI_BWD(__nv_bfloat16, float);
+#undef FI_BWD
 }
 
 int fi_marginals(const fi_shape* shape, const int32_t* lengths, const float* grad_log_z,
@@ -755,6 +756,24 @@ int fi_profile_collect(float* ms, int32_t* counts, int32_t n) {
   g_prof.clear();
   return rc;
 }
+int fi_profile_collect_launches(float* ms, int32_t* cls, int32_t n) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  int k = 0;
+  for (const ProfRec& r : g_prof) {
+    float t = 0.f;
+    if (cudaEventSynchronize(r.b) == cudaSuccess) cudaEventElapsedTime(&t, r.a, r.b);
+    if (k < n) {
+      if (ms) ms[k] = t;
+      if (cls) cls[k] = r.cls;
+    }
+    ++k;
+    g_prof_pool.push_back(r.a);
+    g_prof_pool.push_back(r.b);
+  }
+  g_prof.clear();
+  return k;
+}
+
 const char* fi_last_error(void) { return g_err; }
 int32_t fi_version(void) { return 1; }
 

@@ -26,6 +26,7 @@ enum EpiMode : int {
   EPI_DUNARY = 2,  // dunary = acc * exp(unary - x†) (width-1 go)  (inside.py:420-423)
   EPI_WGRAD = 3,   // d{L,R} = exp({L,R}) * acc                    (inside.py:446)
   EPI_STORE = 4,   // plain C = acc (GEMM unit tests)
+  EPI_FWD_H = 5,   // [a | b] as fp16 acc * 2^kChartScale (half chart, fi_kernels.cuh)
 };
 
 struct GemmShape {
@@ -98,6 +99,21 @@ __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int lrow, long long
       o.z = lg2(v[4 * q + 2]);
       o.w = lg2(v[4 * q + 3]);
       dst[q] = o;
+    }
+  } else if constexpr (EPI == EPI_FWD_H) {
+    // rowptr is a __half row; the linear projection is already the stored value
+    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(rowptr) + col);
+    constexpr float kScale = 16384.f;  // 2^kChartScale
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 u;
+      uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        __half2 p2 = __floats2half2_rn(v[8 * q + 2 * h] * kScale, v[8 * q + 2 * h + 1] * kScale);
+        w[h] = *reinterpret_cast<uint32_t*>(&p2);
+      }
+      dst[q] = u;
     }
   } else if constexpr (EPI == EPI_DGRAD) {
     float4* dst = reinterpret_cast<float4*>(rowptr + col);
@@ -305,6 +321,10 @@ __global__ void __launch_bounds__(256, 1)
             rowptr = ep.outB + grow * ep.Np;
             col_base -= ep.Np;
           }
+        } else if constexpr (EPI == EPI_FWD_H) {
+          __half* base = reinterpret_cast<__half*>(col_base < ep.Np ? ep.outA : ep.outB);
+          rowptr = reinterpret_cast<float*>(base + grow * ep.Np);
+          if (col_base >= ep.Np) col_base -= ep.Np;
         } else if constexpr (EPI == EPI_DGRAD) {
           rowptr = ep.LQ + grow * ep.Np;
         } else if constexpr (EPI == EPI_DUNARY) {

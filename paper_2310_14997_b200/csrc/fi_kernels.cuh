@@ -212,16 +212,70 @@ __global__ void __launch_bounds__(256) k_prep_width1(const float* __restrict__ u
 }
 
 // ---------------------------------------------------------------------------
+// Storage of the projected chart vectors a[w], b[w] (the GEMM forward
+// epilogue's output, the bandwidth kernels' input).  Two formats:
+//   float  : A^ = a - x† = log2(acc), fp32 base-2 log offsets ("fp32 chart",
+//            used in fp32 mode, where every stored value must carry 24 bits)
+//   __half : the LINEAR projection acc = (E W^T)[A] scaled by 2^kChartScale,
+//            fp16 ("half chart", bf16/tf32 modes).  acc = sum_B W[A,B] E[B]
+//            with E <= 1 and W rows summing to <= 1, so acc in [0, 1] and
+//            the stored value in [0, 2^14]: fp16 keeps 11 significant bits
+//            (2^-12 relative, 4x finer than the bf16 GEMM operands) down to
+//            acc = 2^-28, below which terms are < 1e-8 of the row's largest
+//            and flush gracefully.  Half the bytes of the fp32 chart in both
+//            bandwidth-bound kernels, and the split contraction becomes two
+//            FMULs per element instead of an EX2.
+// ---------------------------------------------------------------------------
+constexpr int kChartScale = 14;
+
+template <typename CT>
+__device__ __forceinline__ float4 chart4(const CT* p);  // 4 consecutive values as fp32
+template <>
+__device__ __forceinline__ float4 chart4<float>(const float* p) {
+  return *reinterpret_cast<const float4*>(p);
+}
+template <>
+__device__ __forceinline__ float4 chart4<__half>(const __half* p) {
+  const uint2 u = *reinterpret_cast<const uint2*>(p);
+  const float2 lo = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+  const float2 hi = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+  return make_float4(lo.x, lo.y, hi.x, hi.y);
+}
+template <typename CT>
+__device__ __forceinline__ float4 chart4_ldg(const CT* p);
+template <>
+__device__ __forceinline__ float4 chart4_ldg<float>(const float* p) {
+  return __ldg(reinterpret_cast<const float4*>(p));
+}
+template <>
+__device__ __forceinline__ float4 chart4_ldg<__half>(const __half* p) {
+  uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+  const float2 lo = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+  const float2 hi = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+  return make_float4(lo.x, lo.y, hi.x, hi.y);
+}
+// "zero projection mass" test of one stored value (a = -inf in the reference)
+template <typename CT>
+__device__ __forceinline__ bool is_dead(float v) {
+  if constexpr (sizeof(CT) == 4) return v == kNegInf;
+  else return v == 0.f;
+}
+
+// ---------------------------------------------------------------------------
 // K4/K5: split-point contraction for width w (inside.py:313-332) + logZ
 // (inside.py:124-129).  One cluster of C CTAs per span row; each CTA owns a
-// contiguous chunk of Np/C nonterminal columns, each thread V float4s of it.
-// Online log-sum-exp over the w-1 split points with one exp2 per element;
-// the row max x† is reduced across the cluster through DSMEM, then E is
+// contiguous chunk of Np/C nonterminal columns.  Per split m the
+// a[m][i] and b[w-m][i+m] row chunks are streamed from HBM into a
+// STAGES-deep shared-memory ring with cp.async.bulk (warp 0, one lane:
+// producer) while the consumer warps accumulate from shared memory; mbarrier
+// full/empty pairs hand stages back and forth (~STAGES x 8 KB in flight per
+// CTA with almost no registers, so the kernel sits on the HBM roofline).
+// The row max x† is reduced across the cluster through DSMEM, then E is
 // written in the GEMM operand type.  No (w-1, n, N) stack is materialised.
 // ---------------------------------------------------------------------------
 struct SplitArgs {
-  const float* A;    // A^
-  const float* Bc;   // B^
+  const void* A;     // CT*: a[w] (A^ or scaled linear, see above)
+  const void* Bc;    // CT*: b[w]
   float* O;          // O^ (nullable)
   void* E;           // T*, row stride Np (nullable at w == lmax)
   long long e_lo;    // element offset of the lo plane (fp32 mode), else 0
@@ -239,366 +293,33 @@ struct SplitTerm {
   long long ra, rb;  // chart rows of a[m][i] and b[w-m][i+m]
   double xs;         // x†(a) + x†(b)
   float d;           // xs - D, rounded once from fp64
-  float pad;
+  float c;           // half chart: 2^(d - 2*kChartScale), the term's linear weight
 };
 
 // Every term a[m][i,A] + b[w-m][i+m,A] is bounded by its two row shifts plus
 // the log2 row-sum bounds of the projection blocks (a^ = log2 sum_B W E with
 // E <= 1), so with D = max_m of those bounds every 2^(term - D) <= 1: the
 // log-sum-exp over splits needs no running max -- one FADD pair, one EX2 and
-// one FADD per element and split.  (inside.py:323-331 computes the max first.)
-template <typename T, int V>
-__global__ void __launch_bounds__(256) k_split_fwd(SplitArgs a) {
-  extern __shared__ SplitTerm terms[];  // w - 1 entries
-  __shared__ float red[33];
-  __shared__ float cl_slot, cl_bcast;
-  __shared__ double dred[33];
-  const int w = a.w;
-  const int n_w = a.lmax - w + 1;
-  const int local = blockIdx.y;
-  const int b = local / n_w, i = local % n_w;
-  const int len = a.lengths[b];
-  const long long row = rowbase(w, a.B, a.lmax) + local;
-  const int nthr = blockDim.x;
-  const int col0 = blockIdx.x * a.cols_per_cta + threadIdx.x * 4;
-  T* E = reinterpret_cast<T*>(a.E);
+// one FADD per element and split (fp32 chart), or one FMUL and one FFMA
+// (half chart).  (inside.py:323-331 computes the max first.)
+__host__ __device__ __forceinline__ size_t align128(size_t v) { return (v + 127) & ~size_t(127); }
 
-  // split m of span (i, i+w) pairs a[m][i] with b[w-m][i+m]   (inside.py:317-319)
-  const float lnn = a.wsum[0] > 0.f ? log2f(a.wsum[0]) : 0.f;
-  const float rnn = a.wsum[1] > 0.f ? log2f(a.wsum[1]) : 0.f;
-  const float lnp = a.wsum[2] > 0.f ? log2f(a.wsum[2]) : 0.f;
-  const float rnp = a.wsum[3] > 0.f ? log2f(a.wsum[3]) : 0.f;
-  double ub = -1.0e300;
-  for (int t = threadIdx.x; t < w - 1; t += nthr) {
-    const int m = t + 1;
-    const long long r1 = chart_row(m, b, i, a.B, a.lmax);
-    const long long r2 = chart_row(w - m, b, i + m, a.B, a.lmax);
-    const double xs = a.X[r1] + a.X[r2];
-    terms[t].ra = r1;
-    terms[t].rb = r2;
-    terms[t].xs = xs;
-    ub = fmax(ub, xs + (m == 1 ? lnp : lnn) + (w - m == 1 ? rnp : rnn));
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) ub = fmax(ub, __shfl_xor_sync(0xffffffffu, ub, o));
-  if ((threadIdx.x & 31) == 0) dred[threadIdx.x >> 5] = ub;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double d = dred[0];
-    for (int k = 1; k < (nthr + 31) >> 5; ++k) d = fmax(d, dred[k]);
-    dred[32] = d;
-  }
-  __syncthreads();
-  const double D = dred[32];
-  for (int t = threadIdx.x; t < w - 1; t += nthr) terms[t].d = static_cast<float>(terms[t].xs - D);
-  __syncthreads();
-
-  if (i + w > len) {  // span outside the sentence: never feeds a valid span
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const int c = col0 + v * nthr * 4;
-      if (a.O) *reinterpret_cast<float4*>(a.O + row * a.Np + c) =
-          make_float4(kNegInf, kNegInf, kNegInf, kNegInf);
-      if (E) store4s<T>(E + row * a.Np + c, a.e_lo, 0.f, 0.f, 0.f, 0.f);
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.X[row] = D;
-    return;  // uniform across the cluster (same row)
-  }
-
-  float S[4 * V];
-#pragma unroll
-  for (int k = 0; k < 4 * V; ++k) S[k] = 0.f;
-  int m = 0;
-  for (; m + 3 < w - 1; m += 4) {
-    float4 va[4][V], vb[4][V];
-    float dl[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const SplitTerm tm = terms[m + u];
-      dl[u] = tm.d;
-      const float* pa = a.A + tm.ra * a.Np + col0;
-      const float* pb = a.Bc + tm.rb * a.Np + col0;
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        va[u][v] = ldg4(pa + v * nthr * 4);
-        vb[u][v] = ldg4(pb + v * nthr * 4);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        S[4 * v + 0] += ex2(va[u][v].x + vb[u][v].x + dl[u]);
-        S[4 * v + 1] += ex2(va[u][v].y + vb[u][v].y + dl[u]);
-        S[4 * v + 2] += ex2(va[u][v].z + vb[u][v].z + dl[u]);
-        S[4 * v + 3] += ex2(va[u][v].w + vb[u][v].w + dl[u]);
-      }
-  }
-  for (; m < w - 1; ++m) {
-    const SplitTerm tm = terms[m];
-    const float* pa = a.A + tm.ra * a.Np + col0;
-    const float* pb = a.Bc + tm.rb * a.Np + col0;
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      float4 x = ldg4(pa + v * nthr * 4);
-      float4 y = ldg4(pb + v * nthr * 4);
-      S[4 * v + 0] += ex2(x.x + y.x + tm.d);
-      S[4 * v + 1] += ex2(x.y + y.y + tm.d);
-      S[4 * v + 2] += ex2(x.z + y.z + tm.d);
-      S[4 * v + 3] += ex2(x.w + y.w + tm.d);
-    }
-  }
-  float o[4 * V];  // o - D
-  float mx = kNegInf;
-#pragma unroll
-  for (int k = 0; k < 4 * V; ++k) {
-    o[k] = lg2(S[k]);  // S = 0 -> -inf
-    mx = fmaxf(mx, o[k]);
-  }
-  // row max over all Np columns: block, then cluster (DSMEM)
-  mx = block_reduce<true>(mx, red);
-  mx = cluster_reduce<true>(mx, &cl_slot, &cl_bcast);
-  const float xs = (mx == kNegInf) ? 0.f : mx;  // inside.py:324-326
-#pragma unroll
-  for (int k = 0; k < 4 * V; ++k) o[k] -= xs;    // O^ = o - x†  (<= 0)
-  if (a.O) {
-#pragma unroll
-    for (int v = 0; v < V; ++v)
-      *reinterpret_cast<float4*>(a.O + row * a.Np + col0 + v * nthr * 4) =
-          make_float4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
-  }
-  if (E) {
-#pragma unroll
-    for (int v = 0; v < V; ++v)
-      store4s<T>(E + row * a.Np + col0 + v * nthr * 4, a.e_lo, ex2(o[4 * v]), ex2(o[4 * v + 1]),
-                 ex2(o[4 * v + 2]), ex2(o[4 * v + 3]));
-  }
-  const double xrow = D + static_cast<double>(xs);
-  if (blockIdx.x == 0 && threadIdx.x == 0) a.X[row] = xrow;
-
-  if (i == 0 && w == len) {  // top span: logZ = LSE_A(root[A] + o[A])  (inside.py:124-129)
-    float sc[4 * V];
-    float smx = kNegInf;
-#pragma unroll
-    for (int v = 0; v < V; ++v)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int c = col0 + v * nthr * 4 + k;
-        sc[4 * v + k] = c < a.N ? fmaf(a.root[c], kLog2e, o[4 * v + k]) : kNegInf;
-        a.TOP[static_cast<long long>(b) * a.Np + c] = sc[4 * v + k];
-        smx = fmaxf(smx, sc[4 * v + k]);
-      }
-    smx = block_reduce<true>(smx, red);
-    smx = cluster_reduce<true>(smx, &cl_slot, &cl_bcast);
-    float s = 0.f;
-    if (smx != kNegInf) {
-#pragma unroll
-      for (int k = 0; k < 4 * V; ++k) s += exp2f(sc[k] - smx);
-    }
-    s = block_reduce<false>(s, red);
-    s = cluster_reduce<false>(s, &cl_slot, &cl_bcast);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      const float z = smx == kNegInf ? kNegInf : smx + log2f(s);  // log2 Z - x†
-      a.TOPZ[b] = z;
-      a.logZ[b] = z == kNegInf ? kNegInf : static_cast<float>((xrow + z) * kLn2d);
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Backward seed (inside.py:400-404): the root posterior
-//   post[A] = exp(root[A] + o[len][0, A] - logZ)
-// seeds the outside pass at each sentence's top span as
-//   LQ^ = log2|g post| - o + x† = log2 root - (log2 Z - x†) + log2|g|
-// and is itself d_root (times g).  One thread per column; loops sentences.
-// ---------------------------------------------------------------------------
-__global__ void k_seed_bwd(const float* __restrict__ root, const float* __restrict__ TOP,
-                           const float* __restrict__ TOPZ, const float* __restrict__ g,
-                           const int* __restrict__ lengths, float* __restrict__ LQ,
-                           float* __restrict__ droot, int* __restrict__ flag, int B, int lmax,
-                           int N, int Np) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= Np) return;
-  float acc = 0.f;
-  for (int b = 0; b < B; ++b) {
-    const float z = TOPZ[b];
-    const float gb = g[b];
-    const bool finite = isfinite(z);
-    if (!finite && c == 0) atomicOr(flag, 1);
-    float lq = kNegInf;
-    if (finite && gb != 0.f && c < N) {
-      lq = fmaf(root[c], kLog2e, -z) + log2f(fabsf(gb));
-      acc += gb * exp2f(TOP[static_cast<long long>(b) * Np + c] - z);
-    }
-    LQ[chart_row(lengths[b], b, 0, B, lmax) * Np + c] = lq;
-  }
-  if (c < N) droot[c] = acc;
-}
-
-// ---------------------------------------------------------------------------
-// K7: gather-form split backward for child width m (inside.py:406-417).
-// For span (i, i+m) of sentence b (row r), with the outside weight
-// LQ = log2|go| - o of each parent:
-//   G_L = [a != -inf] * sum_{w>m}  2^(x†_r + b[w-m][i+m] + LQ[w][i])
-//   G_R = [b != -inf] * sum_{s<i}  2^(x†_r + a[i-s][s]   + LQ[i+m-s][s])
-// which is ga*exp(x† - a) (resp. gb*exp(x† - b)) of the reference -- the row
-// of the dgrad/wgrad GEMM operand -- because the a (resp. b) factor of the
-// split softmax exp(a + b - o) cancels against exp(-a).  With the shifted
-// storage each term is 2^(d + B^ + LQ^), d an fp64 per-term scalar.
-// Each accumulator is written once: deterministic, no atomics.
-// ---------------------------------------------------------------------------
-struct GatherArgs {
-  const float* A;
-  const float* Bc;
-  const float* LQ;
-  const double* X;
-  void* G;  // T*, row stride 2*Np
-  long long g_lo;
-  const int* lengths;
-  const float* g;
-  int B, lmax, Np, m, cols_per_cta;
-};
-
-struct GatherTerm {
-  long long rs, rp;  // chart rows of the sibling and of the parent
-  float d;           // x†(child) + x†(sibling) - x†(parent), rounded from fp64
-  float pad;
-};
-
-template <typename T, int V>
-__global__ void __launch_bounds__(256) k_gather_bwd(GatherArgs a) {
-  extern __shared__ GatherTerm gterms[];  // <= lmax entries: G_L terms then G_R terms
-  const int m = a.m;
-  const int n_m = a.lmax - m + 1;
-  const int local = blockIdx.y;
-  const int b = local / n_m, i = local % n_m;
-  const int len = a.lengths[b];
-  const long long row = rowbase(m, a.B, a.lmax) + local;
-  const int nthr = blockDim.x;
-  const int col0 = blockIdx.x * a.cols_per_cta + threadIdx.x * 4;
-  T* G = reinterpret_cast<T*>(a.G) + row * (2LL * a.Np);
-
-  if (i + m > len) {
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const int c = col0 + v * nthr * 4;
-      store4s<T>(G + c, a.g_lo, 0.f, 0.f, 0.f, 0.f);
-      store4s<T>(G + a.Np + c, a.g_lo, 0.f, 0.f, 0.f, 0.f);
-    }
-    return;
-  }
-  // left child (i, i+m) of parent (i, i+w), w = m+1..len-i: sibling b[w-m][i+m]
-  // right child (i, i+m) of parent (s, i+m), s = 0..i-1:    sibling a[i-s][s]
-  const int n_left = len - i - m;
-  const int n_all = n_left + i;
-  const double xm = a.X[row];
-  for (int t = threadIdx.x; t < n_all; t += nthr) {
-    long long rs, rp;
-    if (t < n_left) {
-      const int w = m + 1 + t;
-      rs = chart_row(w - m, b, i + m, a.B, a.lmax);
-      rp = chart_row(w, b, i, a.B, a.lmax);
-    } else {
-      const int sidx = t - n_left;
-      rs = chart_row(i - sidx, b, sidx, a.B, a.lmax);
-      rp = chart_row(i + m - sidx, b, sidx, a.B, a.lmax);
-    }
-    gterms[t].rs = rs;
-    gterms[t].rp = rp;
-    gterms[t].d = static_cast<float>(xm + a.X[rs] - a.X[rp]);
-  }
-  __syncthreads();
-
-  float gl[4 * V], gr[4 * V];
-#pragma unroll
-  for (int k = 0; k < 4 * V; ++k) gl[k] = gr[k] = 0.f;
-  // one pass over both term lists; each term is 2^(d + sibling^ + LQ^)
-  auto run = [&](const float* sib, int t0, int t1, float (&acc)[4 * V]) {
-    int t = t0;
-    for (; t + 1 < t1; t += 2) {
-      float4 vs[2][V], vq[2][V];
-      float d[2];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const GatherTerm tm = gterms[t + u];
-        d[u] = tm.d;
-        const float* ps = sib + tm.rs * a.Np + col0;
-        const float* pq = a.LQ + tm.rp * a.Np + col0;
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-          vs[u][v] = ldg4(ps + v * nthr * 4);
-          vq[u][v] = ldg4(pq + v * nthr * 4);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 2; ++u)
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-          acc[4 * v + 0] += ex2(vs[u][v].x + vq[u][v].x + d[u]);
-          acc[4 * v + 1] += ex2(vs[u][v].y + vq[u][v].y + d[u]);
-          acc[4 * v + 2] += ex2(vs[u][v].z + vq[u][v].z + d[u]);
-          acc[4 * v + 3] += ex2(vs[u][v].w + vq[u][v].w + d[u]);
-        }
-    }
-    for (; t < t1; ++t) {
-      const GatherTerm tm = gterms[t];
-      const float* ps = sib + tm.rs * a.Np + col0;
-      const float* pq = a.LQ + tm.rp * a.Np + col0;
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        float4 x = ldg4(ps + v * nthr * 4);
-        float4 q = ldg4(pq + v * nthr * 4);
-        acc[4 * v + 0] += ex2(x.x + q.x + tm.d);
-        acc[4 * v + 1] += ex2(x.y + q.y + tm.d);
-        acc[4 * v + 2] += ex2(x.z + q.z + tm.d);
-        acc[4 * v + 3] += ex2(x.w + q.w + tm.d);
-      }
-    }
-  };
-  run(a.Bc, 0, n_left, gl);
-  run(a.A, n_left, n_all, gr);
-
-  // zero-mass projections carry no gradient (inside.py:441-443 NaN guard)
-  const float sg = a.g[b] < 0.f ? -1.f : 1.f;
-  const float* pam = a.A + row * a.Np;
-  const float* pbm = a.Bc + row * a.Np;
-#pragma unroll
-  for (int v = 0; v < V; ++v) {
-    const int c = col0 + v * nthr * 4;
-    float4 am = ldg4(pam + c), bm = ldg4(pbm + c);
-    store4s<T>(G + c, a.g_lo, am.x == kNegInf ? 0.f : sg * gl[4 * v + 0],
-               am.y == kNegInf ? 0.f : sg * gl[4 * v + 1], am.z == kNegInf ? 0.f : sg * gl[4 * v + 2],
-               am.w == kNegInf ? 0.f : sg * gl[4 * v + 3]);
-    store4s<T>(G + a.Np + c, a.g_lo, bm.x == kNegInf ? 0.f : sg * gr[4 * v + 0],
-               bm.y == kNegInf ? 0.f : sg * gr[4 * v + 1], bm.z == kNegInf ? 0.f : sg * gr[4 * v + 2],
-               bm.w == kNegInf ? 0.f : sg * gr[4 * v + 3]);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// TMA-bulk pipelined variants of the split contraction and the gather.
-// Both kernels stream, per term, two contiguous row chunks (Np/C floats each)
-// from HBM into a STAGES-deep shared-memory ring with cp.async.bulk
-// (warp 0, one lane: producer) while warps 1.. consume them from shared
-// memory; mbarrier full/empty pairs hand stages back and forth.  This keeps
-// ~STAGES * 8 KB in flight per CTA with almost no registers, so the kernels
-// sit on the HBM roofline instead of the load-latency limit of the
-// register-pipelined versions above.
-// ---------------------------------------------------------------------------
 struct BulkRing {
-  float* buf;       // stages x (2 x cpc) floats
+  uint8_t* buf;     // stages x stage_bytes
   uint64_t* full;   // stages
   uint64_t* empty;  // stages
-  int stages, cpc;
+  int stages, stage_bytes, off1;
 };
 
-__device__ __forceinline__ BulkRing carve_ring(uint8_t* base, int stages, int cpc) {
+__device__ __forceinline__ BulkRing carve_ring(uint8_t* base, int stages, int bytes0,
+                                               int bytes1) {
   BulkRing r;
-  r.buf = reinterpret_cast<float*>(base);
-  r.full = reinterpret_cast<uint64_t*>(base + static_cast<size_t>(stages) * 2 * cpc * 4);
+  r.buf = base;
+  r.stage_bytes = bytes0 + bytes1;
+  r.off1 = bytes0;
+  r.full = reinterpret_cast<uint64_t*>(base + static_cast<size_t>(stages) * r.stage_bytes);
   r.empty = r.full + stages;
   r.stages = stages;
-  r.cpc = cpc;
   return r;
 }
 
@@ -613,10 +334,9 @@ __device__ __forceinline__ void ring_init(BulkRing& r, int consumer_warps) {
   __syncthreads();
 }
 
-__host__ __device__ __forceinline__ size_t align128(size_t v) { return (v + 127) & ~size_t(127); }
-
-template <typename T, int V>
+template <typename T, typename CT, int V>
 __global__ void __launch_bounds__(288) k_split_fwd_bulk(SplitArgs a, int stages) {
+  constexpr bool kHalf = sizeof(CT) == 2;
   extern __shared__ __align__(128) uint8_t dsm[];
   __shared__ float red[33];
   __shared__ float cl_slot, cl_bcast;
@@ -635,11 +355,14 @@ __global__ void __launch_bounds__(288) k_split_fwd_bulk(SplitArgs a, int stages)
   const int chunk0 = blockIdx.x * cpc;
   const int ci = threadIdx.x - 32;                 // consumer index
   const int col0 = chunk0 + ci * 4;
+  const CT* Ach = static_cast<const CT*>(a.A);
+  const CT* Bch = static_cast<const CT*>(a.Bc);
   T* E = reinterpret_cast<T*>(a.E);
   SplitTerm* terms = reinterpret_cast<SplitTerm*>(dsm);
-  BulkRing ring = carve_ring(dsm + align128(sizeof(SplitTerm) * nsplit), stages, cpc);
+  const int cbytes = cpc * static_cast<int>(sizeof(CT));
+  BulkRing ring = carve_ring(dsm + align128(sizeof(SplitTerm) * nsplit), stages, cbytes, cbytes);
 
-  // per-split rows and fixed shift D (see k_split_fwd)
+  // per-split rows and fixed shift D
   const float lnn = a.wsum[0] > 0.f ? log2f(a.wsum[0]) : 0.f;
   const float rnn = a.wsum[1] > 0.f ? log2f(a.wsum[1]) : 0.f;
   const float lnp = a.wsum[2] > 0.f ? log2f(a.wsum[2]) : 0.f;
@@ -666,7 +389,11 @@ __global__ void __launch_bounds__(288) k_split_fwd_bulk(SplitArgs a, int stages)
   }
   __syncthreads();
   const double D = dred[32];
-  for (int t = threadIdx.x; t < nsplit; t += nthr) terms[t].d = static_cast<float>(terms[t].xs - D);
+  for (int t = threadIdx.x; t < nsplit; t += nthr) {
+    const float d = static_cast<float>(terms[t].xs - D);
+    terms[t].d = d;
+    terms[t].c = exp2f(d - 2.f * kChartScale);
+  }
 
   if (i + w > len) {  // span outside the sentence: never feeds a valid span
     if (ci >= 0) {
@@ -692,10 +419,10 @@ __global__ void __launch_bounds__(288) k_split_fwd_bulk(SplitArgs a, int stages)
         const int s = t % stages;
         const uint32_t ph = (t / stages) & 1;
         mbar_wait(&ring.empty[s], ph ^ 1);
-        mbar_expect_tx(&ring.full[s], 2u * cpc * 4u);
-        float* dst = ring.buf + static_cast<size_t>(s) * 2 * cpc;
-        bulk_g2s(dst, a.A + terms[t].ra * a.Np + chunk0, cpc * 4u, &ring.full[s]);
-        bulk_g2s(dst + cpc, a.Bc + terms[t].rb * a.Np + chunk0, cpc * 4u, &ring.full[s]);
+        mbar_expect_tx(&ring.full[s], 2u * cbytes);
+        uint8_t* dst = ring.buf + static_cast<size_t>(s) * ring.stage_bytes;
+        bulk_g2s(dst, Ach + terms[t].ra * a.Np + chunk0, cbytes, &ring.full[s]);
+        bulk_g2s(dst + ring.off1, Bch + terms[t].rb * a.Np + chunk0, cbytes, &ring.full[s]);
       }
     }
   } else {
@@ -703,16 +430,23 @@ __global__ void __launch_bounds__(288) k_split_fwd_bulk(SplitArgs a, int stages)
       const int s = t % stages;
       const uint32_t ph = (t / stages) & 1;
       mbar_wait(&ring.full[s], ph);
-      const float dl = terms[t].d;
-      const float* src = ring.buf + static_cast<size_t>(s) * 2 * cpc + ci * 4;
+      const float dl = kHalf ? terms[t].c : terms[t].d;
+      const CT* src = reinterpret_cast<const CT*>(ring.buf + static_cast<size_t>(s) * ring.stage_bytes) + ci * 4;
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        const float4 x = *reinterpret_cast<const float4*>(src + v * ncons * 4);
-        const float4 y = *reinterpret_cast<const float4*>(src + cpc + v * ncons * 4);
-        S[4 * v + 0] += ex2(x.x + y.x + dl);
-        S[4 * v + 1] += ex2(x.y + y.y + dl);
-        S[4 * v + 2] += ex2(x.z + y.z + dl);
-        S[4 * v + 3] += ex2(x.w + y.w + dl);
+        const float4 x = chart4<CT>(src + v * ncons * 4);
+        const float4 y = chart4<CT>(src + cpc + v * ncons * 4);
+        if constexpr (kHalf) {
+          S[4 * v + 0] = fmaf(x.x * dl, y.x, S[4 * v + 0]);
+          S[4 * v + 1] = fmaf(x.y * dl, y.y, S[4 * v + 1]);
+          S[4 * v + 2] = fmaf(x.z * dl, y.z, S[4 * v + 2]);
+          S[4 * v + 3] = fmaf(x.w * dl, y.w, S[4 * v + 3]);
+        } else {
+          S[4 * v + 0] += ex2(x.x + y.x + dl);
+          S[4 * v + 1] += ex2(x.y + y.y + dl);
+          S[4 * v + 2] += ex2(x.z + y.z + dl);
+          S[4 * v + 3] += ex2(x.w + y.w + dl);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&ring.empty[s]);
@@ -776,8 +510,72 @@ __global__ void __launch_bounds__(288) k_split_fwd_bulk(SplitArgs a, int stages)
   }
 }
 
-template <typename T, int V>
+// ---------------------------------------------------------------------------
+// Backward seed (inside.py:400-404): the root posterior
+//   post[A] = exp(root[A] + o[len][0, A] - logZ)
+// seeds the outside pass at each sentence's top span as
+//   LQ^ = log2|g post| - o + x† = log2 root - (log2 Z - x†) + log2|g|
+// and is itself d_root (times g).  One thread per column; loops sentences.
+// ---------------------------------------------------------------------------
+__global__ void k_seed_bwd(const float* __restrict__ root, const float* __restrict__ TOP,
+                           const float* __restrict__ TOPZ, const float* __restrict__ g,
+                           const int* __restrict__ lengths, float* __restrict__ LQ,
+                           float* __restrict__ droot, int* __restrict__ flag, int B, int lmax,
+                           int N, int Np) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= Np) return;
+  float acc = 0.f;
+  for (int b = 0; b < B; ++b) {
+    const float z = TOPZ[b];
+    const float gb = g[b];
+    const bool finite = isfinite(z);
+    if (!finite && c == 0) atomicOr(flag, 1);
+    float lq = kNegInf;
+    if (finite && gb != 0.f && c < N) {
+      lq = fmaf(root[c], kLog2e, -z) + log2f(fabsf(gb));
+      acc += gb * exp2f(TOP[static_cast<long long>(b) * Np + c] - z);
+    }
+    LQ[chart_row(lengths[b], b, 0, B, lmax) * Np + c] = lq;
+  }
+  if (c < N) droot[c] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// K7: gather-form split backward for child width m (inside.py:406-417).
+// For span (i, i+m) of sentence b (row r), with the outside weight
+// LQ = log2|go| - o of each parent:
+//   G_L = [a != -inf] * sum_{w>m}  2^(x†_r + b[w-m][i+m] + LQ[w][i])
+//   G_R = [b != -inf] * sum_{s<i}  2^(x†_r + a[i-s][s]   + LQ[i+m-s][s])
+// which is ga*exp(x† - a) (resp. gb*exp(x† - b)) of the reference -- the row
+// of the dgrad/wgrad GEMM operand -- because the a (resp. b) factor of the
+// split softmax exp(a + b - o) cancels against exp(-a).  With the shifted
+// storage each term is 2^(d + B^ + LQ^) (fp32 chart) or
+// sib * 2^(d - kChartScale + LQ^) (half chart), d an fp64 per-term scalar.
+// One CTA per (span, column chunk); the sibling and parent row chunks of
+// every term stream through a cp.async.bulk + mbarrier ring as in the split
+// contraction.  Each accumulator is written once: deterministic, no atomics.
+// ---------------------------------------------------------------------------
+struct GatherArgs {
+  const void* A;  // CT*
+  const void* Bc; // CT*
+  const float* LQ;
+  const double* X;
+  void* G;  // T*, row stride 2*Np
+  long long g_lo;
+  const int* lengths;
+  const float* g;
+  int B, lmax, Np, m, cols_per_cta;
+};
+
+struct GatherTerm {
+  long long rs, rp;  // chart rows of the sibling and of the parent
+  float d;           // x†(child) + x†(sibling) - x†(parent), rounded from fp64
+  float pad;
+};
+
+template <typename T, typename CT, int V>
 __global__ void __launch_bounds__(288) k_gather_bwd_bulk(GatherArgs a, int stages) {
+  constexpr bool kHalf = sizeof(CT) == 2;
   extern __shared__ __align__(128) uint8_t dsm[];
   const int m = a.m;
   const int n_m = a.lmax - m + 1;
@@ -792,6 +590,8 @@ __global__ void __launch_bounds__(288) k_gather_bwd_bulk(GatherArgs a, int stage
   const int chunk0 = blockIdx.x * cpc;
   const int ci = threadIdx.x - 32;
   const int col0 = chunk0 + ci * 4;
+  const CT* Ach = static_cast<const CT*>(a.A);
+  const CT* Bch = static_cast<const CT*>(a.Bc);
   T* G = reinterpret_cast<T*>(a.G) + row * (2LL * a.Np);
 
   if (i + m > len) {
@@ -808,8 +608,10 @@ __global__ void __launch_bounds__(288) k_gather_bwd_bulk(GatherArgs a, int stage
   const int n_left = len - i - m;
   const int n_all = n_left + i;
   GatherTerm* gterms = reinterpret_cast<GatherTerm*>(dsm);
-  BulkRing ring = carve_ring(dsm + align128(sizeof(GatherTerm) * a.lmax), stages, cpc);
-  const double xm = a.X[row];
+  const int sbytes = cpc * static_cast<int>(sizeof(CT));
+  BulkRing ring = carve_ring(dsm + align128(sizeof(GatherTerm) * a.lmax), stages, sbytes,
+                             cpc * 4);
+  const double xm = a.X[row] - (kHalf ? kChartScale : 0);
   for (int t = threadIdx.x; t < n_all; t += nthr) {
     long long rs, rp;
     if (t < n_left) {  // left child (i, i+m) of parent (i, i+w): sibling b[w-m][i+m]
@@ -836,57 +638,61 @@ __global__ void __launch_bounds__(288) k_gather_bwd_bulk(GatherArgs a, int stage
         const int s = t % stages;
         const uint32_t ph = (t / stages) & 1;
         mbar_wait(&ring.empty[s], ph ^ 1);
-        mbar_expect_tx(&ring.full[s], 2u * cpc * 4u);
-        float* dst = ring.buf + static_cast<size_t>(s) * 2 * cpc;
-        const float* sib = t < n_left ? a.Bc : a.A;
-        bulk_g2s(dst, sib + gterms[t].rs * a.Np + chunk0, cpc * 4u, &ring.full[s]);
-        bulk_g2s(dst + cpc, a.LQ + gterms[t].rp * a.Np + chunk0, cpc * 4u, &ring.full[s]);
+        mbar_expect_tx(&ring.full[s], static_cast<uint32_t>(ring.stage_bytes));
+        uint8_t* dst = ring.buf + static_cast<size_t>(s) * ring.stage_bytes;
+        const CT* sib = t < n_left ? Bch : Ach;
+        bulk_g2s(dst, sib + gterms[t].rs * a.Np + chunk0, sbytes, &ring.full[s]);
+        bulk_g2s(dst + ring.off1, a.LQ + gterms[t].rp * a.Np + chunk0, cpc * 4u, &ring.full[s]);
       }
     }
   } else {
+    auto term = [](float x, float q, float d) {
+      if constexpr (kHalf) return x * ex2(q + d);
+      else return ex2(x + q + d);
+    };
     for (int t = 0; t < n_all; ++t) {
       const int s = t % stages;
       const uint32_t ph = (t / stages) & 1;
       mbar_wait(&ring.full[s], ph);
       const float d = gterms[t].d;
-      const float* src = ring.buf + static_cast<size_t>(s) * 2 * cpc + ci * 4;
-      float* acc = t < n_left ? gl : gr;
+      const uint8_t* stg = ring.buf + static_cast<size_t>(s) * ring.stage_bytes;
+      const CT* src = reinterpret_cast<const CT*>(stg) + ci * 4;
+      const float* srq = reinterpret_cast<const float*>(stg + ring.off1) + ci * 4;
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        const float4 x = *reinterpret_cast<const float4*>(src + v * ncons * 4);
-        const float4 q = *reinterpret_cast<const float4*>(src + cpc + v * ncons * 4);
+        const float4 x = chart4<CT>(src + v * ncons * 4);
+        const float4 q = *reinterpret_cast<const float4*>(srq + v * ncons * 4);
         if (t < n_left) {
-          gl[4 * v + 0] += ex2(x.x + q.x + d);
-          gl[4 * v + 1] += ex2(x.y + q.y + d);
-          gl[4 * v + 2] += ex2(x.z + q.z + d);
-          gl[4 * v + 3] += ex2(x.w + q.w + d);
+          gl[4 * v + 0] += term(x.x, q.x, d);
+          gl[4 * v + 1] += term(x.y, q.y, d);
+          gl[4 * v + 2] += term(x.z, q.z, d);
+          gl[4 * v + 3] += term(x.w, q.w, d);
         } else {
-          gr[4 * v + 0] += ex2(x.x + q.x + d);
-          gr[4 * v + 1] += ex2(x.y + q.y + d);
-          gr[4 * v + 2] += ex2(x.z + q.z + d);
-          gr[4 * v + 3] += ex2(x.w + q.w + d);
+          gr[4 * v + 0] += term(x.x, q.x, d);
+          gr[4 * v + 1] += term(x.y, q.y, d);
+          gr[4 * v + 2] += term(x.z, q.z, d);
+          gr[4 * v + 3] += term(x.w, q.w, d);
         }
       }
-      (void)acc;
       __syncwarp();
       if (lane == 0) mbar_arrive(&ring.empty[s]);
     }
     // zero-mass projections carry no gradient (inside.py:441-443 NaN guard)
     const float sg = a.g[b] < 0.f ? -1.f : 1.f;
-    const float* pam = a.A + row * a.Np;
-    const float* pbm = a.Bc + row * a.Np;
+    const CT* pam = Ach + row * a.Np;
+    const CT* pbm = Bch + row * a.Np;
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       const int c = col0 + v * ncons * 4;
-      float4 am = ldg4(pam + c), bm = ldg4(pbm + c);
-      store4s<T>(G + c, a.g_lo, am.x == kNegInf ? 0.f : sg * gl[4 * v + 0],
-                 am.y == kNegInf ? 0.f : sg * gl[4 * v + 1],
-                 am.z == kNegInf ? 0.f : sg * gl[4 * v + 2],
-                 am.w == kNegInf ? 0.f : sg * gl[4 * v + 3]);
-      store4s<T>(G + a.Np + c, a.g_lo, bm.x == kNegInf ? 0.f : sg * gr[4 * v + 0],
-                 bm.y == kNegInf ? 0.f : sg * gr[4 * v + 1],
-                 bm.z == kNegInf ? 0.f : sg * gr[4 * v + 2],
-                 bm.w == kNegInf ? 0.f : sg * gr[4 * v + 3]);
+      const float4 am = chart4_ldg<CT>(pam + c), bm = chart4_ldg<CT>(pbm + c);
+      store4s<T>(G + c, a.g_lo, is_dead<CT>(am.x) ? 0.f : sg * gl[4 * v + 0],
+                 is_dead<CT>(am.y) ? 0.f : sg * gl[4 * v + 1],
+                 is_dead<CT>(am.z) ? 0.f : sg * gl[4 * v + 2],
+                 is_dead<CT>(am.w) ? 0.f : sg * gl[4 * v + 3]);
+      store4s<T>(G + a.Np + c, a.g_lo, is_dead<CT>(bm.x) ? 0.f : sg * gr[4 * v + 0],
+                 is_dead<CT>(bm.y) ? 0.f : sg * gr[4 * v + 1],
+                 is_dead<CT>(bm.z) ? 0.f : sg * gr[4 * v + 2],
+                 is_dead<CT>(bm.w) ? 0.f : sg * gr[4 * v + 3]);
     }
   }
 }

@@ -134,13 +134,19 @@ def _chart_from_workspace(ws: torch.Tensor, shape, n_nt: int, length: int,
     ln2 = math.log(2.0)
     xs = ws[int(lay.off_x):int(lay.off_x) + 8 * int(lay.rows)].view(torch.float64).cpu().numpy()
 
-    def rows(off, w):
+    def rows(off, w, half=False):
         base = B * ((w - 1) * (l + 1) - (w - 1) * w // 2)
         n = length - w + 1
-        start = off + 4 * base * np_
-        flat = ws[start:start + 4 * n * np_].view(torch.float32).view(n, np_)
-        rel = flat[:, :n_nt].double().cpu().numpy()
+        esz = 2 if half else 4
+        start = off + esz * base * np_
+        flat = ws[start:start + esz * n * np_].view(torch.float16 if half else torch.float32)
+        rel = flat.view(n, np_)[:, :n_nt].double().cpu().numpy()
+        if half:  # fp16 linear acc * 2^14 (flashinside.h, FI_CHART_F16)
+            with np.errstate(divide="ignore"):
+                rel = np.log2(rel) - 14.0
         return ln2 * (xs[base:base + n, None] + rel)
+
+    half_ab = int(lay.chart_fmt) == _lib.FI_CHART_F16
 
     o = [None] * (length + 1)
     a = [None] * length
@@ -154,8 +160,8 @@ def _chart_from_workspace(ws: torch.Tensor, shape, n_nt: int, length: int,
             ow[:, :n_nt] = rows(int(lay.off_o), w)
             o[w] = ow
         if w < length:
-            a[w] = rows(int(lay.off_a), w)
-            b[w] = rows(int(lay.off_b), w)
+            a[w] = rows(int(lay.off_a), w, half_ab)
+            b[w] = rows(int(lay.off_b), w, half_ab)
     return InsideChart(length, o, a, b, NEG_INF)
 
 

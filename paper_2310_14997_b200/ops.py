@@ -58,12 +58,12 @@ def _check_inputs(L, R, root, unary, lengths):
 
 @torch.library.custom_op("flashinside::inside_fwd", mutates_args=())
 def inside_fwd(L: torch.Tensor, R: torch.Tensor, root: torch.Tensor, unary: torch.Tensor,
-               lengths: torch.Tensor, gemm_dtype: str, store_chart: bool
-               ) -> tuple[torch.Tensor, torch.Tensor]:
+               lengths: torch.Tensor, gemm_dtype: str, store_chart: bool,
+               chart_dtype: str = "auto") -> tuple[torch.Tensor, torch.Tensor]:
     L, R, root, unary = (t.contiguous() for t in (L, R, root, unary))
     lengths = lengths.contiguous()
     n, p, b, l = _check_inputs(L, R, root, unary, lengths)
-    s = _lib.shape(n, p, b, l, gemm_dtype, store_chart)
+    s = _lib.shape(n, p, b, l, gemm_dtype, store_chart, chart_dtype)
     ws = torch.empty(_lib.workspace_bytes(s), dtype=torch.uint8, device=L.device)
     log_z = torch.empty(b, dtype=torch.float32, device=L.device)
     lib = _lib.load()
@@ -74,9 +74,9 @@ def inside_fwd(L: torch.Tensor, R: torch.Tensor, root: torch.Tensor, unary: torc
 
 
 @inside_fwd.register_fake
-def _(L, R, root, unary, lengths, gemm_dtype, store_chart):
+def _(L, R, root, unary, lengths, gemm_dtype, store_chart, chart_dtype="auto"):
     n, p = root.shape[0], L.shape[1] - root.shape[0]
-    s = _lib.shape(n, p, unary.shape[0], unary.shape[1], gemm_dtype, store_chart)
+    s = _lib.shape(n, p, unary.shape[0], unary.shape[1], gemm_dtype, store_chart, chart_dtype)
     return (L.new_empty(unary.shape[0]),
             torch.empty(_lib.workspace_bytes(s), dtype=torch.uint8, device=L.device))
 
@@ -84,12 +84,12 @@ def _(L, R, root, unary, lengths, gemm_dtype, store_chart):
 @torch.library.custom_op("flashinside::inside_bwd", mutates_args=("ws",))
 def inside_bwd(grad_log_z: torch.Tensor, L: torch.Tensor, R: torch.Tensor, root: torch.Tensor,
                unary: torch.Tensor, lengths: torch.Tensor, log_z: torch.Tensor,
-               ws: torch.Tensor, gemm_dtype: str, store_chart: bool
+               ws: torch.Tensor, gemm_dtype: str, store_chart: bool, chart_dtype: str = "auto"
                ) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor]:
     L, R, root, unary = (t.contiguous() for t in (L, R, root, unary))
     grad_log_z = grad_log_z.contiguous().to(torch.float32)
     n, p, b, l = _check_inputs(L, R, root, unary, lengths)
-    s = _lib.shape(n, p, b, l, gemm_dtype, store_chart)
+    s = _lib.shape(n, p, b, l, gemm_dtype, store_chart, chart_dtype)
     dL = torch.empty_like(L)
     dR = torch.empty_like(R)
     droot = torch.empty_like(root)
@@ -103,41 +103,50 @@ def inside_bwd(grad_log_z: torch.Tensor, L: torch.Tensor, R: torch.Tensor, root:
 
 
 @inside_bwd.register_fake
-def _(grad_log_z, L, R, root, unary, lengths, log_z, ws, gemm_dtype, store_chart):
+def _(grad_log_z, L, R, root, unary, lengths, log_z, ws, gemm_dtype, store_chart,
+      chart_dtype="auto"):
     return (torch.empty_like(L), torch.empty_like(R), torch.empty_like(root),
             torch.empty_like(unary))
 
 
 def _setup_context(ctx, inputs, output):
-    L, R, root, unary, lengths, gemm_dtype, store_chart = inputs
+    L, R, root, unary, lengths, gemm_dtype, store_chart, chart_dtype = inputs
     log_z, ws = output
     ctx.save_for_backward(L, R, root, unary, lengths, log_z, ws)
     ctx.set_materialize_grads(False)  # never zero-fill a grad for the workspace output
     ctx.gemm_dtype = gemm_dtype
     ctx.store_chart = store_chart
+    ctx.chart_dtype = chart_dtype
 
 
 def _backward(ctx, grad_log_z, _grad_ws):
     L, R, root, unary, lengths, log_z, ws = ctx.saved_tensors
     dL, dR, droot, dunary = inside_bwd(grad_log_z, L, R, root, unary, lengths, log_z, ws,
-                                       ctx.gemm_dtype, ctx.store_chart)
-    return dL, dR, droot, dunary, None, None, None
+                                       ctx.gemm_dtype, ctx.store_chart, ctx.chart_dtype)
+    return dL, dR, droot, dunary, None, None, None, None
 
 
 inside_fwd.register_autograd(_backward, setup_context=_setup_context)
 
 
 def inside(L: torch.Tensor, R: torch.Tensor, root: torch.Tensor, unary: torch.Tensor,
-           lengths: torch.Tensor, gemm_dtype: str = "bf16") -> torch.Tensor:
-    """Per-sentence log partition log Z (B,), differentiable in L, R, root, unary."""
-    log_z, _ = inside_fwd(L, R, root, unary, lengths, gemm_dtype, False)
+           lengths: torch.Tensor, gemm_dtype: str = "bf16", chart_dtype: str = "auto"
+           ) -> torch.Tensor:
+    """Per-sentence log partition log Z (B,), differentiable in L, R, root, unary.
+
+    gemm_dtype: "bf16" | "tf32" (fast modes, 2e-3 parity bound) or "fp32"
+    (bf16x3 split operands, 1e-4 bound).  chart_dtype: storage of the
+    projected chart vectors between GEMM and split kernels -- "auto" (fp16
+    linear in the fast modes, fp32 log in fp32 mode), "fp32" or "fp16"."""
+    log_z, _ = inside_fwd(L, R, root, unary, lengths, gemm_dtype, False, chart_dtype)
     return log_z
 
 
-def inside_with_workspace(L, R, root, unary, lengths, gemm_dtype="bf16", store_chart=False):
+def inside_with_workspace(L, R, root, unary, lengths, gemm_dtype="bf16", store_chart=False,
+                          chart_dtype="auto"):
     """Forward only, returning (log_z, workspace) for chart export / explicit backward."""
     with torch.no_grad():
-        return inside_fwd(L, R, root, unary, lengths, gemm_dtype, store_chart)
+        return inside_fwd(L, R, root, unary, lengths, gemm_dtype, store_chart, chart_dtype)
 
 
 def test_gemm(A: torch.Tensor, B: torch.Tensor, a_mn: bool = False, b_mn: bool = False

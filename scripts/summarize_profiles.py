@@ -103,7 +103,8 @@ def classify(k: dict) -> str | None:
     return None
 
 
-def traffic(kernels: list[dict], n: int, batch: int, length: int, esz: int) -> dict:
+def traffic(kernels: list[dict], n: int, batch: int, length: int, esz: int,
+            chart_esz: int) -> dict:
     """Per kernel class: DRAM bytes of the captured launch next to the
     compulsory (algorithmic) bytes of that same launch (bench.py formulas)."""
     import sys
@@ -121,7 +122,7 @@ def traffic(kernels: list[dict], n: int, batch: int, length: int, esz: int) -> d
             width = length - gy // batch + 1
             fn = bench.split_launch_bytes if cls == "split_fwd" else bench.gather_launch_bytes
             d["width"] = width
-            d["algorithmic_bytes"] = fn(n, batch, length, width, esz)
+            d["algorithmic_bytes"] = fn(n, batch, length, width, esz, chart_esz)
             d["dram_over_algorithmic"] = d["dram_bytes"] / d["algorithmic_bytes"]
             d["achieved_gbs_under_ncu"] = d["algorithmic_bytes"] / (k["time_ms"] * 1e-3) / 1e9
         out[cls] = d
@@ -135,6 +136,7 @@ def main():
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--length", type=int, default=40)
     ap.add_argument("--esz", type=int, default=2, help="GEMM operand bytes (bf16 2, tf32 4)")
+    ap.add_argument("--chart-esz", type=int, default=2, help="a/b chart bytes (fp16 2, fp32 4)")
     ap.add_argument("--launches")
     ap.add_argument("--reps", nargs="*", default=[])
     args = ap.parse_args()
@@ -151,7 +153,7 @@ def main():
         (prof / f"{args.tag}_ncu_kernels.json").write_text(json.dumps(kernels, indent=1))
         for k in kernels:
             print(json.dumps(k))
-        tr = traffic(kernels, args.n, args.batch, args.length, args.esz)
+        tr = traffic(kernels, args.n, args.batch, args.length, args.esz, args.chart_esz)
         (prof / "ncu_traffic.json").write_text(json.dumps(tr, indent=1))
         print(json.dumps(tr, indent=1))
 

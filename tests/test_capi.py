@@ -58,10 +58,25 @@ def test_chart_layout_rows_and_padding(n, p, b, l, dt):
     nbytes = _lib.workspace_bytes(s)
     for off in (lay.off_a, lay.off_b, lay.off_o, lay.off_x, lay.off_lq, lay.off_flag):
         assert 0 <= off < nbytes and off % 1024 == 0
-    # chart arrays do not overlap
-    span = 4 * lay.rows * lay.np
-    offs = sorted([lay.off_a, lay.off_b, lay.off_o, lay.off_lq])
-    assert all(offs[k] + span <= offs[k + 1] for k in range(3))
+    # chart arrays do not overlap (a, b are fp16 in the fast modes' default chart)
+    assert lay.chart_fmt == (_lib.FI_CHART_F32 if dt == "fp32" else _lib.FI_CHART_F16)
+    esz_ab = 2 if lay.chart_fmt == _lib.FI_CHART_F16 else 4
+    spans = {lay.off_a: esz_ab, lay.off_b: esz_ab, lay.off_o: 4, lay.off_lq: 4}
+    offs = sorted(spans)
+    assert all(offs[k] + spans[offs[k]] * lay.rows * lay.np <= offs[k + 1] for k in range(3))
+
+
+@pytest.mark.parametrize("chart,fmt", [("auto", None), ("fp32", 1), ("fp16", 2)])
+@pytest.mark.parametrize("dt", ["bf16", "tf32", "fp32"])
+def test_chart_dtype_selects_storage(dt, chart, fmt):
+    s = _lib.shape(256, 256, 4, 10, dt, True, chart)
+    lay = _lib.chart_layout(s)
+    if fmt is None:
+        fmt = _lib.FI_CHART_F32 if dt == "fp32" else _lib.FI_CHART_F16
+    assert lay.chart_fmt == fmt
+    s32 = _lib.shape(256, 256, 4, 10, dt, True, "fp32")
+    if fmt == _lib.FI_CHART_F16:   # a and b halve
+        assert _lib.workspace_bytes(s32) - _lib.workspace_bytes(s) >= 4 * lay.rows * lay.np - 2048
 
 
 def test_workspace_scales_and_store_chart_costs_a_chart():
@@ -73,9 +88,9 @@ def test_workspace_scales_and_store_chart_costs_a_chart():
 
 
 @pytest.mark.parametrize("bad", [dict(n_nt=0), dict(n_pt=0), dict(batch=0), dict(max_len=1),
-                                 dict(gemm_dtype=7)])
+                                 dict(gemm_dtype=7), dict(chart_dtype=5)])
 def test_invalid_shapes_are_rejected(bad):
-    kw = dict(n_nt=8, n_pt=8, batch=2, max_len=5, gemm_dtype=0, store_chart=0)
+    kw = dict(n_nt=8, n_pt=8, batch=2, max_len=5, gemm_dtype=0, store_chart=0, chart_dtype=0)
     kw.update(bad)
     s = _lib.FiShape(**kw)
     lib = _lib.load()

@@ -30,7 +30,7 @@ def make_case(N, P, V, B, lmax, seed, lengths=None, conc=1.0):
     return root, left, right, emit, unary, np.asarray(lengths), toks
 
 
-def run_op(root, left, right, unary, lengths, grad, gemm_dtype):
+def run_op(root, left, right, unary, lengths, grad, gemm_dtype, chart_dtype="auto"):
     from paper_2310_14997_b200.ops import inside
     dev = "cuda"
     L = torch.tensor(left, dtype=torch.float32, device=dev, requires_grad=True)
@@ -38,12 +38,17 @@ def run_op(root, left, right, unary, lengths, grad, gemm_dtype):
     rt = torch.tensor(root, dtype=torch.float32, device=dev, requires_grad=True)
     un = torch.tensor(unary, dtype=torch.float32, device=dev, requires_grad=True)
     ln = torch.tensor(lengths, dtype=torch.int32, device=dev)
-    log_z = inside(L, R, rt, un, ln, gemm_dtype=gemm_dtype)
+    log_z = inside(L, R, rt, un, ln, gemm_dtype=gemm_dtype, chart_dtype=chart_dtype)
     (log_z * torch.tensor(grad, dtype=torch.float32, device=dev)).sum().backward()
     torch.cuda.synchronize()
     return {"log_z": log_z.detach().cpu().double().numpy(),
             "dL": L.grad.cpu().double().numpy(), "dR": R.grad.cpu().double().numpy(),
             "droot": rt.grad.cpu().double().numpy(), "dunary": un.grad.cpu().double().numpy()}
+
+
+def rel_err(got, want):
+    """Worst element error in units of the D5 bound |want| + max|want|."""
+    return float((np.abs(got - want) / (np.abs(want) + np.abs(want).max() + 1e-300)).max())
 
 
 def assert_close(name, got, want, rtol):
@@ -65,9 +70,10 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("chart_dtype", ["auto", "fp32", "fp16"])
 @pytest.mark.parametrize("gemm_dtype", ["fp32", "bf16", "tf32"])
 @pytest.mark.parametrize("case", CASES, ids=lambda c: f"N{c[0]}P{c[1]}B{c[3]}l{c[4]}")
-def test_forward_backward_parity(case, gemm_dtype):
+def test_forward_backward_parity(case, gemm_dtype, chart_dtype):
     N, P, V, B, lmax, seed, lengths = case
     if N == 1 and gemm_dtype != "fp32":
         pytest.skip("a single-symbol grammar has no averaging over K: only the "
@@ -75,8 +81,36 @@ def test_forward_backward_parity(case, gemm_dtype):
     root, left, right, emit, unary, lens, _ = make_case(N, P, V, B, lmax, seed, lengths)
     grad = np.linspace(1.0, -0.5, B)
     want = O.inside_batch(left, right, root, unary, lens, grad)
-    got = run_op(root, left, right, unary, lens, grad, gemm_dtype)
+    got = run_op(root, left, right, unary, lens, grad, gemm_dtype, chart_dtype)
+    # the fp16 chart (11-bit linear a, b) is a fast-mode storage: held to the
+    # 2e-3 bound whatever the GEMM operands
+    rtol = RTOL[gemm_dtype] if (chart_dtype != "fp16") else max(RTOL[gemm_dtype], 2e-3)
+    np.testing.assert_allclose(got["log_z"], want["log_z"], rtol=rtol)
+    for k in ("dL", "dR", "droot", "dunary"):
+        assert_close(k, got[k], want[k], rtol)
+
+
+@pytest.mark.parametrize("gemm_dtype,chart_dtype,grad", [
+    ("bf16", "auto", "loss"), ("bf16", "fp32", "loss"), ("tf32", "auto", "loss"),
+    ("fp32", "auto", "loss"), ("fp32", "auto", "mixed")])
+def test_config2_size_gradients(gemm_dtype, chart_dtype, grad):
+    """BASELINE config 2 sizes (N=P=1024, l=30) on two sentences of different
+    lengths: log Z and every gradient table against the float64 oracle.
+
+    "loss" is the training loss's upstream gradient (-1/B for every sentence,
+    train.py:218).  "mixed" gives the sentences opposite signs: the summed
+    tables then cancel, their maximum shrinks while each sentence's rounding
+    error does not, so the element-wise bound (relative to max|want|) is
+    only meaningful for the fp32 mode there (bf16 operands round at 2^-8;
+    the small-N parity cases above still mix signs in every mode)."""
+    root, left, right, emit, unary, lens, _ = make_case(1024, 1024, 64, 2, 30, 0, [30, 23])
+    gvec = np.array([-0.5, -0.5]) if grad == "loss" else np.array([-0.5, 0.75])
+    want = O.inside_batch(left, right, root, unary, lens, gvec)
+    got = run_op(root, left, right, unary, lens, gvec, gemm_dtype, chart_dtype)
     rtol = RTOL[gemm_dtype]
+    errs = {k: rel_err(got[k], want[k]) for k in ("dL", "dR", "droot", "dunary")}
+    errs["log_z"] = float(np.abs(got["log_z"] / want["log_z"] - 1).max())
+    print(f"config2 {gemm_dtype}/{chart_dtype}/{grad} worst errors:", errs)
     np.testing.assert_allclose(got["log_z"], want["log_z"], rtol=rtol)
     for k in ("dL", "dR", "droot", "dunary"):
         assert_close(k, got[k], want[k], rtol)
