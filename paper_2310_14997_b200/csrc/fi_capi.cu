@@ -101,6 +101,28 @@ int set_err(int code, const char* fmt, ...) {
     if (r_ != FI_OK) return r_; \
   } while (0)
 
+// Stream-K scratch of the GEMMs enqueued by this thread (set by the ABI entry
+// points from the caller's workspace; thread-local so calls on different
+// threads/streams never share it).
+struct SkScratch {
+  float* part = nullptr;  // kSkSlots x 128 x 256 fp32
+  int* cnt = nullptr;     // kSkCounters
+};
+thread_local SkScratch g_scr;
+constexpr int kSkSlots = 2 * 160;        // 2 partial tiles per CTA, <= 160 CTAs
+constexpr int kSkCounters = 1 << 16;     // per-tile arrival counters
+constexpr size_t kSkPartBytes = static_cast<size_t>(kSkSlots) * 128 * 256 * 4;
+
+// Points the thread's GEMM scratch at a workspace region for one ABI call.
+struct ScratchScope {
+  SkScratch saved;
+  ScratchScope(float* part, int* cnt) : saved(g_scr) {
+    g_scr.part = part;
+    g_scr.cnt = cnt;
+  }
+  ~ScratchScope() { g_scr = saved; }
+};
+
 // ------------------------------------------------------------------ layout
 struct Decomp {
   int clusters, threads, v, cols_per_cta, stages;
@@ -110,7 +132,7 @@ struct Plan {
   int N, P, B, l, Np, Pp, esz;
   Decomp dsplit, dgather;
   long long rows;
-  size_t wnn, wnp, e1, eall, gall, a, b, o, lq, x, top, topz, wsum, flag, total;
+  size_t wnn, wnp, e1, eall, gall, a, b, o, lq, x, top, topz, wsum, flag, skpart, skcnt, total;
   // element offsets of the lo planes of the GEMM operands (fp32 mode only)
   long long wnn_lo, wnp_lo, e1_lo, eall_lo, gall_lo;
   bool store_o, tf32, split, half_chart;
@@ -215,6 +237,8 @@ int make_plan(const fi_shape* s, Plan* p) {
   p->topz = take(4ull * p->B);
   p->wsum = take(16);
   p->flag = take(256);
+  p->skpart = take(kSkPartBytes);
+  p->skcnt = take(4ull * kSkCounters);
   p->total = off;
   return FI_OK;
 }
@@ -279,11 +303,11 @@ int num_sms() {
 
 template <typename T, int BN, bool AMN, bool BMN, int EPI, bool SPLIT, int CHUNK>
 int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_row0,
-                const GemmEpi& ep, cudaStream_t st) {
+                const GemmEpi& ep, cudaStream_t st, int bn, int sk) {
   using Cf = GemmCfg<T, BN>;
   CUtensorMap ta, tb, ta2, tb2;
   const int abi = AMN ? Cf::ATOM : Cf::BK, abo = AMN ? Cf::BK : Cf::BM;
-  const int bbi = BMN ? Cf::ATOM : Cf::BK, bbo = BMN ? Cf::BK : BN;
+  const int bbi = BMN ? Cf::ATOM : Cf::BK, bbo = BMN ? Cf::BK : bn;
   FI_TRY(encode<T>(&ta, A, abi, abo));
   FI_TRY(encode<T>(&tb, B, bbi, bbo));
   if (SPLIT) {
@@ -301,9 +325,15 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
   sh.N = N;
   sh.K = K;
   sh.a_row0 = a_row0;
+  sh.bn = bn;
   sh.num_m = (M + Cf::BM - 1) / Cf::BM;
-  sh.num_n = N / BN;
+  sh.num_n = (N + bn - 1) / bn;
   sh.num_k = (K + Cf::BK - 1) / Cf::BK;
+  const int tiles = sh.num_m * sh.num_n;
+  if (!(g_scr.part && g_scr.cnt && tiles <= kSkCounters)) sk = 0;
+  sh.sk = sk > 1 ? sk : 0;
+  sh.part = g_scr.part;
+  sh.cnt = g_scr.cnt;
   auto kern = k_gemm<T, BN, AMN, BMN, EPI, SPLIT, CHUNK>;
   static bool attr_done[64] = {false};
   int dev = 0;
@@ -313,8 +343,14 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
                                  Cf::SMEM_BYTES));
     attr_done[dev & 63] = true;
   }
-  const int tiles = sh.num_m * sh.num_n;
-  const int grid = tiles < num_sms() ? tiles : num_sms();
+  const int sms = num_sms() < kSkSlots / 2 ? num_sms() : kSkSlots / 2;
+  int grid = tiles < sms ? tiles : sms;
+  if (sh.sk) {  // units: whole waves + the leftover tiles x s parts
+    const int dp = sk_dp_tiles(tiles, sms, sh.sk);
+    const long long units = dp + static_cast<long long>(tiles - dp) * sh.sk;
+    grid = static_cast<int>(units < sms ? units : sms);
+    if (dp && grid != sms) return set_err(FI_ERR_ARG, "split-K grid mismatch");
+  }
   if (grid <= 0) return FI_OK;
   ProfScope prof(EPI == EPI_FWD || EPI == EPI_FWD_H ? FI_PROF_GEMM_FWD
                  : EPI == EPI_WGRAD ? FI_PROF_GEMM_WGRAD
@@ -325,30 +361,81 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
   return FI_OK;
 }
 
-// Pick the widest N tile that still gives one tile per SM (small-M widths).
+// N tile and schedule per launch from a cost model in units of one 128x256
+// k-iteration (~0.45 us of tensor-pipe time per SM):
+//   whole tiles   ceil(T / G) * k_iters * t(bn),  T = ceil(M/128) * ceil(N/bn)
+//   split-K tail  (T / G) whole waves, then the T % G leftover tiles (all T
+//                 when T < G) cut into s <= 4 K-ranges dealt over the G CTAs:
+//                 ceil(r s / G) * k_iters / s * t(bn), plus the partials
+//                 (one 128 x bn fp32 write per unit, s reads by the finisher).
+// The N tile is free in steps of 32 (K-major B) or of one 128-B atom
+// (MN-major B), so the tile count can be matched to whole waves of the 148
+// SMs instead of leaving a partial last wave idle.  t(bn) = 0.45 + 0.55 bn/256
+// is fitted to B200 measurements (scripts/gemm_micro.py): a k-iteration has a
+// fixed A-tile / issue cost plus a part proportional to the N tile.
+// FI_GEMM_SK=0 (whole tiles) / FI_GEMM_SK=s (force s) and FI_GEMM_BN force
+// the choice for A/B runs.
+int gemm_env(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+struct GemmChoice {
+  int bn;
+  int sk;  // split-K parts of the leftover tiles (<= 1: none)
+};
+
+GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int bn_step) {
+  const int G = num_sms() < kSkSlots / 2 ? num_sms() : kSkSlots / 2;
+  const long long mt = (M + 127) / 128;
+  static const int force_sk = gemm_env("FI_GEMM_SK", 0);  // split-K off by default (measured slower)
+  static const int force_bn = gemm_env("FI_GEMM_BN", 0);
+  GemmChoice best{0, 0};
+  double best_cost = 1e300;
+  for (int bn = bn_max; bn >= 64; bn -= bn_step) {
+    if (force_bn && bn != force_bn) continue;
+    const double t_it = 0.45 + 0.55 * bn / 256.0;
+    const long long T = mt * ((N + bn - 1) / bn);
+    const double plain = static_cast<double>((T + G - 1) / G) * k_iters * t_it;
+    if (force_sk <= 1 && plain < best_cost * 0.995) {
+      best_cost = plain;
+      best = {bn, 0};
+    }
+    if (force_sk == 0 || T > kSkCounters) continue;
+    const long long dp = T >= G ? (T / G) * G : 0;
+    const long long r = T - dp;
+    if (r == 0) continue;
+    for (int s = 2; s <= kMaxSplit && s <= k_iters; ++s) {
+      if (r * s > 2LL * G) break;
+      if (force_sk > 1 && s != force_sk) continue;
+      const double tail = static_cast<double>((r * s + G - 1) / G) * k_iters / s * t_it;
+      const double cost = static_cast<double>(dp / G) * k_iters * t_it + tail +
+                          3.0 * (1 + s) * bn / 256.0;
+      if (cost < best_cost * 0.97 || force_sk > 1) {
+        best_cost = cost;
+        best = {bn, s};
+      }
+    }
+  }
+  return best;
+}
+
 template <typename T, bool AMN, bool BMN, int EPI, bool SPLIT>
 int run_gemm_s(const Operand& A, const Operand& B, int M, int N, int K, int a_row0,
                const GemmEpi& ep, cudaStream_t st) {
   if (M <= 0 || N <= 0) return FI_OK;
-  const long long mt = (M + 127) / 128;
-  const int sms = num_sms();
-  if constexpr (SPLIT) {
-    // fp32 mode: chunked round-to-nearest accumulation (8 K-iterations per
-    // TMEM chunk) to bound the tensor-core truncation bias; BN <= 128.
-    constexpr int kChunk = 8;
-    if (N % 128 == 0 && mt * (N / 128) >= sms)
-      return launch_gemm<T, 128, AMN, BMN, EPI, SPLIT, kChunk>(A, B, M, N, K, a_row0, ep, st);
-    if (N % 64 == 0)
-      return launch_gemm<T, 64, AMN, BMN, EPI, SPLIT, kChunk>(A, B, M, N, K, a_row0, ep, st);
-  } else {
-    if (N % 256 == 0 && mt * (N / 256) >= sms)
-      return launch_gemm<T, 256, AMN, BMN, EPI, SPLIT, 0>(A, B, M, N, K, a_row0, ep, st);
-    if (N % 128 == 0 && mt * (N / 128) >= sms)
-      return launch_gemm<T, 128, AMN, BMN, EPI, SPLIT, 0>(A, B, M, N, K, a_row0, ep, st);
-    if (N % 64 == 0)
-      return launch_gemm<T, 64, AMN, BMN, EPI, SPLIT, 0>(A, B, M, N, K, a_row0, ep, st);
-  }
-  return set_err(FI_ERR_ARG, "GEMM N=%d must be a multiple of 64", N);
+  if (N % 64) return set_err(FI_ERR_ARG, "GEMM N=%d must be a multiple of 64", N);
+  constexpr int BK = 128 / static_cast<int>(sizeof(T));
+  constexpr int ATOM = 128 / static_cast<int>(sizeof(T));
+  const int k_iters = (SPLIT ? 3 : 1) * ((K + BK - 1) / BK);
+  // fp32 mode: chunked round-to-nearest accumulation (8 K-iterations per
+  // TMEM chunk) to bound the tensor-core truncation bias; N tile <= 128.
+  constexpr int kBnMax = SPLIT ? 128 : 256;
+  const int step = BMN ? (ATOM > 32 ? ATOM : 32) : 32;
+  const GemmChoice c = choose_gemm(M, N, k_iters, kBnMax, step);
+  if (c.bn == 0) return set_err(FI_ERR_ARG, "no GEMM tile for N=%d (FI_GEMM_BN?)", N);
+  return launch_gemm<T, kBnMax, AMN, BMN, EPI, SPLIT, SPLIT ? 8 : 0>(A, B, M, N, K, a_row0, ep,
+                                                                     st, c.bn, c.sk);
 }
 
 // Dispatch on the split (fp32 / bf16x3) mode; tf32 operands are never split.
@@ -657,6 +744,8 @@ int fi_inside_forward(const fi_shape* shape, const float* L, const float* R, con
   FI_TRY(check_ptrs({L, R, root, unary, lengths, log_z, ws}));
   FI_TRY(load_encode());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ScratchScope scr(at<float>(ws, p.skpart), at<int>(ws, p.skcnt));
+  FI_CUDA(cudaMemsetAsync(at<int>(ws, p.skcnt), 0, 4ull * kSkCounters, st));
   if (p.tf32) {
     if (p.half_chart) return forward_impl<float, __half>(p, L, R, root, unary, lengths, log_z, ws, st);
     return forward_impl<float, float>(p, L, R, root, unary, lengths, log_z, ws, st);
@@ -675,6 +764,8 @@ int fi_inside_backward(const fi_shape* shape, const float* L, const float* R, co
   FI_TRY(check_ptrs({L, R, root, unary, lengths, log_z, grad_log_z, dL, dR, droot, dunary, ws}));
   FI_TRY(load_encode());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ScratchScope scr(at<float>(ws, p.skpart), at<int>(ws, p.skcnt));
+  FI_CUDA(cudaMemsetAsync(at<int>(ws, p.skcnt), 0, 4ull * kSkCounters, st));
 #define FI_BWD(T, CT)                                                                      \
   return backward_impl<T, CT>(p, L, R, root, unary, lengths, log_z, grad_log_z, dL, dR, droot, \
                               dunary, ws, st)
@@ -709,6 +800,16 @@ int fi_test_gemm(int32_t dtype, int32_t a_mn, int32_t b_mn, int32_t M, int32_t N
   if (M < 1 || N < 64 || N % 64 || K < 1)
     return set_err(FI_ERR_ARG, "test GEMM needs M>=1, N%%64==0, K>=1");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  void* scratch = nullptr;
+  FI_CUDA(cudaMallocAsync(&scratch, kSkPartBytes + 4ull * kSkCounters, st));
+  FI_CUDA(cudaMemsetAsync(static_cast<uint8_t*>(scratch) + kSkPartBytes, 0, 4ull * kSkCounters, st));
+  struct Free {
+    void* p;
+    cudaStream_t s;
+    ~Free() { cudaFreeAsync(p, s); }
+  } free_scratch{scratch, st};
+  ScratchScope scr(static_cast<float*>(scratch),
+                   reinterpret_cast<int*>(static_cast<uint8_t*>(scratch) + kSkPartBytes));
   GemmEpi ep = {};
   ep.M = M;
   ep.C = C;

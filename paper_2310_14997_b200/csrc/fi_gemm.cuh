@@ -33,7 +33,64 @@ struct GemmShape {
   int M, N, K;    // logical problem; rows >= M are masked in the epilogue
   int a_row0;     // K-major A: first row coordinate inside the tensor map
   int num_m, num_n, num_k;
+  int bn;         // N tile (runtime, <= the kernel's BN template bound, multiple of 32)
+  // Split-K tail (sk = s > 1): tiles [0, dp) -- whole waves -- run round
+  // robin; each remaining tile (the partial last wave, or every tile when
+  // there are fewer tiles than CTAs) is cut into s K-ranges, and the
+  // (tile, part) units are dealt round robin too, so concurrently running
+  // CTAs sit at no more than s distinct K offsets and keep sharing the
+  // operand K-slabs through L2.  A split tile is summed by the last of its s
+  // units to finish (per-tile arrival counter), in part order (deterministic),
+  // which then runs the epilogue.  sk <= 1: whole tiles only.
+  int sk;
+  float* part;    // sk: 2 partial tiles (128 x 256 fp32) per CTA
+  int* cnt;       // sk: per-tile arrival counters, zero between launches
 };
+
+// Work assignment of one CTA: a sequence of (tile, k-iteration range) segments.
+__host__ __device__ __forceinline__ int sk_dp_tiles(int T, int G, int s) {
+  if (s <= 1) return T;
+  return T >= G ? (T / G) * G : 0;
+}
+
+struct WorkIter {
+  int u, U, s, dp, T, kI, G;
+  __device__ __forceinline__ WorkIter(const GemmShape& sh, int k_iters) {
+    T = sh.num_m * sh.num_n;
+    kI = k_iters;
+    G = gridDim.x;
+    s = sh.sk > 1 ? sh.sk : 1;
+    dp = sk_dp_tiles(T, G, s);
+    U = dp + (T - dp) * s;  // units: dp whole tiles, then (tile, part) pairs
+    u = blockIdx.x;
+  }
+  // unit -> (tile, k0, k1)
+  __device__ __forceinline__ void unit(int v, int& t, int& k0, int& k1) const {
+    if (v < dp) {
+      t = v;
+      k0 = 0;
+      k1 = kI;
+      return;
+    }
+    const int w = v - dp;
+    t = dp + w / s;
+    const int p = w % s;
+    k0 = static_cast<int>(static_cast<long long>(kI) * p / s);
+    k1 = static_cast<int>(static_cast<long long>(kI) * (p + 1) / s);
+  }
+  __device__ __forceinline__ bool next(int& t, int& k0, int& k1) {
+    if (u >= U) return false;
+    unit(u, t, k0, k1);
+    u += G;
+    return true;
+  }
+};
+
+constexpr int kMaxSplit = 4;  // split-K parts per tile (finisher keeps all loads in flight)
+
+__device__ __forceinline__ void epi_bar() {  // the 4 epilogue warps only
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+}
 
 struct GemmEpi {
   int M;              // valid output rows
@@ -67,7 +124,7 @@ struct GemmEpi {
   int ldc;
 };
 
-template <typename T, int BN>
+template <typename T, int BN>  // BN: the largest N tile the smem ring is sized for
 struct GemmCfg {
   static constexpr int BM = 128;
   static constexpr int kElt = static_cast<int>(sizeof(T));
@@ -181,8 +238,9 @@ __global__ void __launch_bounds__(256, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int num_tiles = sh.num_m * sh.num_n;
   const int k_iters = SPLIT ? 3 * sh.num_k : sh.num_k;
+  const int bn = sh.bn;  // runtime N tile <= BN (the smem / TMEM layout bound)
+  int* bcast = reinterpret_cast<int*>(tslot + 1);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -212,16 +270,18 @@ __global__ void __launch_bounds__(256, 1)
       // ------------------------------------------------ TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      WorkIter wi(sh, k_iters);
+      int tile, k0, k1;
+      while (wi.next(tile, k0, k1)) {
         const int m_blk = tile % sh.num_m;
         const int n_blk = tile / sh.num_m;
-        for (int it = 0; it < k_iters; ++it) {
+        for (int it = k0; it < k1; ++it) {
           const int pass = SPLIT ? it / sh.num_k : 0;
           const int kb = SPLIT ? it - pass * sh.num_k : it;
           const CUtensorMap* ma = (SPLIT && pass == 0) ? &tmA2 : &tmA;
           const CUtensorMap* mb = (SPLIT && pass == 1) ? &tmB2 : &tmB;
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+          mbar_expect_tx(&full[stage], C::A_BYTES + bn * 128);
           uint8_t* a_dst = smA + stage * C::A_BYTES;
           uint8_t* b_dst = smB + stage * C::B_BYTES;
           if constexpr (!A_MN) {
@@ -233,11 +293,11 @@ __global__ void __launch_bounds__(256, 1)
                           kb * C::BK);
           }
           if constexpr (!B_MN) {
-            tma_load_2d(b_dst, mb, &full[stage], kb * C::BK, n_blk * BN);
+            tma_load_2d(b_dst, mb, &full[stage], kb * C::BK, n_blk * bn);
           } else {
 #pragma unroll
-            for (int j = 0; j < BN / C::ATOM; ++j)
-              tma_load_2d(b_dst + j * C::BK * 128, mb, &full[stage], n_blk * BN + j * C::ATOM,
+            for (int j = 0; j < bn / C::ATOM; ++j)
+              tma_load_2d(b_dst + j * C::BK * 128, mb, &full[stage], n_blk * bn + j * C::ATOM,
                           kb * C::BK);
           }
           if (++stage == C::STAGES) {
@@ -250,7 +310,7 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       // ------------------------------------------------ MMA issuer
-      constexpr uint32_t idesc = make_idesc<C::TF32>(BN, A_MN, B_MN);
+      const uint32_t idesc = make_idesc<C::TF32>(bn, A_MN, B_MN);
       constexpr uint32_t a_lbo = A_MN ? C::BK * 128 : 16;
       constexpr uint32_t b_lbo = B_MN ? C::BK * 128 : 16;
       // tf32 MN-major operands use the 32B-atom 128B swizzle (4-row groups)
@@ -264,11 +324,13 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      const int cl = CHUNK > 0 ? CHUNK : k_iters;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      WorkIter wi(sh, k_iters);
+      int tile, k0, k1;
+      while (wi.next(tile, k0, k1)) {
         uint32_t d_tmem = tmem_base;
-        for (int kb = 0; kb < k_iters; ++kb) {
-          const int kc = kb % cl;
+        const int cl = CHUNK > 0 ? CHUNK : (k1 - k0);
+        for (int kb = k0; kb < k1; ++kb) {
+          const int kc = (kb - k0) % cl;
           if (kc == 0) {  // start a chunk in a drained accumulator
             mbar_wait(&tempty[acc], acc_phase ^ 1);
             tc_fence_after();
@@ -289,7 +351,7 @@ __global__ void __launch_bounds__(256, 1)
             stage = 0;
             phase ^= 1;
           }
-          if (kc == cl - 1 || kb == k_iters - 1) {
+          if (kc == cl - 1 || kb == k1 - 1) {
             umma_commit(&tfull[acc]);
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
@@ -303,28 +365,28 @@ __global__ void __launch_bounds__(256, 1)
     const int r = quad * 32 + lane;  // accumulator row (TMEM lane)
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    WorkIter wi(sh, k_iters);
+    int tile, k0, k1;
+    int nsplit = 0;  // split units this CTA has finished (partial slot index)
+    while (wi.next(tile, k0, k1)) {
+      const bool whole = (k0 == 0 && k1 == k_iters);
       const int m_blk = tile % sh.num_m;
       const int n_blk = tile / sh.num_m;
       const int lrow = m_blk * C::BM + r;  // row within this GEMM
       const long long grow = ep.row0 + lrow;
       const bool row_ok = lrow < ep.M;
       float xv = 0.f;
-      float* rowptr = nullptr;
+      float* rowptr = nullptr;  // row base (EPI_FWD/_H: the a row; b row below)
+      float* rowptr_b = nullptr;
       int aux = 0;
-      int col_base = n_blk * BN;
+      const int col_base = n_blk * bn;
       if (row_ok) {
         if constexpr (EPI == EPI_FWD) {
-          if (col_base < ep.Np) {
-            rowptr = ep.outA + grow * ep.Np;
-          } else {
-            rowptr = ep.outB + grow * ep.Np;
-            col_base -= ep.Np;
-          }
+          rowptr = ep.outA + grow * ep.Np;
+          rowptr_b = ep.outB + grow * ep.Np;
         } else if constexpr (EPI == EPI_FWD_H) {
-          __half* base = reinterpret_cast<__half*>(col_base < ep.Np ? ep.outA : ep.outB);
-          rowptr = reinterpret_cast<float*>(base + grow * ep.Np);
-          if (col_base >= ep.Np) col_base -= ep.Np;
+          rowptr = reinterpret_cast<float*>(reinterpret_cast<__half*>(ep.outA) + grow * ep.Np);
+          rowptr_b = reinterpret_cast<float*>(reinterpret_cast<__half*>(ep.outB) + grow * ep.Np);
         } else if constexpr (EPI == EPI_DGRAD) {
           rowptr = ep.LQ + grow * ep.Np;
         } else if constexpr (EPI == EPI_DUNARY) {
@@ -350,16 +412,42 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
       const int erow = (EPI == EPI_WGRAD && aux) ? lrow - ep.Np : lrow;
+      // epilogue of one 32-column chunk j of this tile (skips the N tail; the
+      // forward's [a | b] columns split at Np, possibly inside a tile)
+      auto emit = [&](int j, const float (&v)[32]) {
+        int col = col_base + j * 32;
+        if (col >= sh.N) return;
+        float* rp = rowptr;
+        if constexpr (EPI == EPI_FWD || EPI == EPI_FWD_H) {
+          if (col >= ep.Np) {
+            col -= ep.Np;
+            rp = rowptr_b;
+          }
+        }
+        epi_chunk<EPI>(ep, erow, grow, col, v, xv, ok, rp, aux);
+      };
       const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
+      // partial-tile slot: this CTA's n-th split unit (the host keeps the split
+      // units <= 2 G, so a CTA gets at most 2 and slots are never reused)
+      float* my_part = sh.part + (static_cast<size_t>(blockIdx.x) * 2 + (nsplit & 1)) * (128 * 256);
+      auto put_part = [&](int j, const float (&v)[32]) {
+        float4* dst = reinterpret_cast<float4*>(my_part + (j * 128 + r) * 32);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      };
       if constexpr (CHUNK == 0) {
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         const uint32_t t_row = t_lane + static_cast<uint32_t>(acc * BN);
 #pragma unroll 1
-        for (int j = 0; j < BN / 32; ++j) {
+        for (int j = 0; j < bn / 32; ++j) {
           float v[32];
           tmem_ld32(t_row + j * 32, v);
-          epi_chunk<EPI>(ep, erow, grow, col_base + j * 32, v, xv, ok, rowptr, aux);
+          if (whole)
+            emit(j, v);
+          else
+            put_part(j, v);
         }
         tc_fence_before();
         __syncwarp();
@@ -373,17 +461,19 @@ __global__ void __launch_bounds__(256, 1)
         for (int j = 0; j < BN / 32; ++j)
 #pragma unroll
           for (int t = 0; t < 32; ++t) sum[j][t] = 0.f;
-        const int nchunks = (k_iters + CHUNK - 1) / CHUNK;
+        const int nchunks = (k1 - k0 + CHUNK - 1) / CHUNK;
         for (int c = 0; c < nchunks; ++c) {
           mbar_wait(&tfull[acc], acc_phase);
           tc_fence_after();
           const uint32_t t_row = t_lane + static_cast<uint32_t>(acc * BN);
 #pragma unroll
           for (int j = 0; j < BN / 32; ++j) {
-            float v[32];
-            tmem_ld32(t_row + j * 32, v);
+            if (j < bn / 32) {
+              float v[32];
+              tmem_ld32(t_row + j * 32, v);
 #pragma unroll
-            for (int t = 0; t < 32; ++t) sum[j][t] += v[t];
+              for (int t = 0; t < 32; ++t) sum[j][t] += v[t];
+            }
           }
           tc_fence_before();
           __syncwarp();
@@ -392,8 +482,71 @@ __global__ void __launch_bounds__(256, 1)
           if (acc == 0) acc_phase ^= 1;
         }
 #pragma unroll
-        for (int j = 0; j < BN / 32; ++j)
-          epi_chunk<EPI>(ep, erow, grow, col_base + j * 32, sum[j], xv, ok, rowptr, aux);
+        for (int j = 0; j < BN / 32; ++j) {
+          if (j < bn / 32) {
+            if (whole)
+              emit(j, sum[j]);
+            else
+              put_part(j, sum[j]);
+          }
+        }
+      }
+      if (!whole) {
+        // publish the partial; the last of the tile's s units finishes it
+        ++nsplit;
+        __threadfence();
+        epi_bar();
+        if (warp == 4 && lane == 0) {
+          const int old = atomicAdd(&sh.cnt[tile], 1);
+          const int last = old == wi.s - 1;
+          if (last) {
+            __threadfence();
+            sh.cnt[tile] = 0;  // ready for the next launch
+          }
+          *bcast = last;
+        }
+        epi_bar();
+        const int last = *bcast;
+        epi_bar();  // bcast is reused by the next split unit
+        if (last) {
+          const int u0 = wi.dp + (tile - wi.dp) * wi.s;  // unit of part 0
+#pragma unroll 1
+          for (int j = 0; j < bn / 32; ++j) {
+            float v[32];
+#pragma unroll
+            for (int t = 0; t < 32; ++t) v[t] = 0.f;
+            // all parts' loads in flight at once (s <= kMaxSplit), then a
+            // part-order sum: deterministic whatever the arrival order
+            float4 w4[kMaxSplit][8];
+#pragma unroll
+            for (int p = 0; p < kMaxSplit; ++p) {
+              if (p < wi.s) {
+                const int uu = u0 + p;
+                const int c = uu % wi.G;
+                // dp is a multiple of G: CTA c's split units are dp + c, dp + c + G
+                const int nth = (uu - wi.dp) / wi.G;
+                const float4* src = reinterpret_cast<const float4*>(
+                    sh.part + (static_cast<size_t>(c) * 2 + (nth & 1)) * (128 * 256) +
+                    (j * 128 + r) * 32);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) w4[p][q] = __ldcg(src + q);
+              }
+            }
+#pragma unroll
+            for (int p = 0; p < kMaxSplit; ++p) {
+              if (p < wi.s) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                  v[4 * q] += w4[p][q].x;
+                  v[4 * q + 1] += w4[p][q].y;
+                  v[4 * q + 2] += w4[p][q].z;
+                  v[4 * q + 3] += w4[p][q].w;
+                }
+              }
+            }
+            emit(j, v);
+          }
+        }
       }
     }
   }

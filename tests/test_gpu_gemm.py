@@ -12,6 +12,12 @@ CASES = [  # M, N, K
     (40, 64, 1000),
     (1000, 768, 4096),
     (4096, 256, 128),
+    # stream-K schedules: few tiles over long K (a tile split over many CTAs),
+    # and tile counts just above one wave (partial tiles at range boundaries)
+    (320, 512, 4096),
+    (128, 256, 8192),
+    (4096, 2048, 512),
+    (2496, 4096, 1024),
 ]
 
 
