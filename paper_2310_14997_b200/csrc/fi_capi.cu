@@ -101,28 +101,6 @@ int set_err(int code, const char* fmt, ...) {
     if (r_ != FI_OK) return r_; \
   } while (0)
 
-// Stream-K scratch of the GEMMs enqueued by this thread (set by the ABI entry
-// points from the caller's workspace; thread-local so calls on different
-// threads/streams never share it).
-struct SkScratch {
-  float* part = nullptr;  // kSkSlots x 128 x 256 fp32
-  int* cnt = nullptr;     // kSkCounters
-};
-thread_local SkScratch g_scr;
-constexpr int kSkSlots = 2 * 160;        // 2 partial tiles per CTA, <= 160 CTAs
-constexpr int kSkCounters = 1 << 16;     // per-tile arrival counters
-constexpr size_t kSkPartBytes = static_cast<size_t>(kSkSlots) * 128 * 256 * 4;
-
-// Points the thread's GEMM scratch at a workspace region for one ABI call.
-struct ScratchScope {
-  SkScratch saved;
-  ScratchScope(float* part, int* cnt) : saved(g_scr) {
-    g_scr.part = part;
-    g_scr.cnt = cnt;
-  }
-  ~ScratchScope() { g_scr = saved; }
-};
-
 // ------------------------------------------------------------------ layout
 struct Decomp {
   int clusters, threads, v, cols_per_cta, stages;
@@ -132,7 +110,7 @@ struct Plan {
   int N, P, B, l, Np, Pp, esz;
   Decomp dsplit, dgather;
   long long rows;
-  size_t wnn, wnp, e1, eall, gall, a, b, o, lq, x, top, topz, wsum, flag, skpart, skcnt, total;
+  size_t wnn, wnp, e1, eall, gall, a, b, o, lq, x, top, topz, wsum, flag, total;
   // element offsets of the lo planes of the GEMM operands (fp32 mode only)
   long long wnn_lo, wnp_lo, e1_lo, eall_lo, gall_lo;
   bool store_o, tf32, split, half_chart;
@@ -237,8 +215,6 @@ int make_plan(const fi_shape* s, Plan* p) {
   p->topz = take(4ull * p->B);
   p->wsum = take(16);
   p->flag = take(256);
-  p->skpart = take(kSkPartBytes);
-  p->skcnt = take(4ull * kSkCounters);
   p->total = off;
   return FI_OK;
 }
@@ -301,13 +277,34 @@ int num_sms() {
   return cached[dev] > 0 ? cached[dev] : 148;
 }
 
-template <typename T, int BN, bool AMN, bool BMN, int EPI, bool SPLIT, int CHUNK>
+template <typename K, typename... Args>
+int launch_cluster(K kern, int cluster, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                   Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  FI_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+  ++g_launches;
+  return FI_OK;
+}
+
+template <typename T, int BN, bool AMN, bool BMN, int EPI, bool SPLIT, int CHUNK, bool PAIR>
 int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_row0,
-                const GemmEpi& ep, cudaStream_t st, int bn, int sk) {
+                const GemmEpi& ep, cudaStream_t st, int bn) {
   using Cf = GemmCfg<T, BN>;
+  constexpr int NCTA = PAIR ? 2 : 1;
   CUtensorMap ta, tb, ta2, tb2;
   const int abi = AMN ? Cf::ATOM : Cf::BK, abo = AMN ? Cf::BK : Cf::BM;
-  const int bbi = BMN ? Cf::ATOM : Cf::BK, bbo = BMN ? Cf::BK : bn;
+  const int bbi = BMN ? Cf::ATOM : Cf::BK, bbo = BMN ? Cf::BK : bn / NCTA;
   FI_TRY(encode<T>(&ta, A, abi, abo));
   FI_TRY(encode<T>(&tb, B, bbi, bbo));
   if (SPLIT) {
@@ -326,15 +323,11 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
   sh.K = K;
   sh.a_row0 = a_row0;
   sh.bn = bn;
-  sh.num_m = (M + Cf::BM - 1) / Cf::BM;
+  sh.num_m = (M + Cf::BM * NCTA - 1) / (Cf::BM * NCTA);
   sh.num_n = (N + bn - 1) / bn;
   sh.num_k = (K + Cf::BK - 1) / Cf::BK;
   const int tiles = sh.num_m * sh.num_n;
-  if (!(g_scr.part && g_scr.cnt && tiles <= kSkCounters)) sk = 0;
-  sh.sk = sk > 1 ? sk : 0;
-  sh.part = g_scr.part;
-  sh.cnt = g_scr.cnt;
-  auto kern = k_gemm<T, BN, AMN, BMN, EPI, SPLIT, CHUNK>;
+  auto kern = k_gemm<T, BN, AMN, BMN, EPI, SPLIT, CHUNK, PAIR>;
   static bool attr_done[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -343,38 +336,34 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
                                  Cf::SMEM_BYTES));
     attr_done[dev & 63] = true;
   }
-  const int sms = num_sms() < kSkSlots / 2 ? num_sms() : kSkSlots / 2;
-  int grid = tiles < sms ? tiles : sms;
-  if (sh.sk) {  // units: whole waves + the leftover tiles x s parts
-    const int dp = sk_dp_tiles(tiles, sms, sh.sk);
-    const long long units = dp + static_cast<long long>(tiles - dp) * sh.sk;
-    grid = static_cast<int>(units < sms ? units : sms);
-    if (dp && grid != sms) return set_err(FI_ERR_ARG, "split-K grid mismatch");
-  }
+  const int slots = num_sms() / NCTA;  // persistent: one CTA (pair) per SM (pair)
+  const int grid = (tiles < slots ? tiles : slots) * NCTA;
   if (grid <= 0) return FI_OK;
   ProfScope prof(EPI == EPI_FWD || EPI == EPI_FWD_H ? FI_PROF_GEMM_FWD
                  : EPI == EPI_WGRAD ? FI_PROF_GEMM_WGRAD
                  : EPI == EPI_STORE ? FI_PROF_PREP : FI_PROF_GEMM_DGRAD, st);
-  kern<<<grid, 256, Cf::SMEM_BYTES, st>>>(ta, tb, ta2, tb2, sh, ep);
-  ++g_launches;
+  if constexpr (PAIR) {
+    FI_TRY(launch_cluster(kern, 2, dim3(grid), dim3(256), Cf::SMEM_BYTES, st, ta, tb, ta2, tb2,
+                          sh, ep));
+  } else {
+    kern<<<grid, 256, Cf::SMEM_BYTES, st>>>(ta, tb, ta2, tb2, sh, ep);
+    ++g_launches;
+  }
   FI_CUDA(cudaGetLastError());
   return FI_OK;
 }
 
-// N tile and schedule per launch from a cost model in units of one 128x256
-// k-iteration (~0.45 us of tensor-pipe time per SM):
-//   whole tiles   ceil(T / G) * k_iters * t(bn),  T = ceil(M/128) * ceil(N/bn)
-//   split-K tail  (T / G) whole waves, then the T % G leftover tiles (all T
-//                 when T < G) cut into s <= 4 K-ranges dealt over the G CTAs:
-//                 ceil(r s / G) * k_iters / s * t(bn), plus the partials
-//                 (one 128 x bn fp32 write per unit, s reads by the finisher).
-// The N tile is free in steps of 32 (K-major B) or of one 128-B atom
-// (MN-major B), so the tile count can be matched to whole waves of the 148
-// SMs instead of leaving a partial last wave idle.  t(bn) = 0.45 + 0.55 bn/256
-// is fitted to B200 measurements (scripts/gemm_micro.py): a k-iteration has a
-// fixed A-tile / issue cost plus a part proportional to the N tile.
-// FI_GEMM_SK=0 (whole tiles) / FI_GEMM_SK=s (force s) and FI_GEMM_BN force
-// the choice for A/B runs.
+// Tile shape per launch from a cost model in units of one single-CTA
+// 128 x 256 k-iteration: ceil(T / slots) * k_iters * t, with
+//   single CTA  T = ceil(M/128) ceil(N/bn) over 148 slots, t = 0.77 + 0.23 bn/256
+//   CTA pair    T = ceil(M/256) ceil(N/bn) over  74 slots, t = t_pair(bn)
+// fitted to B200 measurements (scripts/gemm_bn_sweep.py): a k-iteration's
+// cost is dominated by the operand bytes each SM pulls through L2 (A rows +
+// B rows, the pair halving B), not by the tensor pipe, so narrow N tiles
+// are nearly as expensive as wide ones and pairs win whenever the M tiles
+// fill.  The N tile is free in steps of 32 (K-major B) or of one 128-B
+// atom per CTA (MN-major B), so the tile count can be matched to whole
+// waves.  FI_GEMM_PAIR=0/1 and FI_GEMM_BN force the choice for A/B runs.
 int gemm_env(const char* name, int dflt) {
   const char* e = getenv(name);
   return e ? atoi(e) : dflt;
@@ -382,38 +371,31 @@ int gemm_env(const char* name, int dflt) {
 
 struct GemmChoice {
   int bn;
-  int sk;  // split-K parts of the leftover tiles (<= 1: none)
+  bool pair;
 };
 
-GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int bn_step) {
-  const int G = num_sms() < kSkSlots / 2 ? num_sms() : kSkSlots / 2;
-  const long long mt = (M + 127) / 128;
-  static const int force_sk = gemm_env("FI_GEMM_SK", 0);  // split-K off by default (measured slower)
+double gemm_t_single(int bn) { return 0.77 + 0.23 * bn / 256.0; }
+double gemm_t_pair(int bn) { return 0.56 + 0.20 * bn / 256.0; }
+
+GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int step_single,
+                       int step_pair) {
+  static const int force_pair = gemm_env("FI_GEMM_PAIR", -1);
   static const int force_bn = gemm_env("FI_GEMM_BN", 0);
-  GemmChoice best{0, 0};
+  GemmChoice best{0, false};
   double best_cost = 1e300;
-  for (int bn = bn_max; bn >= 64; bn -= bn_step) {
-    if (force_bn && bn != force_bn) continue;
-    const double t_it = 0.45 + 0.55 * bn / 256.0;
-    const long long T = mt * ((N + bn - 1) / bn);
-    const double plain = static_cast<double>((T + G - 1) / G) * k_iters * t_it;
-    if (force_sk <= 1 && plain < best_cost * 0.995) {
-      best_cost = plain;
-      best = {bn, 0};
-    }
-    if (force_sk == 0 || T > kSkCounters) continue;
-    const long long dp = T >= G ? (T / G) * G : 0;
-    const long long r = T - dp;
-    if (r == 0) continue;
-    for (int s = 2; s <= kMaxSplit && s <= k_iters; ++s) {
-      if (r * s > 2LL * G) break;
-      if (force_sk > 1 && s != force_sk) continue;
-      const double tail = static_cast<double>((r * s + G - 1) / G) * k_iters / s * t_it;
-      const double cost = static_cast<double>(dp / G) * k_iters * t_it + tail +
-                          3.0 * (1 + s) * bn / 256.0;
-      if (cost < best_cost * 0.97 || force_sk > 1) {
+  for (int pair = 0; pair < 2; ++pair) {
+    if (force_pair >= 0 && pair != force_pair) continue;
+    const int step = pair ? step_pair : step_single;
+    const int slots = num_sms() / (pair ? 2 : 1);
+    const long long mt = (M + (pair ? 255 : 127)) / (pair ? 256 : 128);
+    for (int bn = bn_max / step * step; bn >= 64 && bn >= step; bn -= step) {
+      if (force_bn && bn != force_bn) continue;
+      const long long T = mt * ((N + bn - 1) / bn);
+      const double t = pair ? gemm_t_pair(bn) : gemm_t_single(bn);
+      const double cost = static_cast<double>((T + slots - 1) / slots) * k_iters * t;
+      if (cost < best_cost * 0.995) {
         best_cost = cost;
-        best = {bn, s};
+        best = {bn, pair != 0};
       }
     }
   }
@@ -431,11 +413,17 @@ int run_gemm_s(const Operand& A, const Operand& B, int M, int N, int K, int a_ro
   // fp32 mode: chunked round-to-nearest accumulation (8 K-iterations per
   // TMEM chunk) to bound the tensor-core truncation bias; N tile <= 128.
   constexpr int kBnMax = SPLIT ? 128 : 256;
-  const int step = BMN ? (ATOM > 32 ? ATOM : 32) : 32;
-  const GemmChoice c = choose_gemm(M, N, k_iters, kBnMax, step);
+  constexpr int kChunk = SPLIT ? 8 : 0;
+  // MN-major B is staged in whole 128-B atoms per CTA
+  const int step1 = BMN ? (ATOM > 32 ? ATOM : 32) : 32;
+  const int step2 = BMN ? 2 * ATOM : 32;
+  const GemmChoice c = choose_gemm(M, N, k_iters, kBnMax, step1, step2);
   if (c.bn == 0) return set_err(FI_ERR_ARG, "no GEMM tile for N=%d (FI_GEMM_BN?)", N);
-  return launch_gemm<T, kBnMax, AMN, BMN, EPI, SPLIT, SPLIT ? 8 : 0>(A, B, M, N, K, a_row0, ep,
-                                                                     st, c.bn, c.sk);
+  if (c.pair)
+    return launch_gemm<T, kBnMax, AMN, BMN, EPI, SPLIT, kChunk, true>(A, B, M, N, K, a_row0, ep,
+                                                                      st, c.bn);
+  return launch_gemm<T, kBnMax, AMN, BMN, EPI, SPLIT, kChunk, false>(A, B, M, N, K, a_row0, ep,
+                                                                     st, c.bn);
 }
 
 // Dispatch on the split (fp32 / bf16x3) mode; tf32 operands are never split.
@@ -467,25 +455,6 @@ int set_smem(K kern, size_t bytes) {
   return FI_OK;
 }
 
-template <typename K, typename... Args>
-int launch_cluster(K kern, int cluster, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-                   Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cluster;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  FI_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
-  ++g_launches;
-  return FI_OK;
-}
 
 int check_ptrs(std::initializer_list<const void*> ps) {
   for (const void* p : ps)
@@ -665,6 +634,8 @@ int backward_impl(const Plan& p, const float* L, const float* R, const float* ro
                                                    static_cast<int>(ep.row0), ep, st)));
     } else {
       ep.dunary = dunary;
+      ep.vec4 = (p.P % 4 == 0 && reinterpret_cast<uintptr_t>(dunary) % 16 == 0 &&
+                 reinterpret_cast<uintptr_t>(unary) % 16 == 0);
       ep.unary = unary;
       ep.P = p.P;
       ep.lmax = p.l;
@@ -681,6 +652,9 @@ int backward_impl(const Plan& p, const float* L, const float* R, const float* ro
   ep.dR = dR;
   ep.n_nt = p.N;
   ep.ld_lr = p.N + p.P;
+  ep.vec4 = ((p.N + p.P) % 4 == 0 && p.N % 4 == 0 && reinterpret_cast<uintptr_t>(L) % 16 == 0 &&
+             reinterpret_cast<uintptr_t>(R) % 16 == 0 && reinterpret_cast<uintptr_t>(dL) % 16 == 0 &&
+             reinterpret_cast<uintptr_t>(dR) % 16 == 0);
   ep.Np = p.Np;
   ep.M = 2 * p.Np;
   const long long r2 = rowbase(2, p.B, p.l), rl = rowbase(p.l, p.B, p.l);
@@ -744,8 +718,6 @@ int fi_inside_forward(const fi_shape* shape, const float* L, const float* R, con
   FI_TRY(check_ptrs({L, R, root, unary, lengths, log_z, ws}));
   FI_TRY(load_encode());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  ScratchScope scr(at<float>(ws, p.skpart), at<int>(ws, p.skcnt));
-  FI_CUDA(cudaMemsetAsync(at<int>(ws, p.skcnt), 0, 4ull * kSkCounters, st));
   if (p.tf32) {
     if (p.half_chart) return forward_impl<float, __half>(p, L, R, root, unary, lengths, log_z, ws, st);
     return forward_impl<float, float>(p, L, R, root, unary, lengths, log_z, ws, st);
@@ -764,8 +736,6 @@ int fi_inside_backward(const fi_shape* shape, const float* L, const float* R, co
   FI_TRY(check_ptrs({L, R, root, unary, lengths, log_z, grad_log_z, dL, dR, droot, dunary, ws}));
   FI_TRY(load_encode());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  ScratchScope scr(at<float>(ws, p.skpart), at<int>(ws, p.skcnt));
-  FI_CUDA(cudaMemsetAsync(at<int>(ws, p.skcnt), 0, 4ull * kSkCounters, st));
 #define FI_BWD(T, CT)                                                                      \
   return backward_impl<T, CT>(p, L, R, root, unary, lengths, log_z, grad_log_z, dL, dR, droot, \
                               dunary, ws, st)
@@ -800,16 +770,6 @@ int fi_test_gemm(int32_t dtype, int32_t a_mn, int32_t b_mn, int32_t M, int32_t N
   if (M < 1 || N < 64 || N % 64 || K < 1)
     return set_err(FI_ERR_ARG, "test GEMM needs M>=1, N%%64==0, K>=1");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  void* scratch = nullptr;
-  FI_CUDA(cudaMallocAsync(&scratch, kSkPartBytes + 4ull * kSkCounters, st));
-  FI_CUDA(cudaMemsetAsync(static_cast<uint8_t*>(scratch) + kSkPartBytes, 0, 4ull * kSkCounters, st));
-  struct Free {
-    void* p;
-    cudaStream_t s;
-    ~Free() { cudaFreeAsync(p, s); }
-  } free_scratch{scratch, st};
-  ScratchScope scr(static_cast<float*>(scratch),
-                   reinterpret_cast<int*>(static_cast<uint8_t*>(scratch) + kSkPartBytes));
   GemmEpi ep = {};
   ep.M = M;
   ep.C = C;

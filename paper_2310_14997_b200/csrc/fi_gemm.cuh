@@ -6,10 +6,19 @@
 // A and B are staged by TMA into 128B-swizzled shared memory; either operand
 // may be K-major (rows of K contiguous) or MN-major (rows of MN contiguous,
 // i.e. the K index is the outer, strided dimension).  One elected thread
-// issues tcgen05.mma (M=128, N=BN, K=16 for bf16 / 8 for tf32) into one of
-// two TMEM accumulators, so the epilogue of tile t overlaps the main loop of
-// tile t+1.  The epilogue reads TMEM with tcgen05.ld and applies one of the
-// inside-algorithm transforms (see EpiMode) before writing fp32 to HBM.
+// issues tcgen05.mma (K=16 for bf16 / 8 for tf32) into one of two TMEM
+// accumulators, so the epilogue of tile t overlaps the main loop of tile
+// t+1.  The epilogue reads TMEM with tcgen05.ld and applies one of the
+// inside-algorithm transforms (see EpiMode) before writing to HBM.
+//
+// PAIR: a cluster of two CTAs (one TPC) computes a 256 x bn tile with
+// tcgen05.mma.cta_group::2 -- each CTA stages its own 128 rows of A and
+// half (bn/2 rows) of B, so the L2 -> SM operand traffic per flop drops by a
+// third against single-CTA 128 x bn tiles (the measured limit of those: the
+// chip's TMA/L2 read rate, not the tensor pipe).  The leader CTA (rank 0)
+// issues the MMAs; both CTAs' TMA loads complete on the leader's full
+// barriers, MMA commits multicast to both CTAs' empty / TMEM-full barriers,
+// and both CTAs' epilogue warps release the leader's TMEM-empty barrier.
 //
 // Warp roles (256 threads): w0 = TMA producer, w1 = MMA issuer,
 // w2 = TMEM allocator, w4..w7 = epilogue (TMEM lane quadrant = warp % 4).
@@ -32,65 +41,9 @@ enum EpiMode : int {
 struct GemmShape {
   int M, N, K;    // logical problem; rows >= M are masked in the epilogue
   int a_row0;     // K-major A: first row coordinate inside the tensor map
-  int num_m, num_n, num_k;
-  int bn;         // N tile (runtime, <= the kernel's BN template bound, multiple of 32)
-  // Split-K tail (sk = s > 1): tiles [0, dp) -- whole waves -- run round
-  // robin; each remaining tile (the partial last wave, or every tile when
-  // there are fewer tiles than CTAs) is cut into s K-ranges, and the
-  // (tile, part) units are dealt round robin too, so concurrently running
-  // CTAs sit at no more than s distinct K offsets and keep sharing the
-  // operand K-slabs through L2.  A split tile is summed by the last of its s
-  // units to finish (per-tile arrival counter), in part order (deterministic),
-  // which then runs the epilogue.  sk <= 1: whole tiles only.
-  int sk;
-  float* part;    // sk: 2 partial tiles (128 x 256 fp32) per CTA
-  int* cnt;       // sk: per-tile arrival counters, zero between launches
+  int num_m, num_n, num_k;  // tiles of (128 or 256 for pairs) x bn x BK
+  int bn;         // N tile (runtime, <= the kernel's BN bound, multiple of 32)
 };
-
-// Work assignment of one CTA: a sequence of (tile, k-iteration range) segments.
-__host__ __device__ __forceinline__ int sk_dp_tiles(int T, int G, int s) {
-  if (s <= 1) return T;
-  return T >= G ? (T / G) * G : 0;
-}
-
-struct WorkIter {
-  int u, U, s, dp, T, kI, G;
-  __device__ __forceinline__ WorkIter(const GemmShape& sh, int k_iters) {
-    T = sh.num_m * sh.num_n;
-    kI = k_iters;
-    G = gridDim.x;
-    s = sh.sk > 1 ? sh.sk : 1;
-    dp = sk_dp_tiles(T, G, s);
-    U = dp + (T - dp) * s;  // units: dp whole tiles, then (tile, part) pairs
-    u = blockIdx.x;
-  }
-  // unit -> (tile, k0, k1)
-  __device__ __forceinline__ void unit(int v, int& t, int& k0, int& k1) const {
-    if (v < dp) {
-      t = v;
-      k0 = 0;
-      k1 = kI;
-      return;
-    }
-    const int w = v - dp;
-    t = dp + w / s;
-    const int p = w % s;
-    k0 = static_cast<int>(static_cast<long long>(kI) * p / s);
-    k1 = static_cast<int>(static_cast<long long>(kI) * (p + 1) / s);
-  }
-  __device__ __forceinline__ bool next(int& t, int& k0, int& k1) {
-    if (u >= U) return false;
-    unit(u, t, k0, k1);
-    u += G;
-    return true;
-  }
-};
-
-constexpr int kMaxSplit = 4;  // split-K parts per tile (finisher keeps all loads in flight)
-
-__device__ __forceinline__ void epi_bar() {  // the 4 epilogue warps only
-  asm volatile("bar.sync 1, 128;" ::: "memory");
-}
 
 struct GemmEpi {
   int M;              // valid output rows
@@ -122,6 +75,7 @@ struct GemmEpi {
   // EPI_STORE
   float* C;
   int ldc;
+  int vec4;           // EPI_DUNARY / EPI_WGRAD rows 16-B aligned: vector loads/stores
 };
 
 template <typename T, int BN>  // BN: the largest N tile the smem ring is sized for
@@ -186,25 +140,54 @@ __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int lrow, long long
   } else if constexpr (EPI == EPI_DUNARY) {
     // rowptr = dunary row, aux = 1 if the token position is inside the sentence
     const float* un = ep.unary + static_cast<long long>(lrow) * ep.P;
+    if (ep.vec4 && col + 32 <= ep.P) {  // 16-B loads/stores (one 128-B line per thread)
+      const float4* u4 = reinterpret_cast<const float4*>(un + col);
+      float4* d4 = reinterpret_cast<float4*>(rowptr + col);
 #pragma unroll
-    for (int t = 0; t < 32; ++t) {
-      int c = col + t;
-      if (c < ep.P) rowptr[c] = aux ? v[t] * ex2(fmaf(un[c], 1.4426950408889634f, -xv)) : 0.f;
+      for (int q = 0; q < 8; ++q) {
+        const float4 u = __ldg(u4 + q);
+        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (aux) {
+          o.x = v[4 * q + 0] * ex2(fmaf(u.x, 1.4426950408889634f, -xv));
+          o.y = v[4 * q + 1] * ex2(fmaf(u.y, 1.4426950408889634f, -xv));
+          o.z = v[4 * q + 2] * ex2(fmaf(u.z, 1.4426950408889634f, -xv));
+          o.w = v[4 * q + 3] * ex2(fmaf(u.w, 1.4426950408889634f, -xv));
+        }
+        d4[q] = o;
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        int c = col + t;
+        if (c < ep.P) rowptr[c] = aux ? v[t] * ex2(fmaf(un[c], 1.4426950408889634f, -xv)) : 0.f;
+      }
     }
   } else if constexpr (EPI == EPI_WGRAD) {
     // rowptr = d{L,R} row start; aux selects the right table; lrow = table row
+    const float* lr = (aux ? ep.Rsrc : ep.Lsrc) + static_cast<long long>(lrow) * ep.ld_lr;
+    if (ep.vec4 && col + 32 <= ep.valid_cols) {
+      const float4* l4 = reinterpret_cast<const float4*>(lr + ep.col_off + col);
+      float4* d4 = reinterpret_cast<float4*>(rowptr + ep.col_off + col);
 #pragma unroll
-    for (int t = 0; t < 32; ++t) {
-      int c = col + t;
-      if (c < ep.valid_cols) {
-        long long off = static_cast<long long>(ep.col_off + c);
-        const float* lr = (aux ? ep.Rsrc : ep.Lsrc) + static_cast<long long>(lrow) * ep.ld_lr;
-        rowptr[off] = expf(lr[off]) * v[t];
+      for (int q = 0; q < 8; ++q) {
+        const float4 u = __ldg(l4 + q);
+        d4[q] = make_float4(expf(u.x) * v[4 * q], expf(u.y) * v[4 * q + 1],
+                            expf(u.z) * v[4 * q + 2], expf(u.w) * v[4 * q + 3]);
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        int c = col + t;
+        if (c < ep.valid_cols) {
+          long long off = static_cast<long long>(ep.col_off + c);
+          rowptr[off] = expf(lr[off]) * v[t];
+        }
       }
     }
-  } else {  // EPI_STORE
+  } else {  // EPI_STORE (test hook; ldc is a multiple of 64, rows 16-B aligned)
+    float4* dst = reinterpret_cast<float4*>(rowptr + col);
 #pragma unroll
-    for (int t = 0; t < 32; ++t) rowptr[col + t] = v[t];
+    for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
   }
 }
 
@@ -219,12 +202,13 @@ __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int lrow, long long
 // accumulator is handed to the epilogue warps, which add it into a
 // round-to-nearest fp32 register sum and hand it back (double-buffered), so
 // the bias is bounded by the chunk length whatever K is.  Requires BN <= 128.
-template <typename T, int BN, bool A_MN, bool B_MN, int EPI, bool SPLIT, int CHUNK>
+template <typename T, int BN, bool A_MN, bool B_MN, int EPI, bool SPLIT, int CHUNK, bool PAIR>
 __global__ void __launch_bounds__(256, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
            GemmShape sh, GemmEpi ep) {
   using C = GemmCfg<T, BN>;
+  constexpr int NCTA = PAIR ? 2 : 1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -238,9 +222,13 @@ __global__ void __launch_bounds__(256, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const int num_tiles = sh.num_m * sh.num_n;
   const int k_iters = SPLIT ? 3 * sh.num_k : sh.num_k;
-  const int bn = sh.bn;  // runtime N tile <= BN (the smem / TMEM layout bound)
-  int* bcast = reinterpret_cast<int*>(tslot + 1);
+  const int bn = sh.bn;                       // runtime N tile <= BN
+  const int bn_cta = bn / NCTA;               // B rows staged by this CTA
+  const uint32_t rank = PAIR ? cluster_rank() : 0;
+  const int tile0 = PAIR ? blockIdx.x / 2 : blockIdx.x;
+  const int tstep = PAIR ? gridDim.x / 2 : gridDim.x;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -255,13 +243,17 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], 4 * NCTA);
     }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc<C::TMEM_COLS>(tslot);
+  if (warp == 2) {
+    if constexpr (PAIR) tmem_alloc2<C::TMEM_COLS>(tslot);
+    else tmem_alloc<C::TMEM_COLS>(tslot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // barrier inits visible to the peer
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tslot;
 
@@ -270,35 +262,44 @@ __global__ void __launch_bounds__(256, 1)
       // ------------------------------------------------ TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      WorkIter wi(sh, k_iters);
-      int tile, k0, k1;
-      while (wi.next(tile, k0, k1)) {
+      const uint32_t stage_tx = NCTA * (C::A_BYTES + bn_cta * 128);
+      for (int tile = tile0; tile < num_tiles; tile += tstep) {
         const int m_blk = tile % sh.num_m;
         const int n_blk = tile / sh.num_m;
-        for (int it = k0; it < k1; ++it) {
+        const int m0 = m_blk * (C::BM * NCTA) + rank * C::BM;  // this CTA's A rows
+        const int n0 = n_blk * bn + rank * bn_cta;              // this CTA's B rows
+        for (int it = 0; it < k_iters; ++it) {
           const int pass = SPLIT ? it / sh.num_k : 0;
           const int kb = SPLIT ? it - pass * sh.num_k : it;
           const CUtensorMap* ma = (SPLIT && pass == 0) ? &tmA2 : &tmA;
           const CUtensorMap* mb = (SPLIT && pass == 1) ? &tmB2 : &tmB;
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], C::A_BYTES + bn * 128);
           uint8_t* a_dst = smA + stage * C::A_BYTES;
           uint8_t* b_dst = smB + stage * C::B_BYTES;
+          // completion is counted on the leader's full barrier (both CTAs' bytes)
+          uint32_t fb = smem_u32(&full[stage]);
+          if constexpr (PAIR) {
+            fb = mapa_rank(&full[stage], 0);
+            if (rank == 0) mbar_expect_tx(&full[stage], stage_tx);
+          } else {
+            mbar_expect_tx(&full[stage], stage_tx);
+          }
+          auto load = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
+            if constexpr (PAIR) tma_load_2d_pair(dst, m, fb, c0, c1);
+            else tma_load_2d(dst, m, &full[stage], c0, c1);
+          };
           if constexpr (!A_MN) {
-            tma_load_2d(a_dst, ma, &full[stage], kb * C::BK, sh.a_row0 + m_blk * C::BM);
+            load(a_dst, ma, kb * C::BK, sh.a_row0 + m0);
           } else {
 #pragma unroll
             for (int j = 0; j < C::BM / C::ATOM; ++j)
-              tma_load_2d(a_dst + j * C::BK * 128, ma, &full[stage], m_blk * C::BM + j * C::ATOM,
-                          kb * C::BK);
+              load(a_dst + j * C::BK * 128, ma, m0 + j * C::ATOM, kb * C::BK);
           }
           if constexpr (!B_MN) {
-            tma_load_2d(b_dst, mb, &full[stage], kb * C::BK, n_blk * bn);
+            load(b_dst, mb, kb * C::BK, n0);
           } else {
-#pragma unroll
-            for (int j = 0; j < bn / C::ATOM; ++j)
-              tma_load_2d(b_dst + j * C::BK * 128, mb, &full[stage], n_blk * bn + j * C::ATOM,
-                          kb * C::BK);
+            for (int j = 0; j < bn_cta / C::ATOM; ++j)
+              load(b_dst + j * C::BK * 128, mb, n0 + j * C::ATOM, kb * C::BK);
           }
           if (++stage == C::STAGES) {
             stage = 0;
@@ -308,9 +309,9 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------ MMA issuer
-      const uint32_t idesc = make_idesc<C::TF32>(bn, A_MN, B_MN);
+    if (lane == 0 && rank == 0) {
+      // ------------------------------------------------ MMA issuer (leader)
+      const uint32_t idesc = make_idesc<C::TF32>(bn, A_MN, B_MN, C::BM * NCTA);
       constexpr uint32_t a_lbo = A_MN ? C::BK * 128 : 16;
       constexpr uint32_t b_lbo = B_MN ? C::BK * 128 : 16;
       // tf32 MN-major operands use the 32B-atom 128B swizzle (4-row groups)
@@ -324,13 +325,11 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      WorkIter wi(sh, k_iters);
-      int tile, k0, k1;
-      while (wi.next(tile, k0, k1)) {
+      const int cl = CHUNK > 0 ? CHUNK : k_iters;
+      for (int tile = tile0; tile < num_tiles; tile += tstep) {
         uint32_t d_tmem = tmem_base;
-        const int cl = CHUNK > 0 ? CHUNK : (k1 - k0);
-        for (int kb = k0; kb < k1; ++kb) {
-          const int kc = (kb - k0) % cl;
+        for (int kb = 0; kb < k_iters; ++kb) {
+          const int kc = kb % cl;
           if (kc == 0) {  // start a chunk in a drained accumulator
             mbar_wait(&tempty[acc], acc_phase ^ 1);
             tc_fence_after();
@@ -344,15 +343,18 @@ __global__ void __launch_bounds__(256, 1)
           for (int k = 0; k < C::BK / C::UK; ++k) {
             uint64_t ad = make_sdesc(a_base + k * a_kstep, a_lbo, a_sbo, a_lay);
             uint64_t bd = make_sdesc(b_base + k * b_kstep, b_lbo, b_sbo, b_lay);
-            umma<C::TF32>(d_tmem, ad, bd, idesc, (kc | k) != 0 ? 1u : 0u);
+            if constexpr (PAIR) umma2<C::TF32>(d_tmem, ad, bd, idesc, (kc | k) != 0 ? 1u : 0u);
+            else umma<C::TF32>(d_tmem, ad, bd, idesc, (kc | k) != 0 ? 1u : 0u);
           }
-          umma_commit(&empty[stage]);
+          if constexpr (PAIR) umma_commit2(&empty[stage]);
+          else umma_commit(&empty[stage]);
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
-          if (kc == cl - 1 || kb == k1 - 1) {
-            umma_commit(&tfull[acc]);
+          if (kc == cl - 1 || kb == k_iters - 1) {
+            if constexpr (PAIR) umma_commit2(&tfull[acc]);
+            else umma_commit(&tfull[acc]);
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
           }
@@ -365,14 +367,22 @@ __global__ void __launch_bounds__(256, 1)
     const int r = quad * 32 + lane;  // accumulator row (TMEM lane)
     int acc = 0;
     uint32_t acc_phase = 0;
-    WorkIter wi(sh, k_iters);
-    int tile, k0, k1;
-    int nsplit = 0;  // split units this CTA has finished (partial slot index)
-    while (wi.next(tile, k0, k1)) {
-      const bool whole = (k0 == 0 && k1 == k_iters);
+    // TMEM-empty arrivals go to the leader (its MMA issuer reuses the buffer)
+    uint32_t te[2];
+    te[0] = PAIR ? mapa_rank(&tempty[0], 0) : smem_u32(&tempty[0]);
+    te[1] = PAIR ? mapa_rank(&tempty[1], 0) : smem_u32(&tempty[1]);
+    auto release = [&](int a) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (PAIR) mbar_arrive_cluster(te[a]);
+        else mbar_arrive(&tempty[a]);
+      }
+    };
+    for (int tile = tile0; tile < num_tiles; tile += tstep) {
       const int m_blk = tile % sh.num_m;
       const int n_blk = tile / sh.num_m;
-      const int lrow = m_blk * C::BM + r;  // row within this GEMM
+      const int lrow = m_blk * (C::BM * NCTA) + rank * C::BM + r;  // row within this GEMM
       const long long grow = ep.row0 + lrow;
       const bool row_ok = lrow < ep.M;
       float xv = 0.f;
@@ -427,15 +437,6 @@ __global__ void __launch_bounds__(256, 1)
         epi_chunk<EPI>(ep, erow, grow, col, v, xv, ok, rp, aux);
       };
       const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
-      // partial-tile slot: this CTA's n-th split unit (the host keeps the split
-      // units <= 2 G, so a CTA gets at most 2 and slots are never reused)
-      float* my_part = sh.part + (static_cast<size_t>(blockIdx.x) * 2 + (nsplit & 1)) * (128 * 256);
-      auto put_part = [&](int j, const float (&v)[32]) {
-        float4* dst = reinterpret_cast<float4*>(my_part + (j * 128 + r) * 32);
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-      };
       if constexpr (CHUNK == 0) {
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
@@ -444,14 +445,9 @@ __global__ void __launch_bounds__(256, 1)
         for (int j = 0; j < bn / 32; ++j) {
           float v[32];
           tmem_ld32(t_row + j * 32, v);
-          if (whole)
-            emit(j, v);
-          else
-            put_part(j, v);
+          emit(j, v);
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        release(acc);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       } else {
@@ -461,7 +457,7 @@ __global__ void __launch_bounds__(256, 1)
         for (int j = 0; j < BN / 32; ++j)
 #pragma unroll
           for (int t = 0; t < 32; ++t) sum[j][t] = 0.f;
-        const int nchunks = (k1 - k0 + CHUNK - 1) / CHUNK;
+        const int nchunks = (k_iters + CHUNK - 1) / CHUNK;
         for (int c = 0; c < nchunks; ++c) {
           mbar_wait(&tfull[acc], acc_phase);
           tc_fence_after();
@@ -475,86 +471,25 @@ __global__ void __launch_bounds__(256, 1)
               for (int t = 0; t < 32; ++t) sum[j][t] += v[t];
             }
           }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
+          release(acc);
           acc ^= 1;
           if (acc == 0) acc_phase ^= 1;
         }
 #pragma unroll
-        for (int j = 0; j < BN / 32; ++j) {
-          if (j < bn / 32) {
-            if (whole)
-              emit(j, sum[j]);
-            else
-              put_part(j, sum[j]);
-          }
-        }
-      }
-      if (!whole) {
-        // publish the partial; the last of the tile's s units finishes it
-        ++nsplit;
-        __threadfence();
-        epi_bar();
-        if (warp == 4 && lane == 0) {
-          const int old = atomicAdd(&sh.cnt[tile], 1);
-          const int last = old == wi.s - 1;
-          if (last) {
-            __threadfence();
-            sh.cnt[tile] = 0;  // ready for the next launch
-          }
-          *bcast = last;
-        }
-        epi_bar();
-        const int last = *bcast;
-        epi_bar();  // bcast is reused by the next split unit
-        if (last) {
-          const int u0 = wi.dp + (tile - wi.dp) * wi.s;  // unit of part 0
-#pragma unroll 1
-          for (int j = 0; j < bn / 32; ++j) {
-            float v[32];
-#pragma unroll
-            for (int t = 0; t < 32; ++t) v[t] = 0.f;
-            // all parts' loads in flight at once (s <= kMaxSplit), then a
-            // part-order sum: deterministic whatever the arrival order
-            float4 w4[kMaxSplit][8];
-#pragma unroll
-            for (int p = 0; p < kMaxSplit; ++p) {
-              if (p < wi.s) {
-                const int uu = u0 + p;
-                const int c = uu % wi.G;
-                // dp is a multiple of G: CTA c's split units are dp + c, dp + c + G
-                const int nth = (uu - wi.dp) / wi.G;
-                const float4* src = reinterpret_cast<const float4*>(
-                    sh.part + (static_cast<size_t>(c) * 2 + (nth & 1)) * (128 * 256) +
-                    (j * 128 + r) * 32);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) w4[p][q] = __ldcg(src + q);
-              }
-            }
-#pragma unroll
-            for (int p = 0; p < kMaxSplit; ++p) {
-              if (p < wi.s) {
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                  v[4 * q] += w4[p][q].x;
-                  v[4 * q + 1] += w4[p][q].y;
-                  v[4 * q + 2] += w4[p][q].z;
-                  v[4 * q + 3] += w4[p][q].w;
-                }
-              }
-            }
-            emit(j, v);
-          }
-        }
+        for (int j = 0; j < BN / 32; ++j)
+          if (j < bn / 32) emit(j, sum[j]);
       }
     }
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // the peer's MMAs / arrivals are done
+  else __syncthreads();
   tc_fence_after();
-  if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tmem_base);
+  if (warp == 2) {
+    if constexpr (PAIR) tmem_dealloc2<C::TMEM_COLS>(tmem_base);
+    else tmem_dealloc<C::TMEM_COLS>(tmem_base);
+  }
 }
 
 }  // namespace fi
