@@ -122,12 +122,14 @@ def gather_launch_bytes(n: int, batch: int, length: int, m: int, gemm_esz: int,
     onto the S_m = (l-m)(l-m+1)/2 spans of width > m (resp. < l-m+1), and
     every parent row is shared by its left and right child, so the launch
     must read 2 * S_m distinct a/b rows (chart_esz bytes per element) and
-    S_m fp32 LQ rows; plus the child's own a, b rows (the -inf guard) and its
-    2N-wide G row written in the operand type."""
+    S_m outside-weight rows (fp32, or fp16 plus one fp32 exponent per 32
+    columns with the fp16 chart); plus the child's own a, b rows (the -inf
+    guard) and its 2N-wide G row written in the operand type."""
     l = length
     s_m = (l - m) * (l - m + 1) // 2
     n_m = l - m + 1
-    return batch * (s_m * n * (2.0 * chart_esz + 4.0)
+    lq_esz = 4.0 if chart_esz == 4 else 2.0 + 4.0 / 32
+    return batch * (s_m * n * (2.0 * chart_esz + lq_esz)
                     + n_m * (2 * n * chart_esz + 2 * n * gemm_esz))
 
 

@@ -79,7 +79,8 @@ typedef struct fi_shape {
  * with x[row] the fp64 per-span shift (off_x) and the stored fp32 offsets
  * a^, b^, o^ (o^ <= 0) and, after a backward, lq^ = log2|go| - log2 o + x.
  * With chart_fmt == FI_CHART_F16 the a/b arrays hold fp16 s = acc * 2^14
- * (row stride np halves), i.e. a^ = log2(s) - 14. */
+ * (row stride np halves), i.e. a^ = log2(s) - 14, and lq holds fp16 q with
+ * lq^ = log2(q) + e[row, A / 32] (e: fp32 exponents at off_lqs). */
 typedef struct fi_chart_layout {
   int64_t np;       /* padded N (row stride, floats)          */
   int64_t pp;       /* padded P                               */
@@ -90,7 +91,8 @@ typedef struct fi_chart_layout {
   int64_t off_x;    /* x†    fp64 per row (log2 units)        */
   int64_t off_lq;   /* log|go|-o, widths 2..l (after backward)*/
   int64_t off_flag; /* int32 error flags (bit0: non-finite logZ in backward) */
-  int64_t chart_fmt; /* FI_CHART_F32 or FI_CHART_F16: storage of a, b     */
+  int64_t chart_fmt; /* FI_CHART_F32 or FI_CHART_F16: storage of a, b, lq */
+  int64_t off_lqs;   /* FI_CHART_F16: fp32 exponent per 32 columns of lq (-1 otherwise) */
 } fi_chart_layout;
 
 /* Workspace bytes needed for `shape` (0 on invalid shape). */

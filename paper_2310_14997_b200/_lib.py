@@ -54,6 +54,7 @@ class FiChartLayout(Structure):
         ("off_lq", c_int64),
         ("off_flag", c_int64),
         ("chart_fmt", c_int64),
+        ("off_lqs", c_int64),
     ]
 
 

@@ -110,7 +110,7 @@ struct Plan {
   int N, P, B, l, Np, Pp, esz;
   Decomp dsplit, dgather;
   long long rows;
-  size_t wnn, wnp, e1, eall, gall, a, b, o, lq, x, top, topz, wsum, flag, total;
+  size_t wnn, wnp, e1, eall, gall, a, b, o, lq, lqs, x, top, topz, wsum, flag, total;
   // element offsets of the lo planes of the GEMM operands (fp32 mode only)
   long long wnn_lo, wnp_lo, e1_lo, eall_lo, gall_lo;
   bool store_o, tf32, split, half_chart;
@@ -209,7 +209,8 @@ int make_plan(const fi_shape* s, Plan* p) {
   p->a = take(ab_esz * rows * p->Np);
   p->b = take(ab_esz * rows * p->Np);
   p->o = p->store_o ? take(4ull * rows * p->Np) : static_cast<size_t>(-1);
-  p->lq = take(4ull * rows * p->Np);
+  p->lq = take(ab_esz * rows * p->Np);  // fp16 |q| in the half chart, else fp32 LQ^
+  p->lqs = p->half_chart ? take(4ull * rows * (p->Np / 32)) : static_cast<size_t>(-1);
   p->x = take(8ull * rows);  // fp64 row shifts
   p->top = take(4ull * p->B * p->Np);
   p->topz = take(4ull * p->B);
@@ -341,7 +342,7 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
   if (grid <= 0) return FI_OK;
   ProfScope prof(EPI == EPI_FWD || EPI == EPI_FWD_H ? FI_PROF_GEMM_FWD
                  : EPI == EPI_WGRAD ? FI_PROF_GEMM_WGRAD
-                 : EPI == EPI_STORE ? FI_PROF_PREP : FI_PROF_GEMM_DGRAD, st);
+                 : EPI == EPI_STORE ? FI_PROF_PREP : FI_PROF_GEMM_DGRAD, st);  // DGRAD(_H), DUNARY
   if constexpr (PAIR) {
     FI_TRY(launch_cluster(kern, 2, dim3(grid), dim3(256), Cf::SMEM_BYTES, st, ta, tb, ta2, tb2,
                           sh, ep));
@@ -567,7 +568,8 @@ int backward_impl(const Plan& p, const float* L, const float* R, const float* ro
   T* gall = at<T>(ws, p.gall);
   float* A = at<float>(ws, p.a);
   float* Bc = at<float>(ws, p.b);
-  float* LQ = at<float>(ws, p.lq);
+  float* LQ = at<float>(ws, p.lq);  // CT-typed storage (see make_plan)
+  float* LQS = p.half_chart ? at<float>(ws, p.lqs) : nullptr;
   double* X = at<double>(ws, p.x);
   float* TOP = at<float>(ws, p.top);
   float* TOPZ = at<float>(ws, p.topz);
@@ -577,7 +579,8 @@ int backward_impl(const Plan& p, const float* L, const float* R, const float* ro
   {
   ProfScope prof(FI_PROF_SEED, st);
   (void)logZ;  // the fp64-consistent log2 Z - x† (TOPZ) is used instead
-  k_seed_bwd<<<(p.Np + 255) / 256, 256, 0, st>>>(root, TOP, TOPZ, g, lengths, LQ, droot, flag,
+  k_seed_bwd<sizeof(CT) == 2><<<(p.Np + 255) / 256, 256, 0, st>>>(root, TOP, TOPZ, g, lengths, LQ,
+                                                                  LQS, droot, flag,
                                                  p.B, p.l, p.N, p.Np);
   ++g_launches;
   FI_CUDA(cudaGetLastError());
@@ -593,6 +596,7 @@ int backward_impl(const Plan& p, const float* L, const float* R, const float* ro
     ga.A = A;
     ga.Bc = Bc;
     ga.LQ = LQ;
+    ga.LQS = LQS;
     ga.X = X;
     ga.G = gall;
     ga.g_lo = p.gall_lo;
@@ -608,8 +612,10 @@ int backward_impl(const Plan& p, const float* L, const float* R, const float* ro
     {
       ProfScope prof(FI_PROF_GATHER, st);
       const int stages = dc.stages;
+      const size_t qb = sizeof(CT) == 2 ? dc.cols_per_cta * 2 + dc.cols_per_cta / 8
+                                         : dc.cols_per_cta * 4;
       const size_t smem = align128(sizeof(GatherTerm) * p.l) +
-                          static_cast<size_t>(stages) * (dc.cols_per_cta * (sizeof(CT) + 4) + 16);
+                          static_cast<size_t>(stages) * (dc.cols_per_cta * sizeof(CT) + qb + 16);
       FI_TRY(dispatch_v(dc.v, [&](auto vc) {
         constexpr int V = decltype(vc)::value;
         FI_TRY(set_smem(k_gather_bwd_bulk<T, CT, V>, smem));
@@ -630,7 +636,9 @@ int backward_impl(const Plan& p, const float* L, const float* R, const float* ro
     ep.n_w = n_m;
     if (m >= 2) {
       ep.LQ = LQ;
-      FI_TRY((run_gemm<T, false, true, EPI_DGRAD>(opGall, opWnnMN, ep.M, p.Np, 2 * p.Np,
+      ep.LQS = LQS;
+      constexpr int kEpiDgrad = sizeof(CT) == 2 ? EPI_DGRAD_H : EPI_DGRAD;
+      FI_TRY((run_gemm<T, false, true, kEpiDgrad>(opGall, opWnnMN, ep.M, p.Np, 2 * p.Np,
                                                    static_cast<int>(ep.row0), ep, st)));
     } else {
       ep.dunary = dunary;
@@ -705,6 +713,7 @@ int fi_get_chart_layout(const fi_shape* shape, fi_chart_layout* out) {
   out->off_o = p.store_o ? static_cast<int64_t>(p.o) : -1;
   out->off_x = static_cast<int64_t>(p.x);
   out->off_lq = static_cast<int64_t>(p.lq);
+  out->off_lqs = p.half_chart ? static_cast<int64_t>(p.lqs) : -1;
   out->off_flag = static_cast<int64_t>(p.flag);
   out->chart_fmt = p.half_chart ? FI_CHART_F16 : FI_CHART_F32;
   return FI_OK;
@@ -757,8 +766,9 @@ int fi_marginals(const fi_shape* shape, const int32_t* lengths, const float* gra
   const long long nrows = p.rows - rowbase(2, p.B, p.l);
   if (nrows <= 0) return FI_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  k_marginals<<<static_cast<unsigned>(nrows), 256, 0, st>>>(
-      at<float>(ws, p.lq), at<float>(ws, p.o), grad_log_z, lengths, mu, p.B, p.l, p.Np, p.N);
+  (p.half_chart ? k_marginals<true> : k_marginals<false>)<<<static_cast<unsigned>(nrows), 256, 0, st>>>(
+      at<float>(ws, p.lq), p.half_chart ? at<float>(ws, p.lqs) : nullptr, at<float>(ws, p.o),
+      grad_log_z, lengths, mu, p.B, p.l, p.Np, p.N);
   FI_CUDA(cudaGetLastError());
   return FI_OK;
 }

@@ -36,6 +36,7 @@ enum EpiMode : int {
   EPI_WGRAD = 3,   // d{L,R} = exp({L,R}) * acc                    (inside.py:446)
   EPI_STORE = 4,   // plain C = acc (GEMM unit tests)
   EPI_FWD_H = 5,   // [a | b] as fp16 acc * 2^kChartScale (half chart, fi_kernels.cuh)
+  EPI_DGRAD_H = 6, // |acc| as fp16 per-32-column scaled + exponent (half chart)
 };
 
 struct GemmShape {
@@ -53,8 +54,9 @@ struct GemmEpi {
   float* outA;
   float* outB;
   int Np;             // padded nonterminal count == row stride of chart arrays
-  // EPI_DGRAD
+  // EPI_DGRAD (EPI_DGRAD_H: LQ is the fp16 array, LQS its per-32-column exponents)
   float* LQ;
+  float* LQS;
   const int* lengths;
   int width;
   int n_w;
@@ -126,6 +128,26 @@ __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int lrow, long long
       }
       dst[q] = u;
     }
+  } else if constexpr (EPI == EPI_DGRAD_H) {
+    float m = 0.f;
+#pragma unroll
+    for (int t = 0; t < 32; ++t) m = fmaxf(m, fabsf(v[t]));
+    const int sc = lq_chunk_exp(m);
+    const float f = exp2_int(-sc);
+    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(rowptr) + col);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 u;
+      uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        __half2 p2 = __floats2half2_rn(fabsf(v[8 * q + 2 * h]) * f,
+                                       fabsf(v[8 * q + 2 * h + 1]) * f);
+        w[h] = *reinterpret_cast<uint32_t*>(&p2);
+      }
+      dst[q] = u;
+    }
+    ep.LQS[grow * (ep.Np / 32) + col / 32] = static_cast<float>(sc);
   } else if constexpr (EPI == EPI_DGRAD) {
     float4* dst = reinterpret_cast<float4*>(rowptr + col);
 #pragma unroll
@@ -399,6 +421,8 @@ __global__ void __launch_bounds__(256, 1)
           rowptr_b = reinterpret_cast<float*>(reinterpret_cast<__half*>(ep.outB) + grow * ep.Np);
         } else if constexpr (EPI == EPI_DGRAD) {
           rowptr = ep.LQ + grow * ep.Np;
+        } else if constexpr (EPI == EPI_DGRAD_H) {
+          rowptr = reinterpret_cast<float*>(reinterpret_cast<__half*>(ep.LQ) + grow * ep.Np);
         } else if constexpr (EPI == EPI_DUNARY) {
           xv = static_cast<float>(ep.X[grow]);
           const int b = lrow / ep.lmax, i = lrow % ep.lmax;
@@ -414,7 +438,7 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
       bool ok = row_ok && rowptr != nullptr;
-      if constexpr (EPI == EPI_DGRAD) {
+      if constexpr (EPI == EPI_DGRAD || EPI == EPI_DGRAD_H) {
         // the seed kernel owns the top span of each sentence (inside.py:400-404)
         if (ok) {
           const int b = lrow / ep.n_w, i = lrow % ep.n_w;

@@ -517,11 +517,13 @@ __global__ void __launch_bounds__(288) k_split_fwd_bulk(SplitArgs a, int stages)
 //   LQ^ = log2|g post| - o + x† = log2 root - (log2 Z - x†) + log2|g|
 // and is itself d_root (times g).  One thread per column; loops sentences.
 // ---------------------------------------------------------------------------
+template <bool kHalfLQ>
 __global__ void k_seed_bwd(const float* __restrict__ root, const float* __restrict__ TOP,
                            const float* __restrict__ TOPZ, const float* __restrict__ g,
-                           const int* __restrict__ lengths, float* __restrict__ LQ,
-                           float* __restrict__ droot, int* __restrict__ flag, int B, int lmax,
-                           int N, int Np) {
+                           const int* __restrict__ lengths, void* __restrict__ LQv,
+                           float* __restrict__ LQS, float* __restrict__ droot,
+                           int* __restrict__ flag, int B, int lmax, int N, int Np) {
+  // blockDim is a multiple of 32 and Np of 256: each warp owns one 32-column chunk
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= Np) return;
   float acc = 0.f;
@@ -535,7 +537,18 @@ __global__ void k_seed_bwd(const float* __restrict__ root, const float* __restri
       lq = fmaf(root[c], kLog2e, -z) + log2f(fabsf(gb));
       acc += gb * exp2f(TOP[static_cast<long long>(b) * Np + c] - z);
     }
-    LQ[chart_row(lengths[b], b, 0, B, lmax) * Np + c] = lq;
+    const long long row = chart_row(lengths[b], b, 0, B, lmax);
+    if constexpr (kHalfLQ) {  // fp16 outside weight with a per-chunk exponent
+      float mx = lq;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      int sc = mx == kNegInf ? 0 : static_cast<int>(floorf(mx)) - 14;
+      sc = sc < -126 ? -126 : sc;
+      static_cast<__half*>(LQv)[row * Np + c] = __float2half_rn(exp2f(lq - sc));
+      if ((threadIdx.x & 31) == 0) LQS[row * (Np / 32) + c / 32] = static_cast<float>(sc);
+    } else {
+      static_cast<float*>(LQv)[row * Np + c] = lq;
+    }
   }
   if (c < N) droot[c] = acc;
 }
@@ -558,7 +571,8 @@ __global__ void k_seed_bwd(const float* __restrict__ root, const float* __restri
 struct GatherArgs {
   const void* A;  // CT*
   const void* Bc; // CT*
-  const float* LQ;
+  const void* LQ;   // fp32 LQ^ (fp32 chart) or fp16 scaled |q| (half chart)
+  const float* LQS; // half chart: per 32-column exponents of LQ
   const double* X;
   void* G;  // T*, row stride 2*Np
   long long g_lo;
@@ -609,8 +623,11 @@ __global__ void __launch_bounds__(288) k_gather_bwd_bulk(GatherArgs a, int stage
   const int n_all = n_left + i;
   GatherTerm* gterms = reinterpret_cast<GatherTerm*>(dsm);
   const int sbytes = cpc * static_cast<int>(sizeof(CT));
+  // parent chunk: fp32 LQ^, or fp16 |q| followed by its cpc/32 exponents
+  const int qbytes = kHalf ? cpc * 2 : cpc * 4;
+  const int sxbytes = kHalf ? cpc / 8 : 0;
   BulkRing ring = carve_ring(dsm + align128(sizeof(GatherTerm) * a.lmax), stages, sbytes,
-                             cpc * 4);
+                             qbytes + sxbytes);
   const double xm = a.X[row] - (kHalf ? kChartScale : 0);
   for (int t = threadIdx.x; t < n_all; t += nthr) {
     long long rs, rp;
@@ -642,14 +659,19 @@ __global__ void __launch_bounds__(288) k_gather_bwd_bulk(GatherArgs a, int stage
         uint8_t* dst = ring.buf + static_cast<size_t>(s) * ring.stage_bytes;
         const CT* sib = t < n_left ? Bch : Ach;
         bulk_g2s(dst, sib + gterms[t].rs * a.Np + chunk0, sbytes, &ring.full[s]);
-        bulk_g2s(dst + ring.off1, a.LQ + gterms[t].rp * a.Np + chunk0, cpc * 4u, &ring.full[s]);
+        if constexpr (kHalf) {
+          bulk_g2s(dst + ring.off1,
+                   static_cast<const __half*>(a.LQ) + gterms[t].rp * a.Np + chunk0, qbytes,
+                   &ring.full[s]);
+          bulk_g2s(dst + ring.off1 + qbytes, a.LQS + gterms[t].rp * (a.Np / 32) + chunk0 / 32,
+                   sxbytes, &ring.full[s]);
+        } else {
+          bulk_g2s(dst + ring.off1, static_cast<const float*>(a.LQ) + gterms[t].rp * a.Np + chunk0,
+                   qbytes, &ring.full[s]);
+        }
       }
     }
   } else {
-    auto term = [](float x, float q, float d) {
-      if constexpr (kHalf) return x * ex2(q + d);
-      else return ex2(x + q + d);
-    };
     for (int t = 0; t < n_all; ++t) {
       const int s = t % stages;
       const uint32_t ph = (t / stages) & 1;
@@ -657,23 +679,45 @@ __global__ void __launch_bounds__(288) k_gather_bwd_bulk(GatherArgs a, int stage
       const float d = gterms[t].d;
       const uint8_t* stg = ring.buf + static_cast<size_t>(s) * ring.stage_bytes;
       const CT* src = reinterpret_cast<const CT*>(stg) + ci * 4;
-      const float* srq = reinterpret_cast<const float*>(stg + ring.off1) + ci * 4;
+      float* acc = t < n_left ? gl : gr;
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         const float4 x = chart4<CT>(src + v * ncons * 4);
-        const float4 q = *reinterpret_cast<const float4*>(srq + v * ncons * 4);
-        if (t < n_left) {
-          gl[4 * v + 0] += term(x.x, q.x, d);
-          gl[4 * v + 1] += term(x.y, q.y, d);
-          gl[4 * v + 2] += term(x.z, q.z, d);
-          gl[4 * v + 3] += term(x.w, q.w, d);
+        if constexpr (kHalf) {
+          // term = sib * q * 2^(d + s_chunk): one EX2 per 4 columns
+          const __half* qh = reinterpret_cast<const __half*>(stg + ring.off1);
+          const float* sx = reinterpret_cast<const float*>(stg + ring.off1 + qbytes);
+          const int cl = ci * 4 + v * ncons * 4;  // column within the CTA chunk
+          const float4 q = chart4<__half>(qh + cl);
+          const float f = ex2(d + sx[cl >> 5]);
+          if (t < n_left) {
+            gl[4 * v + 0] = fmaf(x.x * q.x, f, gl[4 * v + 0]);
+            gl[4 * v + 1] = fmaf(x.y * q.y, f, gl[4 * v + 1]);
+            gl[4 * v + 2] = fmaf(x.z * q.z, f, gl[4 * v + 2]);
+            gl[4 * v + 3] = fmaf(x.w * q.w, f, gl[4 * v + 3]);
+          } else {
+            gr[4 * v + 0] = fmaf(x.x * q.x, f, gr[4 * v + 0]);
+            gr[4 * v + 1] = fmaf(x.y * q.y, f, gr[4 * v + 1]);
+            gr[4 * v + 2] = fmaf(x.z * q.z, f, gr[4 * v + 2]);
+            gr[4 * v + 3] = fmaf(x.w * q.w, f, gr[4 * v + 3]);
+          }
         } else {
-          gr[4 * v + 0] += term(x.x, q.x, d);
-          gr[4 * v + 1] += term(x.y, q.y, d);
-          gr[4 * v + 2] += term(x.z, q.z, d);
-          gr[4 * v + 3] += term(x.w, q.w, d);
+          const float* srq = reinterpret_cast<const float*>(stg + ring.off1) + ci * 4;
+          const float4 q = *reinterpret_cast<const float4*>(srq + v * ncons * 4);
+          if (t < n_left) {
+            gl[4 * v + 0] += ex2(x.x + q.x + d);
+            gl[4 * v + 1] += ex2(x.y + q.y + d);
+            gl[4 * v + 2] += ex2(x.z + q.z + d);
+            gl[4 * v + 3] += ex2(x.w + q.w + d);
+          } else {
+            gr[4 * v + 0] += ex2(x.x + q.x + d);
+            gr[4 * v + 1] += ex2(x.y + q.y + d);
+            gr[4 * v + 2] += ex2(x.z + q.z + d);
+            gr[4 * v + 3] += ex2(x.w + q.w + d);
+          }
         }
       }
+      (void)acc;
       __syncwarp();
       if (lane == 0) mbar_arrive(&ring.empty[s]);
     }
@@ -698,9 +742,11 @@ __global__ void __launch_bounds__(288) k_gather_bwd_bulk(GatherArgs a, int stage
 }
 
 // Span marginals mu_sym[w][i, A] = go / |g| = 2^(LQ^ + O^ - log2|g|)  (inside.py:425-430)
-__global__ void k_marginals(const float* __restrict__ LQ, const float* __restrict__ O,
-                            const float* __restrict__ g, const int* __restrict__ lengths,
-                            float* __restrict__ mu, int B, int lmax, int Np, int N) {
+template <bool kHalfLQ>
+__global__ void k_marginals(const void* __restrict__ LQv, const float* __restrict__ LQS,
+                            const float* __restrict__ O, const float* __restrict__ g,
+                            const int* __restrict__ lengths, float* __restrict__ mu, int B,
+                            int lmax, int Np, int N) {
   const long long row = rowbase(2, B, lmax) + blockIdx.x;  // rows of widths >= 2
   int w = 2;
   while (w < lmax && row >= rowbase(w + 1, B, lmax)) ++w;
@@ -711,7 +757,14 @@ __global__ void k_marginals(const float* __restrict__ LQ, const float* __restric
   const float lg = ok ? log2f(fabsf(g[b])) : 0.f;
   for (int c = threadIdx.x; c < N; c += blockDim.x) {
     float v = 0.f;
-    if (ok) v = exp2f(LQ[row * Np + c] + O[row * Np + c] - lg);
+    if (ok) {
+      if constexpr (kHalfLQ) {
+        const float q = __half2float(static_cast<const __half*>(LQv)[row * Np + c]);
+        v = q * exp2f(LQS[row * (Np / 32) + c / 32] + O[row * Np + c] - lg);
+      } else {
+        v = exp2f(static_cast<const float*>(LQv)[row * Np + c] + O[row * Np + c] - lg);
+      }
+    }
     mu[(row - rowbase(2, B, lmax)) * N + c] = v;
   }
 }

@@ -254,6 +254,20 @@ __device__ __forceinline__ float lg2(float x) {  // log2 x, MUFU.LG2 (0 -> -inf)
   return y;
 }
 
+// Outside weights in the fp16 (half-chart) layout: per 32-column chunk a
+// power-of-two exponent s with max|q| * 2^-s in [2^14, 2^15): 11 significant
+// bits down to 2^-24 of the chunk maximum.  Returns s for chunk maximum m.
+// s is clamped to [-126, 113] so that 2^-s is a normal float (chunks whose
+// maximum is below 2^-112 keep fewer bits; they carry no weight anyway).
+__device__ __forceinline__ int lq_chunk_exp(float m) {
+  if (!(m > 0.f) || !(m < __builtin_huge_valf())) return 0;
+  const int e = static_cast<int>((__float_as_uint(m) >> 23) & 0xffu) - 127;  // floor(log2 m)
+  return e - 14 < -126 ? -126 : e - 14;
+}
+__device__ __forceinline__ float exp2_int(int s) {  // 2^s for s in [-126, 127]
+  return __uint_as_float(static_cast<uint32_t>(s + 127) << 23);
+}
+
 __device__ __forceinline__ float4 ldg_nc_f4(const float* p) {
   float4 r;
   asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];"
