@@ -445,6 +445,7 @@ int dispatch_v(int v, F&& f) {
     case 1: return f(VC<1>{});
     case 2: return f(VC<2>{});
     case 4: return f(VC<4>{});
+    case 8: return f(VC<8>{});
   }
   return set_err(FI_ERR_UNSUPPORTED, "columns per thread %d", v);
 }
@@ -535,16 +536,48 @@ int forward_impl(const Plan& p, const float* L, const float* R, const float* roo
     const dim3 grid(dc.clusters, p.B * n_w);
     {
       ProfScope prof(FI_PROF_SPLIT, st);
-      const int stages = dc.stages;
-      const size_t smem = align128(sizeof(SplitTerm) * (w - 1)) +
-                          static_cast<size_t>(stages) * (2 * dc.cols_per_cta * sizeof(CT) + 16);
-      const dim3 block(32 + dc.threads);
-      FI_TRY(dispatch_v(dc.v, [&](auto vc) {
-        constexpr int V = decltype(vc)::value;
-        FI_TRY(set_smem(k_split_fwd_bulk<T, CT, V>, smem));
-        return launch_cluster(k_split_fwd_bulk<T, CT, V>, dc.clusters, grid, block, smem, st, sa,
-                              stages);
-      }));
+      static const int pers = env_int("FI_SPLIT_PERS", 1);
+      if (pers && p.Np <= 8192) {
+        // persistent one-CTA-per-row kernel: ~72 KB of ring per CTA (2-3 CTAs/SM)
+        const int cons = p.Np / 4 < 256 ? p.Np / 4 : 256;
+        const int V = p.Np / (4 * cons);
+        const size_t stage_bytes = 2ull * p.Np * sizeof(CT);
+        static const int env_st = env_int("FI_PSTAGES", 0);
+        int stages = env_st ? env_st : static_cast<int>(73728 / stage_bytes);
+        stages = stages < 2 ? 2 : (stages > 8 ? 8 : stages);
+        static const int nprod = env_int("FI_NPROD", 4);
+        const size_t smem = static_cast<size_t>(stages) * (stage_bytes + 16 + sizeof(StageHdr)) +
+                            8ull * p.l + 64;
+        const int nrows = p.B * n_w;
+        FI_TRY(dispatch_v(V, [&](auto vc) {
+          constexpr int VV = decltype(vc)::value;
+          auto kern = k_split_fwd_pers<T, CT, VV>;
+          FI_TRY(set_smem(kern, smem));
+          int occ = 0;
+          FI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 + cons, smem));
+          occ = occ < 1 ? 1 : occ;
+          const int grid = nrows < occ * num_sms() ? nrows : occ * num_sms();
+          kern<<<grid, 32 + cons, smem, st>>>(sa, stages, nprod);
+          ++g_launches;
+          FI_CUDA(cudaGetLastError());
+          return FI_OK;
+        }));
+      } else {
+        const int stages = dc.stages;
+        const size_t smem = align128(sizeof(SplitTerm) * (w - 1)) +
+                            static_cast<size_t>(stages) * (2 * dc.cols_per_cta * sizeof(CT) + 16);
+        const dim3 block(32 + dc.threads);
+        FI_TRY(dispatch_v(dc.v, [&](auto vc) {
+          constexpr int V = decltype(vc)::value;
+          if constexpr (V > 4) {
+            return set_err(FI_ERR_UNSUPPORTED, "split decomposition V=%d", V);
+          } else {
+            FI_TRY(set_smem(k_split_fwd_bulk<T, CT, V>, smem));
+            return launch_cluster(k_split_fwd_bulk<T, CT, V>, dc.clusters, grid, block, smem, st,
+                                  sa, stages);
+          }
+        }));
+      }
     }
     if (w < p.l) {
       ep.M = p.B * n_w;
@@ -618,9 +651,13 @@ int backward_impl(const Plan& p, const float* L, const float* R, const float* ro
                           static_cast<size_t>(stages) * (dc.cols_per_cta * sizeof(CT) + qb + 16);
       FI_TRY(dispatch_v(dc.v, [&](auto vc) {
         constexpr int V = decltype(vc)::value;
-        FI_TRY(set_smem(k_gather_bwd_bulk<T, CT, V>, smem));
-        k_gather_bwd_bulk<T, CT, V><<<grid, 32 + dc.threads, smem, st>>>(ga, stages);
-        return FI_OK;
+        if constexpr (V > 4) {
+          return set_err(FI_ERR_UNSUPPORTED, "gather decomposition V=%d", V);
+        } else {
+          FI_TRY(set_smem(k_gather_bwd_bulk<T, CT, V>, smem));
+          k_gather_bwd_bulk<T, CT, V><<<grid, 32 + dc.threads, smem, st>>>(ga, stages);
+          return FI_OK;
+        }
       }));
     }
     ++g_launches;

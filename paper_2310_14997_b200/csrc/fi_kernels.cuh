@@ -511,6 +511,248 @@ __global__ void __launch_bounds__(288) k_split_fwd_bulk(SplitArgs a, int stages)
 }
 
 // ---------------------------------------------------------------------------
+// Persistent split contraction (one CTA per span row, C = 1).  The CTA loops
+// over rows blockIdx.x, blockIdx.x + gridDim.x, ... of width w.  Its producer
+// warp computes each row's term table and fixed shift D (all 32 lanes), then
+// `nprod` lanes issue the row's 2 (w-1) row-chunk copies into the ring, each
+// stage carrying a small header (the term's weight, and D on a row's first
+// term); the consumer warps accumulate, and at a row's last term reduce the
+// row max, write E / X / logZ -- while the producer is already streaming the
+// next row.  So the ring never drains between rows (the per-row prologue /
+// epilogue latency of one-CTA-per-row launches is hidden), several lanes keep
+// more bulk copies in flight per CTA than one issuing thread can, and the
+// grid is sized to the SMs instead of leaving a partial last wave.  A row
+// outside its sentence takes one header-only stage (dead = 1).
+// ---------------------------------------------------------------------------
+struct StageHdr {
+  float scal;  // term weight: d (fp32 chart) or c = 2^(d - 2 kChartScale) (half chart)
+  int dead;    // 1: the row is outside its sentence (no copies in this stage)
+  double D;    // the row's fixed shift (valid on the row's first stage)
+};
+
+__device__ __forceinline__ void cons_bar(int nthreads) {  // consumer warps only (barrier 1)
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+template <bool kMax>
+__device__ __forceinline__ float cons_reduce(float v, float* red, int ncons) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    float t = __shfl_xor_sync(0xffffffffu, v, o);
+    v = kMax ? fmaxf(v, t) : v + t;
+  }
+  const int cw = (threadIdx.x >> 5) - 1, lane = threadIdx.x & 31;  // consumer warp index
+  cons_bar(ncons);
+  if (lane == 0) red[cw] = v;
+  cons_bar(ncons);
+  float u = kMax ? kNegInf : 0.f;
+  for (int k = 0; k < (ncons >> 5); ++k) u = kMax ? fmaxf(u, red[k]) : u + red[k];
+  cons_bar(ncons);  // red is reused by the next reduction
+  return u;
+}
+
+template <typename T, typename CT, int V>
+__global__ void __launch_bounds__(288, 3) k_split_fwd_pers(SplitArgs a, int stages, int nprod) {
+  constexpr bool kHalf = sizeof(CT) == 2;
+  nprod = nprod < 1 ? 1 : (nprod > stages ? stages : (nprod > 32 ? 32 : nprod));
+  extern __shared__ __align__(128) uint8_t dsm[];
+  __shared__ float red[32];
+  const int w = a.w;
+  const int nsplit = w - 1;
+  const int n_w = a.lmax - w + 1;
+  const int nrows = a.B * n_w;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ncons = blockDim.x - 32;
+  const int cpc = a.Np;  // one CTA per row
+  const int cbytes = cpc * static_cast<int>(sizeof(CT));
+  const CT* Ach = static_cast<const CT*>(a.A);
+  const CT* Bch = static_cast<const CT*>(a.Bc);
+  T* E = reinterpret_cast<T*>(a.E);
+  uint8_t* ring = dsm;
+  const int stage_bytes = 2 * cbytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + static_cast<size_t>(stages) * stage_bytes);
+  uint64_t* empty = full + stages;
+  StageHdr* hdr = reinterpret_cast<StageHdr*>(empty + stages);
+  double* ptab = reinterpret_cast<double*>(hdr + stages);  // producer-private: xs per term
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], ncons >> 5);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const float lnn = a.wsum[0] > 0.f ? log2f(a.wsum[0]) : 0.f;
+  const float rnn = a.wsum[1] > 0.f ? log2f(a.wsum[1]) : 0.f;
+  const float lnp = a.wsum[2] > 0.f ? log2f(a.wsum[2]) : 0.f;
+  const float rnp = a.wsum[3] > 0.f ? log2f(a.wsum[3]) : 0.f;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    long long g0 = 0;  // stages used before this row (identical count in the consumers)
+    for (int local = blockIdx.x; local < nrows; local += gridDim.x) {
+      const int b = local / n_w, i = local % n_w;
+      const bool dead = i + w > a.lengths[b];
+      double ub = -1.0e300;
+      if (!dead) {
+        for (int t = lane; t < nsplit; t += 32) {
+          const int m = t + 1;
+          const double xs = a.X[chart_row(m, b, i, a.B, a.lmax)] +
+                            a.X[chart_row(w - m, b, i + m, a.B, a.lmax)];
+          ptab[t] = xs;
+          ub = fmax(ub, xs + (m == 1 ? lnp : lnn) + (w - m == 1 ? rnp : rnn));
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ub = fmax(ub, __shfl_xor_sync(0xffffffffu, ub, o));
+      __syncwarp();
+      const double D = ub;
+      if (dead) {
+        if (lane == 0) {
+          const int s = static_cast<int>(g0 % stages);
+          mbar_wait(&empty[s], static_cast<uint32_t>((g0 / stages) & 1) ^ 1);
+          hdr[s].dead = 1;
+          hdr[s].D = D;
+          mbar_arrive(&full[s]);
+        }
+        g0 += 1;
+      } else {
+        // lanes issue in lockstep batches of nprod consecutive terms (nprod <=
+        // stages): a parity wait on empty[] is then never more than one phase
+        // behind, so no lane can reuse a stage whose previous round is unread
+        for (int t0 = 0; t0 < nsplit; t0 += nprod) {
+          const int t = t0 + lane;
+          if (lane < nprod && t < nsplit) {
+            const long long g = g0 + t;
+            const int s = static_cast<int>(g % stages);
+            mbar_wait(&empty[s], static_cast<uint32_t>((g / stages) & 1) ^ 1);
+            const int m = t + 1;
+            const float d = static_cast<float>(ptab[t] - D);
+            hdr[s].scal = kHalf ? exp2f(d - 2.f * kChartScale) : d;
+            hdr[s].dead = 0;
+            hdr[s].D = D;
+            mbar_expect_tx(&full[s], static_cast<uint32_t>(stage_bytes));
+            uint8_t* dst = ring + static_cast<size_t>(s) * stage_bytes;
+            bulk_g2s(dst, Ach + chart_row(m, b, i, a.B, a.lmax) * a.Np, cbytes, &full[s]);
+            bulk_g2s(dst + cbytes, Bch + chart_row(w - m, b, i + m, a.B, a.lmax) * a.Np, cbytes,
+                     &full[s]);
+          }
+          __syncwarp();
+        }
+        g0 += nsplit;
+      }
+      __syncwarp();  // the term table is rewritten for the next row
+    }
+    return;
+  }
+  // -------------------------------------------------------------- consumers
+  const int ci = threadIdx.x - 32;
+  const int col0 = ci * 4;
+  long long g0 = 0;
+  for (int local = blockIdx.x; local < nrows; local += gridDim.x) {
+    const int b = local / n_w, i = local % n_w;
+    const int len = a.lengths[b];
+    const long long row = rowbase(w, a.B, a.lmax) + local;
+    // first stage: D, or the dead marker
+    int s = static_cast<int>(g0 % stages);
+    mbar_wait(&full[s], static_cast<uint32_t>((g0 / stages) & 1));
+    const double D = hdr[s].D;
+    if (hdr[s].dead) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const int c = col0 + v * ncons * 4;
+        if (a.O) *reinterpret_cast<float4*>(a.O + row * a.Np + c) =
+            make_float4(kNegInf, kNegInf, kNegInf, kNegInf);
+        if (E) store4s<T>(E + row * a.Np + c, a.e_lo, 0.f, 0.f, 0.f, 0.f);
+      }
+      if (ci == 0) a.X[row] = D;
+      g0 += 1;
+      continue;
+    }
+    float S[4 * V];
+#pragma unroll
+    for (int k = 0; k < 4 * V; ++k) S[k] = 0.f;
+    for (int t = 0; t < nsplit; ++t) {
+      const long long g = g0 + t;
+      s = static_cast<int>(g % stages);
+      if (t) mbar_wait(&full[s], static_cast<uint32_t>((g / stages) & 1));
+      const float dl = hdr[s].scal;
+      const CT* src = reinterpret_cast<const CT*>(ring + static_cast<size_t>(s) * stage_bytes) + col0;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const float4 x = chart4<CT>(src + v * ncons * 4);
+        const float4 y = chart4<CT>(src + cpc + v * ncons * 4);
+        if constexpr (kHalf) {
+          S[4 * v + 0] = fmaf(x.x * dl, y.x, S[4 * v + 0]);
+          S[4 * v + 1] = fmaf(x.y * dl, y.y, S[4 * v + 1]);
+          S[4 * v + 2] = fmaf(x.z * dl, y.z, S[4 * v + 2]);
+          S[4 * v + 3] = fmaf(x.w * dl, y.w, S[4 * v + 3]);
+        } else {
+          S[4 * v + 0] += ex2(x.x + y.x + dl);
+          S[4 * v + 1] += ex2(x.y + y.y + dl);
+          S[4 * v + 2] += ex2(x.z + y.z + dl);
+          S[4 * v + 3] += ex2(x.w + y.w + dl);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    g0 += nsplit;
+    float o[4 * V];  // o - D
+    float mx = kNegInf;
+#pragma unroll
+    for (int k = 0; k < 4 * V; ++k) {
+      o[k] = lg2(S[k]);  // S = 0 -> -inf
+      mx = fmaxf(mx, o[k]);
+    }
+    mx = cons_reduce<true>(mx, red, ncons);
+    const float xs = (mx == kNegInf) ? 0.f : mx;  // inside.py:324-326
+#pragma unroll
+    for (int k = 0; k < 4 * V; ++k) o[k] -= xs;  // O^ = o - x†  (<= 0)
+    if (a.O) {
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        *reinterpret_cast<float4*>(a.O + row * a.Np + col0 + v * ncons * 4) =
+            make_float4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+    }
+    if (E) {
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        store4s<T>(E + row * a.Np + col0 + v * ncons * 4, a.e_lo, ex2(o[4 * v]),
+                   ex2(o[4 * v + 1]), ex2(o[4 * v + 2]), ex2(o[4 * v + 3]));
+    }
+    const double xrow = D + static_cast<double>(xs);
+    if (ci == 0) a.X[row] = xrow;
+    if (i == 0 && w == len) {  // top span: logZ = LSE_A(root[A] + o[A])  (inside.py:124-129)
+      float sc[4 * V];
+      float smx = kNegInf;
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int c = col0 + v * ncons * 4 + k;
+          sc[4 * v + k] = c < a.N ? fmaf(a.root[c], kLog2e, o[4 * v + k]) : kNegInf;
+          a.TOP[static_cast<long long>(b) * a.Np + c] = sc[4 * v + k];
+          smx = fmaxf(smx, sc[4 * v + k]);
+        }
+      smx = cons_reduce<true>(smx, red, ncons);
+      float sum = 0.f;
+      if (smx != kNegInf) {
+#pragma unroll
+        for (int k = 0; k < 4 * V; ++k) sum += exp2f(sc[k] - smx);
+      }
+      sum = cons_reduce<false>(sum, red, ncons);
+      if (ci == 0) {
+        const float z = smx == kNegInf ? kNegInf : smx + log2f(sum);  // log2 Z - x†
+        a.TOPZ[b] = z;
+        a.logZ[b] = z == kNegInf ? kNegInf : static_cast<float>((xrow + z) * kLn2d);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Backward seed (inside.py:400-404): the root posterior
 //   post[A] = exp(root[A] + o[len][0, A] - logZ)
 // seeds the outside pass at each sentence's top span as
