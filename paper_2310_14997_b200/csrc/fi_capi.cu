@@ -655,7 +655,8 @@ int backward_impl(const Plan& p, const float* L, const float* R, const float* ro
           return set_err(FI_ERR_UNSUPPORTED, "gather decomposition V=%d", V);
         } else {
           FI_TRY(set_smem(k_gather_bwd_bulk<T, CT, V>, smem));
-          k_gather_bwd_bulk<T, CT, V><<<grid, 32 + dc.threads, smem, st>>>(ga, stages);
+          static const int nprod = env_int("FI_GNPROD", 4);
+          k_gather_bwd_bulk<T, CT, V><<<grid, 32 + dc.threads, smem, st>>>(ga, stages, nprod);
           return FI_OK;
         }
       }));

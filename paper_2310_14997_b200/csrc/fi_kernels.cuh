@@ -830,8 +830,9 @@ struct GatherTerm {
 };
 
 template <typename T, typename CT, int V>
-__global__ void __launch_bounds__(288) k_gather_bwd_bulk(GatherArgs a, int stages) {
+__global__ void __launch_bounds__(288) k_gather_bwd_bulk(GatherArgs a, int stages, int nprod) {
   constexpr bool kHalf = sizeof(CT) == 2;
+  nprod = nprod < 1 ? 1 : (nprod > stages ? stages : (nprod > 32 ? 32 : nprod));
   extern __shared__ __align__(128) uint8_t dsm[];
   const int m = a.m;
   const int n_m = a.lmax - m + 1;
@@ -892,8 +893,13 @@ __global__ void __launch_bounds__(288) k_gather_bwd_bulk(GatherArgs a, int stage
 #pragma unroll
   for (int k = 0; k < 4 * V; ++k) gl[k] = gr[k] = 0.f;
   if (warp == 0) {
-    if (lane == 0) {
-      for (int t = 0; t < n_all; ++t) {
+    // `nprod` lanes issue in lockstep batches of consecutive terms (nprod <=
+    // stages, so a parity wait is never more than one phase behind): a CTA
+    // keeps more bulk copies in flight than one issuing thread can
+    const unsigned imask = (1u << nprod) - 1u;
+    for (int t0 = 0; t0 < n_all && lane < nprod; t0 += nprod) {
+      const int t = t0 + lane;
+      if (t < n_all) {
         const int s = t % stages;
         const uint32_t ph = (t / stages) & 1;
         mbar_wait(&ring.empty[s], ph ^ 1);
@@ -912,6 +918,7 @@ __global__ void __launch_bounds__(288) k_gather_bwd_bulk(GatherArgs a, int stage
                    qbytes, &ring.full[s]);
         }
       }
+      __syncwarp(imask);
     }
   } else {
     for (int t = 0; t < n_all; ++t) {
