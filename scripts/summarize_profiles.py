@@ -99,12 +99,13 @@ def classify(k: dict) -> str | None:
         return "gather_bwd"
     m = re.match(r"k_gemm<[^,]+, \d+, \d, \d, (\d)", name)
     if m:
-        return {"0": "gemm_fwd", "1": "gemm_dgrad", "2": "gemm_dgrad", "3": "gemm_wgrad"}.get(m.group(1))
+        return {"0": "gemm_fwd", "5": "gemm_fwd", "1": "gemm_dgrad", "6": "gemm_dgrad",
+                "2": "gemm_dgrad", "3": "gemm_wgrad"}.get(m.group(1))
     return None
 
 
 def traffic(kernels: list[dict], n: int, batch: int, length: int, esz: int,
-            chart_esz: int) -> dict:
+            chart_esz: int, widths: dict) -> dict:
     """Per kernel class: DRAM bytes of the captured launch next to the
     compulsory (algorithmic) bytes of that same launch (bench.py formulas)."""
     import sys
@@ -119,7 +120,8 @@ def traffic(kernels: list[dict], n: int, batch: int, length: int, esz: int,
         d = {"dram_bytes": k["dram_read"] + k["dram_write"], "time_ms": k["time_ms"],
              "launch": f"{k['file']} grid {k['grid']}"}
         if cls in ("split_fwd", "gather_bwd"):
-            width = length - gy // batch + 1
+            # the captured launch's width (persistent grids do not encode it)
+            width = widths.get(cls) or length - gy // batch + 1
             fn = bench.split_launch_bytes if cls == "split_fwd" else bench.gather_launch_bytes
             d["width"] = width
             d["algorithmic_bytes"] = fn(n, batch, length, width, esz, chart_esz)
@@ -137,6 +139,8 @@ def main():
     ap.add_argument("--length", type=int, default=40)
     ap.add_argument("--esz", type=int, default=2, help="GEMM operand bytes (bf16 2, tf32 4)")
     ap.add_argument("--chart-esz", type=int, default=2, help="a/b chart bytes (fp16 2, fp32 4)")
+    ap.add_argument("--split-width", type=int, default=20, help="width of the captured split launch")
+    ap.add_argument("--gather-width", type=int, default=20, help="child width of the captured gather")
     ap.add_argument("--launches")
     ap.add_argument("--reps", nargs="*", default=[])
     args = ap.parse_args()
@@ -153,7 +157,8 @@ def main():
         (prof / f"{args.tag}_ncu_kernels.json").write_text(json.dumps(kernels, indent=1))
         for k in kernels:
             print(json.dumps(k))
-        tr = traffic(kernels, args.n, args.batch, args.length, args.esz, args.chart_esz)
+        tr = traffic(kernels, args.n, args.batch, args.length, args.esz, args.chart_esz,
+                     {"split_fwd": args.split_width, "gather_bwd": args.gather_width})
         (prof / "ncu_traffic.json").write_text(json.dumps(tr, indent=1))
         print(json.dumps(tr, indent=1))
 
