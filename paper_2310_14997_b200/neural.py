@@ -1,0 +1,286 @@
+"""Grammar parameterisations and the batched training step on the GPU
+(the producer of the op's L, R, root, unary).
+
+Mirrors /root/reference/pkg/src/flashpcfg/neuralparam.py and the per-batch
+step of train.py, with the same names and semantics:
+
+* ``init_params``        neuralparam.py:86-102  same RNG draw order as the
+                         reference (Xavier-normal weights, scaled-normal
+                         embeddings, zero biases): identical tensors per seed
+* ``grammar_tables``     neuralparam.py:149-208 (``_Forward``): root from
+                         f1(start) . u_nt, left/right from f3(parent) .
+                         f2/f4(child), emission from f5(preterminal) . u_voc,
+                         each row log-softmaxed; ``tied`` reuses the left head
+* backward               neuralparam.py:242-320 (``backward_params``) is torch
+                         autograd through the same graph; gradients are checked
+                         against the reference's manual backward in the tests
+* ``init_direct`` / direct tables  neuralparam.py:359-389
+* ``clip_grads_``        train.py:133-142 (global norm)
+* ``adam_step``          neuralparam.py:337-354 (bias-corrected Adam)
+* ``TrainStep``          train.py:201-227: tables -> unary gather -> inside op
+                         (fwd+bwd on the sm_100a engine) -> loss = -mean log Z
+                         -> backward -> (data-parallel all-reduce of the
+                         PARAMETER gradients) -> clip -> Adam
+
+The parameterisation's dense products (N x d by d x (N+P) score tables) are
+plain library GEMMs (cuBLAS through torch.matmul); the inside algorithm runs
+on this repo's engine.  With data parallelism the single collective is an
+all-reduce of the parameter gradients (~9.2 M + 512 V floats at N = 4096,
+d = 512), not of dL and dR (67 M floats).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+import torch.distributed as dist
+import torch.nn.functional as F
+
+from .dp import allreduce_grads
+from .grammar import GrammarDims
+from .ops import inside
+
+
+class ParamError(Exception):
+    """Invalid parameters or a non-finite value (neuralparam.py:24-25)."""
+
+
+def tensor_shapes(dims: GrammarDims, d: int) -> dict[str, tuple[int, ...]]:
+    """Names and shapes of the embedding parameterisation (neuralparam.py:70-83)."""
+    shapes: dict[str, tuple[int, ...]] = {
+        "w_sym": (1 + dims.n_nt + dims.n_pt, d),  # start symbol, nonterminals, preterminals
+        "u_nt": (dims.n_nt, d),
+        "u_voc": (dims.vocab_size, d),
+    }
+    for blk in ("f1", "f5"):  # two residual two-layer blocks each
+        for k in range(1, 5):
+            shapes[f"{blk}.w{k}"] = (d, d)
+        for k in range(1, 5):
+            shapes[f"{blk}.b{k}"] = (d,)
+    for blk in ("f2", "f3", "f4"):  # single relu layer with a residual connection
+        shapes[f"{blk}.w"] = (d, d)
+        shapes[f"{blk}.b"] = (d,)
+    return shapes
+
+
+@dataclass
+class EmbeddingParams:
+    """Named parameter tensors (neuralparam.py:42-67), here torch tensors."""
+
+    dims: GrammarDims
+    d: int
+    tensors: dict[str, torch.Tensor]
+
+
+def init_params(dims: GrammarDims, d: int = 512, seed: int = 0, device=None,
+                dtype=torch.float32) -> EmbeddingParams:
+    """Fresh parameters drawn exactly as the reference's init_params."""
+    if d < 2:
+        raise ParamError(f"embedding dimension must be at least 2, got {d}")
+    rng = np.random.default_rng(seed)
+    out: dict[str, torch.Tensor] = {}
+    for name, shape in tensor_shapes(dims, d).items():
+        if name in ("w_sym", "u_nt", "u_voc"):
+            a = rng.standard_normal(shape) / math.sqrt(d)
+        elif len(shape) == 2:
+            n_out, n_in = shape
+            a = rng.normal(0.0, math.sqrt(2.0 / (n_in + n_out)), size=shape)
+        else:
+            a = np.zeros(shape)
+        out[name] = torch.tensor(a, dtype=dtype, device=device)
+    return EmbeddingParams(dims, d, out)
+
+
+def _residual_relu(x, w, b):
+    return torch.relu(x @ w.T + b) + x
+
+
+def _two_layer(x, w1, b1, w2, b2):
+    return x + torch.relu(x @ w1.T + b1) @ w2.T + b2
+
+
+def grammar_tables(p: EmbeddingParams, tied: bool = False):
+    """(log_root (N,), log_left (N, N+P), log_right, log_emit (P, V)), differentiable."""
+    t = p.tensors
+    n = p.dims.n_nt
+    x_start = t["w_sym"][0:1]
+    x_nt = t["w_sym"][1:1 + n]
+    x_child = t["w_sym"][1:]
+    x_pt = t["w_sym"][1 + n:]
+    f1 = _two_layer(_two_layer(x_start, t["f1.w1"], t["f1.b1"], t["f1.w2"], t["f1.b2"]),
+                    t["f1.w3"], t["f1.b3"], t["f1.w4"], t["f1.b4"])
+    f3 = _residual_relu(x_nt, t["f3.w"], t["f3.b"])
+    f2 = _residual_relu(x_child, t["f2.w"], t["f2.b"])
+    f5 = _two_layer(_two_layer(x_pt, t["f5.w1"], t["f5.b1"], t["f5.w2"], t["f5.b2"]),
+                    t["f5.w3"], t["f5.b3"], t["f5.w4"], t["f5.b4"])
+    for name, a in (("f1", f1), ("f2", f2), ("f3", f3), ("f5", f5)):
+        if not torch.isfinite(a).all():
+            raise ParamError(f"non-finite activation in {name}")
+    log_root = F.log_softmax((f1 @ t["u_nt"].T)[0], dim=-1)
+    log_left = F.log_softmax(f3 @ f2.T, dim=-1)
+    if tied:
+        log_right = log_left
+    else:
+        f4 = _residual_relu(x_child, t["f4.w"], t["f4.b"])
+        if not torch.isfinite(f4).all():
+            raise ParamError("non-finite activation in f4")
+        log_right = F.log_softmax(f3 @ f4.T, dim=-1)
+    log_emit = F.log_softmax(f5 @ t["u_voc"].T, dim=-1)
+    return log_root, log_left, log_right, log_emit
+
+
+@dataclass
+class DirectLogits:
+    """Raw score tables softmaxed row-wise (neuralparam.py:359-375)."""
+
+    dims: GrammarDims
+    tensors: dict[str, torch.Tensor]
+
+
+def init_direct(dims: GrammarDims, seed: int = 0, scale: float = 0.5, device=None,
+                dtype=torch.float32) -> DirectLogits:
+    rng = np.random.default_rng(seed)
+    shapes = (("root", (dims.n_nt,)), ("left", (dims.n_nt, dims.n_sym)),
+              ("right", (dims.n_nt, dims.n_sym)), ("emit", (dims.n_pt, dims.vocab_size)))
+    return DirectLogits(dims, {k: torch.tensor(scale * rng.standard_normal(s), dtype=dtype,
+                                               device=device) for k, s in shapes})
+
+
+def direct_tables(p: DirectLogits, tied: bool = False):
+    t = p.tensors
+    log_left = F.log_softmax(t["left"], dim=-1)
+    log_right = log_left if tied else F.log_softmax(t["right"], dim=-1)
+    return (F.log_softmax(t["root"], dim=-1), log_left, log_right,
+            F.log_softmax(t["emit"], dim=-1))
+
+
+# --------------------------------------------------------------- optimiser
+@dataclass
+class AdamState:
+    """First / second moments and the step counter (neuralparam.py:325-334)."""
+
+    m: dict[str, torch.Tensor]
+    v: dict[str, torch.Tensor]
+    t: int = 0
+
+    @staticmethod
+    def zeros(tensors: dict[str, torch.Tensor]) -> "AdamState":
+        return AdamState({k: torch.zeros_like(x) for k, x in tensors.items()},
+                         {k: torch.zeros_like(x) for k, x in tensors.items()})
+
+
+def clip_grads_(grads: dict[str, torch.Tensor], max_norm: float) -> torch.Tensor:
+    """Scale all gradients so their joint norm is at most max_norm (train.py:133-142).
+    Returns the pre-clip norm (a device scalar: no host sync)."""
+    g = list(grads.values())
+    norm = torch.linalg.vector_norm(torch.stack([torch.linalg.vector_norm(x) for x in g]))
+    scale = torch.clamp(max_norm / norm, max=1.0)
+    torch._foreach_mul_(g, scale)
+    return norm
+
+
+def adam_step(tensors: dict[str, torch.Tensor], grads: dict[str, torch.Tensor],
+              state: AdamState, lr: float = 0.002, beta1: float = 0.75,
+              beta2: float = 0.999, eps: float = 1e-8, check_finite: bool = True) -> None:
+    """One bias-corrected Adam update in place (neuralparam.py:337-354):
+    x -= lr * (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps)."""
+    names = list(tensors)
+    if check_finite:
+        bad = [k for k in names if not torch.isfinite(grads[k]).all()]
+        if bad:
+            raise ParamError(f"non-finite gradient for {bad[0]}")
+    state.t += 1
+    c1 = 1.0 - beta1 ** state.t
+    c2 = 1.0 - beta2 ** state.t
+    xs = [tensors[k] for k in names]
+    gs = [grads[k] for k in names]
+    ms = [state.m[k] for k in names]
+    vs = [state.v[k] for k in names]
+    torch._foreach_mul_(ms, beta1)
+    torch._foreach_add_(ms, gs, alpha=1.0 - beta1)
+    torch._foreach_mul_(vs, beta2)
+    torch._foreach_addcmul_(vs, gs, gs, value=1.0 - beta2)
+    denom = torch._foreach_div(vs, c2)
+    torch._foreach_sqrt_(denom)
+    torch._foreach_add_(denom, eps)
+    step = torch._foreach_div(ms, denom)
+    torch._foreach_add_(xs, step, alpha=-lr / c1)
+
+
+# ------------------------------------------------------------ training step
+@dataclass
+class TrainConfig:
+    """The optimiser / model knobs of the reference TrainConfig (train.py:38-57)."""
+
+    parameterization: str = "neural"
+    d: int = 512
+    lr: float = 0.002
+    beta1: float = 0.75
+    beta2: float = 0.999
+    eps: float = 1e-8
+    clip: float = 5.0
+    tied: bool = False
+    gemm_dtype: str = "bf16"
+
+
+@dataclass
+class TrainStep:
+    """One optimisation step of train.py:201-227 on the GPU, batched.
+
+    ``step(tokens, lengths)`` takes a (B, lmax) int64 token tensor and
+    (B,) int32 lengths on the device; returns the mean per-sentence NLL
+    (a device scalar).  Under torch.distributed each rank passes its shard
+    of the batch; the parameter gradients are summed with ONE all-reduce
+    of a flat buffer and the loss is the global mean (every rank applies
+    the identical update)."""
+
+    params: EmbeddingParams | DirectLogits
+    config: TrainConfig = field(default_factory=TrainConfig)
+    state: AdamState | None = None
+
+    def __post_init__(self):
+        for x in self.params.tensors.values():
+            x.requires_grad_(True)
+        if self.state is None:
+            self.state = AdamState.zeros({k: v.detach() for k, v in self.params.tensors.items()})
+
+    def tables(self):
+        if isinstance(self.params, EmbeddingParams):
+            return grammar_tables(self.params, self.config.tied)
+        return direct_tables(self.params, self.config.tied)
+
+    def loss_and_grads(self, tokens: torch.Tensor, lengths: torch.Tensor,
+                       global_batch: int | None = None):
+        """Loss = -sum(log Z) / global_batch and its parameter gradients
+        (the train.py:208-224 chain, batched: tables -> unary gather ->
+        inside fwd+bwd on the engine -> autograd through the tables)."""
+        cfg = self.config
+        xs = list(self.params.tensors.values())
+        log_root, log_left, log_right, log_emit = self.tables()
+        unary = log_emit.T[tokens]                                 # inside.py:296-298
+        log_z = inside(log_left.contiguous(), log_right.contiguous(), log_root.contiguous(),
+                       unary.contiguous(), lengths, gemm_dtype=cfg.gemm_dtype)
+        nb = global_batch or tokens.shape[0]
+        loss = -log_z.sum() / nb                                   # train.py:218: -1/B
+        grads = torch.autograd.grad(loss, xs, allow_unused=True)  # tied: f4 unused
+        return loss, [torch.zeros_like(x) if g is None else g for x, g in zip(xs, grads)]
+
+    def step(self, tokens: torch.Tensor, lengths: torch.Tensor, global_batch: int | None = None,
+             group=None) -> torch.Tensor:
+        cfg = self.config
+        names = list(self.params.tensors)
+        xs = [self.params.tensors[k] for k in names]
+        loss, grads = self.loss_and_grads(tokens, lengths, global_batch)
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        if world > 1:  # one collective: the flat parameter-gradient bucket (+ the loss)
+            *grads, loss = allreduce_grads(list(grads) + [loss.detach().reshape(1)], group)
+            loss = loss[0]
+        gd = dict(zip(names, grads))
+        clip_grads_(gd, cfg.clip)
+        with torch.no_grad():
+            adam_step({k: x.data for k, x in zip(names, xs)}, gd, self.state, lr=cfg.lr,
+                      beta1=cfg.beta1, beta2=cfg.beta2, eps=cfg.eps, check_finite=False)
+        return loss.detach()
