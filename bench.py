@@ -260,6 +260,52 @@ def run_e2e(args, g, tokens, step, dev, batch, n, world, barrier):
                     "double-buffered across steps; wall clock over K steps"}
 
 
+def roofline_block(prof: dict, steps: int, n: int, batch: int, length: int, esz: int,
+                   chart_esz: int) -> dict:
+    """roofline{} of the dominant kernel class from per-class CUDA-event
+    times (_lib.profile_collect over `steps` steps) and the algorithmic work."""
+    peaks = measured_peaks()
+    work = algorithmic_work(n, n, batch, length, esz, store_o=False, chart_esz=chart_esz)
+    per_class = {}
+    for name, (tot_ms, cnt) in prof.items():
+        if cnt:
+            per_class[name] = {"ms_per_step": tot_ms / steps, "launches_per_step": cnt // steps}
+    dominant = max((k for k in per_class if k in work), key=lambda k: per_class[k]["ms_per_step"])
+    bound, amount = work[dominant]
+    k_ms = per_class[dominant]["ms_per_step"]
+    if bound == "hbm":
+        achieved = amount / (k_ms / 1e3) / 1e9
+        peak = peaks["hbm_gbs"]
+        unit = "GB/s"
+    else:
+        achieved = amount / (k_ms / 1e3) / 1e12
+        peak = peaks["bf16_tflops_sustained"]
+        unit = "TFLOP/s"
+    for name, d in per_class.items():
+        if name in work:
+            b, amt = work[name]
+            d["achieved"] = amt / (d["ms_per_step"] / 1e3) / (1e9 if b == "hbm" else 1e12)
+            d["unit"] = "GB/s" if b == "hbm" else "TFLOP/s"
+            d["frac"] = d["achieved"] / (peaks["hbm_gbs"] if b == "hbm"
+                                         else peaks["bf16_tflops_sustained"])
+    # DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of one launch
+    # of the dominant class from the committed ncu --set full capture, next
+    # to the compulsory bytes of that same launch (scripts/summarize_profiles.py)
+    traffic, traffic_launch = None, None
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if tf.exists():
+        traffic_launch = json.loads(tf.read_text()).get(dominant)
+        if traffic_launch:
+            traffic = traffic_launch.get("dram_bytes")
+    return {"kernel": dominant, "bound": bound, "achieved": achieved, "peak": peak,
+            "unit": unit, "frac": achieved / peak, "traffic": traffic,
+            "traffic_launch": traffic_launch,
+            "method": "algorithmic work per step / CUDA-event time of the class's launches "
+                      "(same K steps re-run with per-launch events)",
+            "peak_source": peaks["source"] + (" sustained" if bound == "tensor" else ""),
+            "per_class": per_class}
+
+
 # -------------------------------------------------------------- our arm
 def run_ours(args, world, rank, local):
     import torch
@@ -359,49 +405,9 @@ def run_ours(args, world, rank, local):
         e2e = run_e2e(args, g, tokens, step, dev, batch, n, world, barrier)
 
     # ---- roofline of the dominant kernel class
-    peaks = measured_peaks()
     esz = 4 if args.gemm_dtype == "tf32" else 2
     chart_esz = 2 if chart_fmt == _lib.FI_CHART_F16 else 4
-    work = algorithmic_work(n, n, batch, length, esz, store_o=False, chart_esz=chart_esz)
-    per_class = {}
-    for name, (tot_ms, cnt) in prof.items():
-        if cnt:
-            per_class[name] = {"ms_per_step": tot_ms / args.steps,
-                               "launches_per_step": cnt // args.steps}
-    dominant = max((k for k in per_class if k in work), key=lambda k: per_class[k]["ms_per_step"])
-    bound, amount = work[dominant]
-    k_ms = per_class[dominant]["ms_per_step"]
-    if bound == "hbm":
-        achieved = amount / (k_ms / 1e3) / 1e9
-        peak = peaks["hbm_gbs"]
-        unit = "GB/s"
-    else:
-        achieved = amount / (k_ms / 1e3) / 1e12
-        peak = peaks["bf16_tflops_sustained"]
-        unit = "TFLOP/s"
-    for name, d in per_class.items():
-        if name in work:
-            b, amt = work[name]
-            d["achieved"] = amt / (d["ms_per_step"] / 1e3) / (1e9 if b == "hbm" else 1e12)
-            d["unit"] = "GB/s" if b == "hbm" else "TFLOP/s"
-            d["frac"] = d["achieved"] / (peaks["hbm_gbs"] if b == "hbm"
-                                         else peaks["bf16_tflops_sustained"])
-    # DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of one launch
-    # of the dominant class from the committed ncu --set full capture, next
-    # to the compulsory bytes of that same launch (scripts/summarize_profiles.py)
-    traffic, traffic_launch = None, None
-    tf = ROOT / "profiles" / "ncu_traffic.json"
-    if tf.exists():
-        traffic_launch = json.loads(tf.read_text()).get(dominant)
-        if traffic_launch:
-            traffic = traffic_launch.get("dram_bytes")
-    roofline = {"kernel": dominant, "bound": bound, "achieved": achieved, "peak": peak,
-                "unit": unit, "frac": achieved / peak, "traffic": traffic,
-                "traffic_launch": traffic_launch,
-                "method": "algorithmic work per step / CUDA-event time of the class's launches "
-                          "(same K steps re-run with per-launch events)",
-                "peak_source": peaks["source"] + (" sustained" if bound == "tensor" else ""),
-                "per_class": per_class}
+    roofline = roofline_block(prof, args.steps, n, batch, length, esz, chart_esz)
 
     # ---- CPU baseline (oracle port) on rank 0, N = 1 only
     cpu = None
@@ -435,6 +441,88 @@ def run_ours(args, world, rank, local):
             "loss": loss_val,
         }
         print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------ training workload
+TRAIN_METRIC = "neural SimplePCFG train step sentences/sec @|N|=4096,len40,d=512"
+
+
+def run_train(args, world, rank, local):
+    """--workload train: the full training step of train.py:201-227 on the GPU
+    (neural parameterisation d=512 -> inside fwd+bwd on the engine ->
+    autograd -> one all-reduce of the parameter gradients -> clip -> Adam),
+    B sentences per GPU (weak scaling)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2310_14997_b200 import _lib, neural
+    from paper_2310_14997_b200.grammar import GrammarDims
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS[args.config]
+    n, length = cfg["n"], cfg["length"]
+    batch = args.batch or cfg["batch"]
+    dims = GrammarDims(n, n, VOCAB)
+    ts = neural.TrainStep(neural.init_params(dims, 512, 0, device=dev),
+                          neural.TrainConfig(gemm_dtype=args.gemm_dtype))
+    tok = torch.as_tensor(np.random.default_rng(1 + rank).integers(0, VOCAB, (batch, length)),
+                          device=dev)
+    lengths = torch.full((batch,), length, dtype=torch.int32, device=dev)
+    lib = _lib.load()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        ts.step(tok, lengths, global_batch=batch * world)
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launch0 = lib.fi_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        loss = ts.step(tok, lengths, global_batch=batch * world)
+    e1.record()
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    gpu_launches = int(lib.fi_launch_count() - launch0)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    _lib.profile_enable(True)
+    for _ in range(args.steps):
+        ts.step(tok, lengths, global_batch=batch * world)
+    barrier()
+    _lib.profile_enable(False)
+    prof = _lib.profile_collect()
+    chart_fmt = int(_lib.chart_layout(_lib.shape(n, n, batch, length, args.gemm_dtype)).chart_fmt)
+    roofline = roofline_block(prof, args.steps, n, batch, length,
+                              4 if args.gemm_dtype == "tf32" else 2,
+                              2 if chart_fmt == _lib.FI_CHART_F16 else 4)
+    inside_ms = sum(d["ms_per_step"] for d in roofline["per_class"].values())
+    if rank == 0:
+        print(json.dumps({
+            "metric": TRAIN_METRIC, "value": world * batch / (ms / 1e3), "unit": "sentences/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": f"{args.gemm_dtype} GEMM operands, fp32 parameters / Adam",
+            "data": "synthetic uniform tokens; init_params(seed=0)",
+            "config": {"workload": f"config {args.config} train step: neural PCFG N=P={n}, d=512, "
+                                   f"length {length}, batch {batch} per GPU",
+                       "parallelism": f"dp{world}", "global_batch": batch * world},
+            "clocks": clk, "gpu_launches": gpu_launches, "loss": float(loss),
+            "inside_engine_ms_per_step": inside_ms,
+            "parameterisation_and_optimizer_ms_per_step": ms - inside_ms,
+            "roofline": roofline}), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
@@ -516,6 +604,8 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["inside", "train"], default="inside",
+                    help="inside: the op's fwd+bwd (headline); train: the full GPU training step")
     ap.add_argument("--config", type=int, choices=sorted(CONFIGS), default=3)
     ap.add_argument("--batch", type=int, default=None, help="sentences per GPU (weak) / "
                     "global (strong); default: the config's batch")
@@ -532,6 +622,8 @@ def main(argv=None):
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args, world, rank)
+    elif args.workload == "train":
+        run_train(args, world, rank, local)
     else:
         run_ours(args, world, rank, local)
 

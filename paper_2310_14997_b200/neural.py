@@ -259,13 +259,20 @@ class TrainStep:
         inside fwd+bwd on the engine -> autograd through the tables)."""
         cfg = self.config
         xs = list(self.params.tensors.values())
-        log_root, log_left, log_right, log_emit = self.tables()
-        unary = log_emit.T[tokens]                                 # inside.py:296-298
-        log_z = inside(log_left.contiguous(), log_right.contiguous(), log_root.contiguous(),
-                       unary.contiguous(), lengths, gemm_dtype=cfg.gemm_dtype)
-        nb = global_batch or tokens.shape[0]
-        loss = -log_z.sum() / nb                                   # train.py:218: -1/B
-        grads = torch.autograd.grad(loss, xs, allow_unused=True)  # tied: f4 unused
+        # the score-table GEMMs (N x d x (N+P)) run on TF32 tensor cores in the
+        # fast modes; fp32 mode keeps exact fp32 products (parity mode)
+        prev = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = cfg.gemm_dtype != "fp32"
+        try:
+            log_root, log_left, log_right, log_emit = self.tables()
+            unary = log_emit.T[tokens]                                 # inside.py:296-298
+            log_z = inside(log_left.contiguous(), log_right.contiguous(), log_root.contiguous(),
+                           unary.contiguous(), lengths, gemm_dtype=cfg.gemm_dtype)
+            nb = global_batch or tokens.shape[0]
+            loss = -log_z.sum() / nb                                   # train.py:218: -1/B
+            grads = torch.autograd.grad(loss, xs, allow_unused=True)  # tied: f4 unused
+        finally:
+            torch.backends.cuda.matmul.allow_tf32 = prev
         return loss, [torch.zeros_like(x) if g is None else g for x, g in zip(xs, grads)]
 
     def step(self, tokens: torch.Tensor, lengths: torch.Tensor, global_batch: int | None = None,
