@@ -120,6 +120,20 @@ int fi_inside_backward(const fi_shape* shape, const float* L, const float* R, co
 int fi_marginals(const fi_shape* shape, const int32_t* lengths, const float* grad_log_z,
                  float* mu, void* ws, void* stream);
 
+/* Span posterior mass mu(i, j) = sum_A mu_sym (MarginalTable.mu, inside.py:355-372)
+ * for widths >= 2, one float per chart row from rowbase(2) (same order as
+ * fi_marginals).  Requires store_chart = 1 and a completed backward. */
+int fi_span_marginals(const fi_shape* shape, const int32_t* lengths, const float* grad_log_z,
+                      float* mass, void* ws, void* stream);
+
+/* Minimum-Bayes-risk CKY over span masses (mbr_decode, parse.py:98-131),
+ * batched: for every sentence b and span (i, j), split[b, i, j] is the best
+ * split point (ties -> smallest) and score[b, i, j] the best total mass; both
+ * (B, l, l + 1) with index (b * l + i) * (l + 1) + j.  The tree is read off
+ * split from (0, len) down. */
+int fi_mbr_decode(const fi_shape* shape, const int32_t* lengths, const float* mass,
+                  float* score, int32_t* split, void* stream);
+
 /* Test hook: C[M,N] = A * B^T in the engine's tcgen05 GEMM (fp32 out).
  * a_mn / b_mn select MN-major operands: A is (M,K) K-major or (K,M) MN-major,
  * B is (N,K) K-major or (K,N) MN-major; elements bf16 (dtype 0) or fp32/tf32. */

@@ -26,6 +26,7 @@
 #include "../../include/flashinside.h"
 #include "fi_gemm.cuh"
 #include "fi_kernels.cuh"
+#include "fi_decode.cuh"
 
 using namespace fi;
 
@@ -807,6 +808,36 @@ int fi_marginals(const fi_shape* shape, const int32_t* lengths, const float* gra
   (p.half_chart ? k_marginals<true> : k_marginals<false>)<<<static_cast<unsigned>(nrows), 256, 0, st>>>(
       at<float>(ws, p.lq), p.half_chart ? at<float>(ws, p.lqs) : nullptr, at<float>(ws, p.o),
       grad_log_z, lengths, mu, p.B, p.l, p.Np, p.N);
+  FI_CUDA(cudaGetLastError());
+  return FI_OK;
+}
+
+int fi_span_marginals(const fi_shape* shape, const int32_t* lengths, const float* grad_log_z,
+                      float* mass, void* ws, void* stream) {
+  Plan p;
+  FI_TRY(make_plan(shape, &p));
+  FI_TRY(check_ptrs({lengths, grad_log_z, mass, ws}));
+  if (!p.store_o) return set_err(FI_ERR_ARG, "span marginals need store_chart = 1");
+  const long long nrows = p.rows - rowbase(2, p.B, p.l);
+  if (nrows <= 0) return FI_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  (p.half_chart ? k_span_mass<true> : k_span_mass<false>)<<<static_cast<unsigned>(nrows), 256, 0,
+                                                             st>>>(
+      at<float>(ws, p.lq), p.half_chart ? at<float>(ws, p.lqs) : nullptr, at<float>(ws, p.o),
+      grad_log_z, lengths, mass, p.B, p.l, p.Np, p.N);
+  ++g_launches;
+  FI_CUDA(cudaGetLastError());
+  return FI_OK;
+}
+
+int fi_mbr_decode(const fi_shape* shape, const int32_t* lengths, const float* mass,
+                  float* score, int32_t* split, void* stream) {
+  Plan p;
+  FI_TRY(make_plan(shape, &p));
+  FI_TRY(check_ptrs({lengths, mass, score, split}));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  k_mbr_cky<<<p.B, 128, 0, st>>>(mass, lengths, score, split, p.B, p.l);
+  ++g_launches;
   FI_CUDA(cudaGetLastError());
   return FI_OK;
 }

@@ -1,0 +1,49 @@
+"""GPU decoders against the reference's parse.py (tests/golden/decode.npz)."""
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2310_14997_b200.decode import mbr_decode_batch, mbr_score
+from paper_2310_14997_b200.grammar import GrammarDims, random_grammar
+
+pytestmark = pytest.mark.gpu
+GOLD = np.load(Path(__file__).parent / "golden" / "decode.npz")
+CASES = range(int(GOLD["n_cases"]))
+
+
+def case(k):
+    n_nt, n_pt, V, gseed, l = (int(x) for x in GOLD[f"c{k}_meta"])
+    g = random_grammar(GrammarDims(n_nt, n_pt, V), seed=gseed,
+                       concentration=float(GOLD[f"c{k}_conc"]))
+    return g, GOLD[f"c{k}_tokens"], l
+
+
+def spans(arr):
+    return frozenset(map(tuple, arr.tolist()))
+
+
+@pytest.mark.parametrize("k", CASES)
+def test_mbr_matches_reference(k):
+    g, toks, l = case(k)
+    (tree,), (mu,) = mbr_decode_batch(g, [toks], return_mass=True)
+    want_mu = GOLD[f"c{k}_mu"]
+    np.testing.assert_allclose(mu, want_mu, atol=1e-5)
+    want = spans(GOLD[f"c{k}_mbr"])
+    # same tree, or (a near-tie at fp32) a tree of equal objective under the
+    # reference's own float64 marginals
+    assert tree == want or mbr_score(want_mu, tree) == pytest.approx(mbr_score(want_mu, want),
+                                                                      abs=1e-5)
+    assert len(tree) == l - 1 and (0, l) in tree
+
+
+def test_mbr_batch_with_ragged_lengths():
+    g = random_grammar(GrammarDims(16, 12, 20), seed=4)
+    rng = np.random.default_rng(5)
+    sents = [rng.integers(0, 20, size=n) for n in (9, 3, 14, 2, 9)]
+    trees = mbr_decode_batch(g, sents)
+    solo = [mbr_decode_batch(g, [s])[0] for s in sents]
+    assert trees == solo
+    for s, t in zip(sents, trees):
+        assert len(t) == len(s) - 1 and (0, len(s)) in t
