@@ -134,6 +134,18 @@ int fi_span_marginals(const fi_shape* shape, const int32_t* lengths, const float
 int fi_mbr_decode(const fi_shape* shape, const int32_t* lengths, const float* mass,
                   float* score, int32_t* split, void* stream);
 
+/* Viterbi parse (viterbi_decode, parse.py:33-95), batched: the inside
+ * recursion in the (max, +) semiring with fp32 natural-log scores.  The
+ * caller provides va, vb, vo: (rows, np) fp32 scratch charts (rows / np of
+ * fi_get_chart_layout); outputs per sentence b: best[b] = the best
+ * derivation's log probability, and nodes[b, k, 0:3] = (i, j, sym) for the
+ * 2 len - 1 nodes of that derivation in preorder (internal nodes carry a
+ * nonterminal index, leaves a preterminal index); nodes is (B, 2 l, 3).
+ * Ties prefer the smallest split, then the smallest symbol index. */
+int fi_viterbi(const fi_shape* shape, const float* L, const float* R, const float* root,
+               const float* unary, const int32_t* lengths, float* va, float* vb, float* vo,
+               int32_t* nodes, float* best, void* stream);
+
 /* Test hook: C[M,N] = A * B^T in the engine's tcgen05 GEMM (fp32 out).
  * a_mn / b_mn select MN-major operands: A is (M,K) K-major or (K,M) MN-major,
  * B is (N,K) K-major or (K,N) MN-major; elements bf16 (dtype 0) or fp32/tf32. */

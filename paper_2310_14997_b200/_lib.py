@@ -75,6 +75,9 @@ SIGNATURES = [
      [POINTER(FiShape), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("fi_mbr_decode", c_int32,
      [POINTER(FiShape), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("fi_viterbi", c_int32,
+     [POINTER(FiShape), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+      c_void_p, c_void_p, c_void_p, c_void_p]),
     ("fi_test_gemm", c_int32,
      [c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p,
       c_void_p]),

@@ -842,6 +842,43 @@ int fi_mbr_decode(const fi_shape* shape, const int32_t* lengths, const float* ma
   return FI_OK;
 }
 
+int fi_viterbi(const fi_shape* shape, const float* L, const float* R, const float* root,
+               const float* unary, const int32_t* lengths, float* va, float* vb, float* vo,
+               int32_t* nodes, float* best, void* stream) {
+  Plan p;
+  FI_TRY(make_plan(shape, &p));
+  FI_TRY(check_ptrs({L, R, root, unary, lengths, va, vb, vo, nodes, best}));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int ld = p.N + p.P;
+  auto trop = [&](const float* A, int lda, const float* W, int M, int Ncols, int K, float* out) {
+    const dim3 grid((Ncols + kTropTile - 1) / kTropTile, (M + kTropTile - 1) / kTropTile);
+    k_trop_gemm<<<grid, 256, 0, st>>>(A, lda, W, ld, M, Ncols, K, out, out, Ncols, p.Np);
+    ++g_launches;
+    return cudaGetLastError();
+  };
+  // width 1: va/vb = max_t L/R[A, N + t] + unary[b, i, t]   (parse.py:56-57, :66-71)
+  const int m1 = p.B * p.l;
+  FI_CUDA(trop(unary, p.P, L + p.N, m1, p.N, p.P, va));
+  FI_CUDA(trop(unary, p.P, R + p.N, m1, p.N, p.P, vb));
+  for (int w = 2; w <= p.l; ++w) {
+    const int n_w = p.l - w + 1;
+    const long long r0 = rowbase(w, p.B, p.l);
+    k_vit_split<<<dim3((p.Np + 255) / 256, p.B * n_w), 256, 0, st>>>(va, vb, vo, lengths, p.B,
+                                                                      p.l, w, p.Np);
+    ++g_launches;
+    FI_CUDA(cudaGetLastError());
+    if (w < p.l) {  // parse.py:66-71 over the nonterminal block
+      FI_CUDA(trop(vo + r0 * p.Np, p.Np, L, p.B * n_w, p.N, p.N, va + r0 * p.Np));
+      FI_CUDA(trop(vo + r0 * p.Np, p.Np, R, p.B * n_w, p.N, p.N, vb + r0 * p.Np));
+    }
+  }
+  k_vit_backtrack<<<p.B, 256, 0, st>>>(va, vb, vo, unary, L, R, root, lengths, nodes, best, p.B,
+                                       p.l, p.N, p.P, p.Np, p.P);
+  ++g_launches;
+  FI_CUDA(cudaGetLastError());
+  return FI_OK;
+}
+
 int fi_test_gemm(int32_t dtype, int32_t a_mn, int32_t b_mn, int32_t M, int32_t N, int32_t K,
                  const void* A, const void* B, float* C, void* stream) {
   FI_TRY(check_ptrs({A, B, C}));

@@ -81,3 +81,228 @@ __global__ void __launch_bounds__(256) k_mbr_cky(const float* __restrict__ mass,
 }
 
 }  // namespace fi
+
+namespace fi {
+
+// ---------------------------------------------------------------------------
+// Viterbi (parse.py:33-95): the inside recursion in the (max, +) semiring.
+// Chart rows as in the inside pass (row(w, b, i)); log values in fp32 (no
+// shifts: max-plus never exponentiates).
+//   project:  va[r, A] = max_k (L[A, k] + vo[r, k]), vb likewise with R
+//             (k over the live block: preterminals at width 1, else
+//             nonterminals) -- a tropical GEMM on the CUDA cores
+//   split:    vo[r, A] = max_m va[m][i, A] + vb[w-m][i+m, A]
+//   root:     argmax_A root[A] + vo[top][A]
+//   backtrack per sentence on the device: smallest maximising split, then
+//             the maximising child symbols (ties -> smallest index).
+// ---------------------------------------------------------------------------
+
+// C[r, c] = max_k A[r, k] + W[c, k] for r < M, c < Ncols; A row stride lda,
+// W row stride ldw (K-major both).  64 x 64 tile per CTA, 256 threads x 4x4
+// outputs, K staged through shared memory in slices of 32.  Output columns
+// [0, Nhalf) go to outA, [Nhalf, 2 Nhalf) to outB (row stride ldo).
+constexpr int kTropTile = 64;
+constexpr int kTropK = 32;
+__global__ void __launch_bounds__(256) k_trop_gemm(const float* __restrict__ A, int lda,
+                                                   const float* __restrict__ W, int ldw, int M,
+                                                   int Ncols, int K, float* __restrict__ outA,
+                                                   float* __restrict__ outB, int Nhalf,
+                                                   int ldo) {
+  __shared__ float sa[kTropK][kTropTile + 4];
+  __shared__ float sw[kTropK][kTropTile + 4];
+  const int r0 = blockIdx.y * kTropTile, c0 = blockIdx.x * kTropTile;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  float acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = kNegInf;
+  for (int k0 = 0; k0 < K; k0 += kTropK) {
+    // stage a 64 x 32 slice of A and of W (transposed: [k][row])
+    for (int e = threadIdx.x; e < kTropTile * kTropK; e += 256) {
+      const int rr = e / kTropK, kk = e % kTropK;
+      const int gr = r0 + rr, gc = c0 + rr, gk = k0 + kk;
+      sa[kk][rr] = (gr < M && gk < K) ? A[static_cast<long long>(gr) * lda + gk] : kNegInf;
+      sw[kk][rr] = (gc < Ncols && gk < K) ? W[static_cast<long long>(gc) * ldw + gk] : kNegInf;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < kTropK; ++kk) {
+      float av[4], wv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = sa[kk][ty * 4 + a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) wv[b] = sw[kk][tx * 4 + b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fmaxf(acc[a][b], av[a] + wv[b]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int r = r0 + ty * 4 + a;
+    if (r >= M) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int c = c0 + tx * 4 + b;
+      if (c >= Ncols) continue;
+      if (c < Nhalf) outA[static_cast<long long>(r) * ldo + c] = acc[a][b];
+      else outB[static_cast<long long>(r) * ldo + c - Nhalf] = acc[a][b];
+    }
+  }
+}
+
+// vo[row(w, b, i), A] = max_m va[m][b, i, A] + vb[w-m][b, i+m, A]; padded spans -inf.
+__global__ void __launch_bounds__(256) k_vit_split(const float* __restrict__ VA,
+                                                   const float* __restrict__ VB,
+                                                   float* __restrict__ VO,
+                                                   const int* __restrict__ lengths, int B,
+                                                   int lmax, int w, int Np) {
+  const int local = blockIdx.y;
+  const int n_w = lmax - w + 1;
+  const int b = local / n_w, i = local % n_w;
+  const long long row = rowbase(w, B, lmax) + local;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= Np) return;
+  float best = kNegInf;
+  if (i + w <= lengths[b]) {
+    for (int m = 1; m < w; ++m) {
+      const float s = VA[chart_row(m, b, i, B, lmax) * Np + c] +
+                      VB[chart_row(w - m, b, i + m, B, lmax) * Np + c];
+      best = fmaxf(best, s);
+    }
+  }
+  VO[row * Np + c] = best;
+}
+
+// Per sentence: root argmax, then the derivation top-down.  Output per
+// sentence: nodes[b][k] = (i, j, sym) for the 2 len - 1 nodes (internal
+// nodes carry a nonterminal, leaves a preterminal index), root first.
+// L/R are the (N, N+P) log tables; VO width-1 rows hold the unary
+// (preterminal) scores in columns [0, P) (row stride Pp), wider rows the
+// nonterminal scores (row stride Np).
+__global__ void __launch_bounds__(256) k_vit_backtrack(
+    const float* __restrict__ VA, const float* __restrict__ VB, const float* __restrict__ VO,
+    const float* __restrict__ VO1, const float* __restrict__ L, const float* __restrict__ R,
+    const float* __restrict__ root, const int* __restrict__ lengths, int* __restrict__ nodes,
+    float* __restrict__ best_score, int B, int lmax, int N, int P, int Np, int Pp) {
+  __shared__ float sval[256];
+  __shared__ int sidx[256];
+  __shared__ int stack[3 * 1024];
+  __shared__ int top;
+  const int b = blockIdx.x;
+  const int len = lengths[b];
+  int* out = nodes + static_cast<long long>(b) * (2 * lmax) * 3;
+  auto argmax = [&](float v, int idx) {  // block argmax, ties -> smallest index
+    sval[threadIdx.x] = v;
+    sidx[threadIdx.x] = idx;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+      if (threadIdx.x < s) {
+        const float o = sval[threadIdx.x + s];
+        const int oi = sidx[threadIdx.x + s];
+        if (o > sval[threadIdx.x] || (o == sval[threadIdx.x] && oi < sidx[threadIdx.x])) {
+          sval[threadIdx.x] = o;
+          sidx[threadIdx.x] = oi;
+        }
+      }
+      __syncthreads();
+    }
+    const int r = sidx[0];
+    const float rv = sval[0];
+    __syncthreads();
+    return make_float2(rv, __int_as_float(r));
+  };
+  // root symbol
+  float v = kNegInf;
+  int vi = 0x7fffffff;
+  const long long top_row = chart_row(len, b, 0, B, lmax);
+  for (int a = threadIdx.x; a < N; a += blockDim.x) {
+    const float s = (len == 1 ? kNegInf : root[a] + VO[top_row * Np + a]);
+    if (s > v || (s == v && a < vi)) {
+      v = s;
+      vi = a;
+    }
+  }
+  float2 r = argmax(v, vi);
+  if (threadIdx.x == 0) {
+    best_score[b] = r.x;
+    stack[0] = 0;
+    stack[1] = len;
+    stack[2] = __float_as_int(r.y);
+    top = 1;
+  }
+  __syncthreads();
+  int nout = 0;
+  while (true) {
+    __syncthreads();
+    if (top == 0) break;
+    const int i = stack[3 * (top - 1)], j = stack[3 * (top - 1) + 1],
+              sym = stack[3 * (top - 1) + 2];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      --top;
+      out[3 * nout] = i;
+      out[3 * nout + 1] = j;
+      out[3 * nout + 2] = sym;
+    }
+    ++nout;
+    const int w = j - i;
+    if (w == 1) continue;  // leaf: sym is a preterminal index
+    // smallest maximising split (parse.py:62-64 argmax over m)
+    v = kNegInf;
+    vi = 0x7fffffff;
+    for (int m = 1 + threadIdx.x; m < w; m += blockDim.x) {
+      const float s = VA[chart_row(m, b, i, B, lmax) * Np + sym] +
+                      VB[chart_row(w - m, b, i + m, B, lmax) * Np + sym];
+      if (s > v || (s == v && m < vi)) {
+        v = s;
+        vi = m;
+      }
+    }
+    const int k = __float_as_int(argmax(v, vi).y);
+    // children: argmax over the live symbols of L[sym, s] + vo[k][i, s]
+    int child[2];
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const int ci = side ? i + k : i;
+      const int cw = side ? w - k : k;
+      const float* tab = (side ? R : L) + static_cast<long long>(sym) * (N + P);
+      v = kNegInf;
+      vi = 0x7fffffff;
+      if (cw == 1) {  // preterminal child: columns N + t
+        const float* u = VO1 + (static_cast<long long>(b) * lmax + ci) * Pp;
+        for (int t = threadIdx.x; t < P; t += blockDim.x) {
+          const float s = tab[N + t] + u[t];
+          if (s > v || (s == v && t < vi)) {
+            v = s;
+            vi = t;
+          }
+        }
+      } else {
+        const float* o = VO + chart_row(cw, b, ci, B, lmax) * Np;
+        for (int a = threadIdx.x; a < N; a += blockDim.x) {
+          const float s = tab[a] + o[a];
+          if (s > v || (s == v && a < vi)) {
+            v = s;
+            vi = a;
+          }
+        }
+      }
+      child[side] = __float_as_int(argmax(v, vi).y);
+    }
+    if (threadIdx.x == 0) {  // push right then left: left subtree is emitted first
+      stack[3 * top] = i + k;
+      stack[3 * top + 1] = j;
+      stack[3 * top + 2] = child[1];
+      stack[3 * top + 3] = i;
+      stack[3 * top + 4] = i + k;
+      stack[3 * top + 5] = child[0];
+      top += 2;
+    }
+  }
+}
+
+}  // namespace fi

@@ -7,6 +7,10 @@ Mirrors /root/reference/pkg/src/flashpcfg/parse.py:
   of sentences: one forward with the chart kept, one backward, the span
   masses (``fi_span_marginals``) and a batched CKY (``fi_mbr_decode``) all
   on the GPU; the host only reads the trees off the split tables.
+* ``viterbi_decode_batch``  ``viterbi_decode`` (parse.py:33-95): the inside
+  recursion in the (max, +) semiring -- tropical projections on the CUDA
+  cores, a max-over-splits kernel and a per-sentence device backtrack
+  (``fi_viterbi``); ``tree_log_prob`` (parse.py:134-158) rescoring on the host.
 * ``sentence_f1``       parse.py:161-183 (trivial spans removed).
 
 Ties prefer the smallest split point, as in the reference.  The engine works
@@ -132,3 +136,77 @@ def mbr_decode_batch(g, sentences, gemm_dtype: str = "fp32", dg: DeviceGrammar |
 def mbr_score(mu: np.ndarray, spans) -> float:
     """Total posterior mass of a tree's internal spans (the MBR objective)."""
     return float(sum(mu[i, j] for (i, j) in spans))
+
+
+# ------------------------------------------------------------------ Viterbi
+def viterbi_decode_batch(g, sentences, dg: DeviceGrammar | None = None, max_batch: int = 64):
+    """Best derivation of every sentence (viterbi_decode, parse.py:33-95).
+
+    Returns a list of dicts {"spans": frozenset, "labels": {(i, j): "NT<a>"},
+    "leaf_labels": ("PT<t>", ...), "log_prob": float}.  The (max, +) chart,
+    the tropical projections and the backtrack all run on the GPU."""
+    sents = [_prepare(g, s) for s in sentences]
+    dg = dg or DeviceGrammar(g)
+    lib = _lib.load()
+    n_nt, n_pt = g.dims.n_nt, g.dims.n_pt
+    out: list = [None] * len(sents)
+    with torch.no_grad():
+        for idx in _batches(sents, max_batch):
+            B = len(idx)
+            lmax = max(sents[k].size for k in idx)
+            tok = torch.zeros(B, lmax, dtype=torch.long, device=dg.device)
+            for r, k in enumerate(idx):
+                tok[r, :sents[k].size] = torch.as_tensor(sents[k])
+            lens = torch.tensor([sents[k].size for k in idx], dtype=torch.int32, device=dg.device)
+            unary = dg.unary(tok)
+            shape = _lib.shape(n_nt, n_pt, B, lmax, "fp32", False)
+            lay = _lib.chart_layout(shape)
+            rows, np_ = int(lay.rows), int(lay.np)
+            va, vb, vo = (torch.empty(rows, np_, dtype=torch.float32, device=dg.device)
+                          for _ in range(3))
+            nodes = torch.zeros(B, 2 * lmax, 3, dtype=torch.int32, device=dg.device)
+            best = torch.empty(B, dtype=torch.float32, device=dg.device)
+            _lib.check(lib.fi_viterbi(ctypes.byref(shape), _p(dg.L), _p(dg.R), _p(dg.root),
+                                      _p(unary), _p(lens), _p(va), _p(vb), _p(vo), _p(nodes),
+                                      _p(best), _stream(dg.device)))
+            nd = nodes.cpu().numpy()
+            bs = best.double().cpu().numpy()
+            for r, k in enumerate(idx):
+                l = sents[k].size
+                if not np.isfinite(bs[r]):
+                    raise ParseError(f"sentence {k}: no parse with positive probability")
+                spans, labels, leaves = set(), {}, [""] * l
+                for i, j, sym in nd[r, :2 * l - 1]:
+                    if j - i == 1:
+                        leaves[int(i)] = f"PT{int(sym)}"
+                    else:
+                        spans.add((int(i), int(j)))
+                        labels[(int(i), int(j))] = f"NT{int(sym)}"
+                out[k] = {"spans": frozenset(spans), "labels": labels,
+                          "leaf_labels": tuple(leaves), "log_prob": float(bs[r])}
+    return out
+
+
+def tree_log_prob(g, tokens, tree: dict) -> float:
+    """Log probability of a labelled derivation (parse.py:134-158), float64 on the host."""
+    toks = np.asarray(tokens, dtype=np.int64)
+    n_nt = g.dims.n_nt
+    spans = tree["spans"]
+    l = toks.size
+
+    def sym_of(i, j):
+        if j - i == 1:
+            return n_nt + int(tree["leaf_labels"][i][2:])
+        return int(tree["labels"][(i, j)][2:])
+
+    def covered(i, j):
+        return j - i == 1 or (i, j) in spans
+
+    total = g.log_root[sym_of(0, l)]
+    for (i, j) in spans:
+        k = next(k for k in range(i + 1, j) if covered(i, k) and covered(k, j))
+        parent = sym_of(i, j)
+        total += g.log_left[parent, sym_of(i, k)] + g.log_right[parent, sym_of(k, j)]
+    for i, tok in enumerate(toks):
+        total += g.log_emit[sym_of(i, i + 1) - n_nt, tok]
+    return float(total)

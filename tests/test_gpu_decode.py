@@ -47,3 +47,28 @@ def test_mbr_batch_with_ragged_lengths():
     assert trees == solo
     for s, t in zip(sents, trees):
         assert len(t) == len(s) - 1 and (0, len(s)) in t
+
+
+@pytest.mark.parametrize("k", CASES)
+def test_viterbi_matches_reference(k):
+    from paper_2310_14997_b200.decode import tree_log_prob, viterbi_decode_batch
+    g, toks, l = case(k)
+    (t,) = viterbi_decode_batch(g, [toks])
+    want_lp = float(GOLD[f"c{k}_vit_logp"])
+    lp = tree_log_prob(g, toks, t)                     # float64 score of our tree
+    assert t["log_prob"] == pytest.approx(lp, abs=1e-3)  # fp32 chart vs float64 rescoring
+    # same tree, or an equally probable one (near-tie at fp32)
+    assert t["spans"] == spans(GOLD[f"c{k}_vit"]) or lp == pytest.approx(want_lp, abs=1e-4)
+    assert lp == pytest.approx(want_lp, abs=1e-4)
+
+
+def test_viterbi_batch_matches_single_sentences():
+    from paper_2310_14997_b200.decode import viterbi_decode_batch
+    g = random_grammar(GrammarDims(24, 16, 30), seed=9)
+    rng = np.random.default_rng(10)
+    sents = [rng.integers(0, 30, size=n) for n in (11, 2, 17, 6)]
+    batch = viterbi_decode_batch(g, sents)
+    for s, t in zip(sents, batch):
+        (solo,) = viterbi_decode_batch(g, [s])
+        assert t["spans"] == solo["spans"] and t["labels"] == solo["labels"]
+        assert len(t["spans"]) == len(s) - 1
