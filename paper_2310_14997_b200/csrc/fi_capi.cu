@@ -299,6 +299,11 @@ int launch_cluster(K kern, int cluster, dim3 grid, dim3 block, size_t smem, cuda
   return FI_OK;
 }
 
+// GEMM smem ring depth for launches enqueued by this thread: 0 = the deepest
+// ring that fits (one CTA per SM); the dual-stream sweep (see forward_impl)
+// caps it so a bandwidth-kernel CTA can share each SM with a GEMM CTA.
+thread_local int g_gemm_stages = 0;
+
 template <typename T, int BN, bool AMN, bool BMN, int EPI, bool SPLIT, int CHUNK, bool PAIR>
 int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_row0,
                 const GemmEpi& ep, cudaStream_t st, int bn) {
@@ -325,6 +330,8 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
   sh.K = K;
   sh.a_row0 = a_row0;
   sh.bn = bn;
+  sh.stages = (g_gemm_stages > 1 && g_gemm_stages < Cf::STAGES) ? g_gemm_stages : Cf::STAGES;
+  const size_t smem_bytes = static_cast<size_t>(sh.stages) * Cf::STAGE_BYTES + 1024 + 256;
   sh.num_m = (M + Cf::BM * NCTA - 1) / (Cf::BM * NCTA);
   sh.num_n = (N + bn - 1) / bn;
   sh.num_k = (K + Cf::BK - 1) / Cf::BK;
@@ -345,10 +352,10 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
                  : EPI == EPI_WGRAD ? FI_PROF_GEMM_WGRAD
                  : EPI == EPI_STORE ? FI_PROF_PREP : FI_PROF_GEMM_DGRAD, st);  // DGRAD(_H), DUNARY
   if constexpr (PAIR) {
-    FI_TRY(launch_cluster(kern, 2, dim3(grid), dim3(256), Cf::SMEM_BYTES, st, ta, tb, ta2, tb2,
+    FI_TRY(launch_cluster(kern, 2, dim3(grid), dim3(256), smem_bytes, st, ta, tb, ta2, tb2,
                           sh, ep));
   } else {
-    kern<<<grid, 256, Cf::SMEM_BYTES, st>>>(ta, tb, ta2, tb2, sh, ep);
+    kern<<<grid, 256, smem_bytes, st>>>(ta, tb, ta2, tb2, sh, ep);
     ++g_launches;
   }
   FI_CUDA(cudaGetLastError());
@@ -465,6 +472,77 @@ int check_ptrs(std::initializer_list<const void*> ps) {
   return FI_OK;
 }
 
+// ------------------------------------------------------ dual-stream sweep
+// The width sweep is a chain of dependent launches, alternating a tensor-bound
+// GEMM and an HBM-bound split / gather kernel.  Sentences are independent, so
+// the batch is cut in two halves run on two streams, the second one launch
+// behind the first: while one half's GEMM runs, the other half's bandwidth
+// kernel streams HBM on the same SMs (the GEMM ring is capped at
+// FI_DUAL_GEMM_STAGES so a bandwidth CTA fits beside it).  FI_DUAL=0 runs the
+// whole batch on the caller's stream (the default: measured 15.4 vs 14.6 ms at
+// config 3 -- the co-resident kernels contend more than they overlap).
+struct AuxStream {
+  cudaStream_t s[64] = {};
+};
+cudaStream_t aux_stream(int& err) {
+  static AuxStream a;
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (!a.s[dev & 63]) {
+    if (cudaStreamCreateWithFlags(&a.s[dev & 63], cudaStreamNonBlocking) != cudaSuccess) {
+      err = 1;
+      return nullptr;
+    }
+  }
+  return a.s[dev & 63];
+}
+
+// Record on `from`, make `to` wait; the event is released once enqueued.
+int stream_wait(cudaStream_t to, cudaStream_t from) {
+  cudaEvent_t e;
+  FI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  FI_CUDA(cudaEventRecord(e, from));
+  FI_CUDA(cudaStreamWaitEvent(to, e, 0));
+  FI_CUDA(cudaEventDestroy(e));
+  return FI_OK;
+}
+
+struct Halves {
+  int n = 1;
+  int b0[2] = {0, 0}, nb[2] = {0, 0};
+  cudaStream_t st[2] = {nullptr, nullptr};
+};
+
+int make_halves(const Plan& p, cudaStream_t st, Halves* h) {
+  static const int dual = env_int("FI_DUAL", 0);  // measured slower (contention), opt-in
+  h->st[0] = st;
+  h->b0[0] = 0;
+  h->nb[0] = p.B;
+  h->n = 1;
+  if (!dual || p.B < 2) return FI_OK;
+  int err = 0;
+  cudaStream_t s2 = aux_stream(err);
+  if (err || !s2) return set_err(FI_ERR_CUDA, "cannot create the auxiliary stream");
+  h->n = 2;
+  h->st[1] = s2;
+  h->nb[0] = p.B / 2;
+  h->b0[1] = p.B / 2;
+  h->nb[1] = p.B - p.B / 2;
+  return stream_wait(s2, st);  // the second stream starts after everything before
+}
+
+struct GemmStagesScope {  // cap the GEMM ring for this thread's launches
+  int saved;
+  explicit GemmStagesScope(int s) : saved(g_gemm_stages) { g_gemm_stages = s; }
+  ~GemmStagesScope() { g_gemm_stages = saved; }
+};
+int dual_gemm_stages(const Halves& h) {
+  static const int s = env_int("FI_DUAL_GEMM_STAGES", 3);
+  return h.n > 1 ? s : 0;
+}
+
 // ------------------------------------------------------------------ forward
 template <typename T, typename CT>
 int forward_impl(const Plan& p, const float* L, const float* R, const float* root,
@@ -503,16 +581,27 @@ int forward_impl(const Plan& p, const float* L, const float* R, const float* roo
   const Operand opE1{e1, p.Pp, static_cast<long long>(p.B) * p.l, p.Pp, false, p.e1_lo};
   const Operand opEall{eall, p.Np, p.rows, p.Np, false, p.eall_lo};
 
-  GemmEpi ep = {};
-  ep.X = X;
-  ep.outA = A;
-  ep.outB = Bc;
-  ep.Np = p.Np;
-  ep.M = p.B * p.l;
-  ep.row0 = 0;
-  FI_TRY((run_gemm<T, false, false, kEpiFwd>(opE1, opWnp, ep.M, 2 * p.Np, p.Pp, 0, ep, st)));
-
-  for (int w = 2; w <= p.l; ++w) {
+  // projection GEMM of width w for sentences [b0, b0 + nb)
+  auto gemm = [&](int w, int b0, int nb, cudaStream_t s) -> int {
+    GemmEpi ep = {};
+    ep.X = X;
+    ep.outA = A;
+    ep.outB = Bc;
+    ep.Np = p.Np;
+    if (w == 1) {
+      ep.M = nb * p.l;
+      ep.row0 = static_cast<long long>(b0) * p.l;
+      return run_gemm<T, false, false, kEpiFwd>(opE1, opWnp, ep.M, 2 * p.Np, p.Pp,
+                                                 static_cast<int>(ep.row0), ep, s);
+    }
+    const int n_w = p.l - w + 1;
+    ep.M = nb * n_w;
+    ep.row0 = rowbase(w, p.B, p.l) + static_cast<long long>(b0) * n_w;
+    return run_gemm<T, false, false, kEpiFwd>(opEall, opWnn, ep.M, 2 * p.Np, p.Np,
+                                               static_cast<int>(ep.row0), ep, s);
+  };
+  // split contraction of width w for sentences [b0, b0 + nb)
+  auto split = [&](int w, int b0, int nb, cudaStream_t s) -> int {
     const int n_w = p.l - w + 1;
     SplitArgs sa;
     sa.A = A;
@@ -532,61 +621,71 @@ int forward_impl(const Plan& p, const float* L, const float* R, const float* roo
     sa.N = p.N;
     sa.Np = p.Np;
     sa.w = w;
+    sa.b0 = b0;
+    sa.nb = nb;
     const Decomp& dc = p.dsplit;
     sa.cols_per_cta = dc.cols_per_cta;
-    const dim3 grid(dc.clusters, p.B * n_w);
-    {
-      ProfScope prof(FI_PROF_SPLIT, st);
-      static const int pers = env_int("FI_SPLIT_PERS", 1);
-      if (pers && p.Np <= 8192) {
-        // persistent one-CTA-per-row kernel: ~72 KB of ring per CTA (2-3 CTAs/SM)
-        const int cons = p.Np / 4 < 256 ? p.Np / 4 : 256;
-        const int V = p.Np / (4 * cons);
-        const size_t stage_bytes = 2ull * p.Np * sizeof(CT);
-        static const int env_st = env_int("FI_PSTAGES", 0);
-        int stages = env_st ? env_st : static_cast<int>(73728 / stage_bytes);
-        stages = stages < 2 ? 2 : (stages > 8 ? 8 : stages);
-        static const int nprod = env_int("FI_NPROD", 4);
-        const size_t smem = static_cast<size_t>(stages) * (stage_bytes + 16 + sizeof(StageHdr)) +
-                            8ull * p.l + 64;
-        const int nrows = p.B * n_w;
-        FI_TRY(dispatch_v(V, [&](auto vc) {
-          constexpr int VV = decltype(vc)::value;
-          auto kern = k_split_fwd_pers<T, CT, VV>;
-          FI_TRY(set_smem(kern, smem));
-          int occ = 0;
-          FI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 + cons, smem));
-          occ = occ < 1 ? 1 : occ;
-          const int grid = nrows < occ * num_sms() ? nrows : occ * num_sms();
-          kern<<<grid, 32 + cons, smem, st>>>(sa, stages, nprod);
-          ++g_launches;
-          FI_CUDA(cudaGetLastError());
-          return FI_OK;
-        }));
-      } else {
-        const int stages = dc.stages;
-        const size_t smem = align128(sizeof(SplitTerm) * (w - 1)) +
-                            static_cast<size_t>(stages) * (2 * dc.cols_per_cta * sizeof(CT) + 16);
-        const dim3 block(32 + dc.threads);
-        FI_TRY(dispatch_v(dc.v, [&](auto vc) {
-          constexpr int V = decltype(vc)::value;
-          if constexpr (V > 4) {
-            return set_err(FI_ERR_UNSUPPORTED, "split decomposition V=%d", V);
-          } else {
-            FI_TRY(set_smem(k_split_fwd_bulk<T, CT, V>, smem));
-            return launch_cluster(k_split_fwd_bulk<T, CT, V>, dc.clusters, grid, block, smem, st,
-                                  sa, stages);
-          }
-        }));
-      }
+    ProfScope prof(FI_PROF_SPLIT, s);
+    static const int pers = env_int("FI_SPLIT_PERS", 1);
+    if (pers && p.Np <= 8192) {
+      // persistent one-CTA-per-row kernel: ~72 KB of ring per CTA (2-3 CTAs/SM)
+      const int cons = p.Np / 4 < 256 ? p.Np / 4 : 256;
+      const int V = p.Np / (4 * cons);
+      const size_t stage_bytes = 2ull * p.Np * sizeof(CT);
+      static const int env_st = env_int("FI_PSTAGES", 0);
+      int stages = env_st ? env_st : static_cast<int>(73728 / stage_bytes);
+      stages = stages < 2 ? 2 : (stages > 8 ? 8 : stages);
+      static const int nprod = env_int("FI_NPROD", 4);
+      const size_t smem = static_cast<size_t>(stages) * (stage_bytes + 16 + sizeof(StageHdr)) +
+                          8ull * p.l + 64;
+      const int nrows = nb * n_w;
+      return dispatch_v(V, [&](auto vc) {
+        constexpr int VV = decltype(vc)::value;
+        auto kern = k_split_fwd_pers<T, CT, VV>;
+        FI_TRY(set_smem(kern, smem));
+        int occ = 0;
+        FI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 + cons, smem));
+        occ = occ < 1 ? 1 : occ;
+        const int grid = nrows < occ * num_sms() ? nrows : occ * num_sms();
+        kern<<<grid, 32 + cons, smem, s>>>(sa, stages, nprod);
+        ++g_launches;
+        FI_CUDA(cudaGetLastError());
+        return FI_OK;
+      });
     }
-    if (w < p.l) {
-      ep.M = p.B * n_w;
-      ep.row0 = rowbase(w, p.B, p.l);
-      FI_TRY((run_gemm<T, false, false, kEpiFwd>(opEall, opWnn, ep.M, 2 * p.Np, p.Np,
-                                                  static_cast<int>(ep.row0), ep, st)));
+    const int stages = dc.stages;
+    const size_t smem = align128(sizeof(SplitTerm) * (w - 1)) +
+                        static_cast<size_t>(stages) * (2 * dc.cols_per_cta * sizeof(CT) + 16);
+    const dim3 grid(dc.clusters, nb * n_w);
+    const dim3 block(32 + dc.threads);
+    return dispatch_v(dc.v, [&](auto vc) {
+      constexpr int V = decltype(vc)::value;
+      if constexpr (V > 4) {
+        return set_err(FI_ERR_UNSUPPORTED, "split decomposition V=%d", V);
+      } else {
+        FI_TRY(set_smem(k_split_fwd_bulk<T, CT, V>, smem));
+        return launch_cluster(k_split_fwd_bulk<T, CT, V>, dc.clusters, grid, block, smem, s, sa,
+                              stages);
+      }
+    });
+  };
+
+  Halves h;
+  FI_TRY(make_halves(p, st, &h));
+  GemmStagesScope gs(dual_gemm_stages(h));
+  // width 1 GEMMs; the second stream trails the first by one launch
+  FI_TRY(gemm(1, h.b0[0], h.nb[0], h.st[0]));
+  if (h.n > 1) {
+    FI_TRY(stream_wait(h.st[1], h.st[0]));
+    FI_TRY(gemm(1, h.b0[1], h.nb[1], h.st[1]));
+  }
+  for (int w = 2; w <= p.l; ++w) {
+    for (int k = 0; k < h.n; ++k) {
+      FI_TRY(split(w, h.b0[k], h.nb[k], h.st[k]));
+      if (w < p.l) FI_TRY(gemm(w, h.b0[k], h.nb[k], h.st[k]));
     }
   }
+  if (h.n > 1) FI_TRY(stream_wait(st, h.st[1]));  // join: the caller's stream sees all
   return FI_OK;
 }
 
@@ -597,8 +696,8 @@ int backward_impl(const Plan& p, const float* L, const float* R, const float* ro
                   float* dL, float* dR, float* droot, float* dunary, void* ws, cudaStream_t st) {
   T* wnn = at<T>(ws, p.wnn);
   T* wnp = at<T>(ws, p.wnp);
-  T* e1 = at<T>(ws, p.e1);
   T* eall = at<T>(ws, p.eall);
+  T* e1 = at<T>(ws, p.e1);
   T* gall = at<T>(ws, p.gall);
   float* A = at<float>(ws, p.a);
   float* Bc = at<float>(ws, p.b);
@@ -624,7 +723,8 @@ int backward_impl(const Plan& p, const float* L, const float* R, const float* ro
   const Operand opWnpMN{wnp, p.Pp, 2LL * p.Np, p.Pp, true, p.wnp_lo};
   const Operand opGall{gall, 2LL * p.Np, p.rows, 2LL * p.Np, false, p.gall_lo};
 
-  for (int m = p.l - 1; m >= 1; --m) {
+  // gather-form split backward of child width m for sentences [b0, b0 + nb)
+  auto gather = [&](int m, int b0, int nb, cudaStream_t s) -> int {
     const int n_m = p.l - m + 1;
     GatherArgs ga;
     ga.A = A;
@@ -640,55 +740,77 @@ int backward_impl(const Plan& p, const float* L, const float* R, const float* ro
     ga.lmax = p.l;
     ga.Np = p.Np;
     ga.m = m;
+    ga.b0 = b0;
+    ga.nb = nb;
     const Decomp& dc = p.dgather;
     ga.cols_per_cta = dc.cols_per_cta;
-    const dim3 grid(dc.clusters, p.B * n_m);
-    {
-      ProfScope prof(FI_PROF_GATHER, st);
-      const int stages = dc.stages;
-      const size_t qb = sizeof(CT) == 2 ? dc.cols_per_cta * 2 + dc.cols_per_cta / 8
-                                         : dc.cols_per_cta * 4;
-      const size_t smem = align128(sizeof(GatherTerm) * p.l) +
-                          static_cast<size_t>(stages) * (dc.cols_per_cta * sizeof(CT) + qb + 16);
-      FI_TRY(dispatch_v(dc.v, [&](auto vc) {
-        constexpr int V = decltype(vc)::value;
-        if constexpr (V > 4) {
-          return set_err(FI_ERR_UNSUPPORTED, "gather decomposition V=%d", V);
-        } else {
-          FI_TRY(set_smem(k_gather_bwd_bulk<T, CT, V>, smem));
-          static const int nprod = env_int("FI_GNPROD", 4);
-          k_gather_bwd_bulk<T, CT, V><<<grid, 32 + dc.threads, smem, st>>>(ga, stages, nprod);
-          return FI_OK;
-        }
-      }));
-    }
+    const dim3 grid(dc.clusters, nb * n_m);
+    ProfScope prof(FI_PROF_GATHER, s);
+    const int stages = dc.stages;
+    const size_t qb = sizeof(CT) == 2 ? dc.cols_per_cta * 2 + dc.cols_per_cta / 8
+                                       : dc.cols_per_cta * 4;
+    const size_t smem = align128(sizeof(GatherTerm) * p.l) +
+                        static_cast<size_t>(stages) * (dc.cols_per_cta * sizeof(CT) + qb + 16);
+    FI_TRY(dispatch_v(dc.v, [&](auto vc) {
+      constexpr int V = decltype(vc)::value;
+      if constexpr (V > 4) {
+        return set_err(FI_ERR_UNSUPPORTED, "gather decomposition V=%d", V);
+      } else {
+        FI_TRY(set_smem(k_gather_bwd_bulk<T, CT, V>, smem));
+        static const int nprod = env_int("FI_GNPROD", 4);
+        k_gather_bwd_bulk<T, CT, V><<<grid, 32 + dc.threads, smem, s>>>(ga, stages, nprod);
+        return FI_OK;
+      }
+    }));
     ++g_launches;
     FI_CUDA(cudaGetLastError());
-
+    return FI_OK;
+  };
+  // outside-weight GEMM of child width m (dunary at m = 1) for sentences [b0, b0 + nb)
+  auto dgrad = [&](int m, int b0, int nb, cudaStream_t s) -> int {
+    const int n_m = p.l - m + 1;
     GemmEpi ep = {};
     ep.X = X;
     ep.Np = p.Np;
-    ep.M = p.B * n_m;
-    ep.row0 = rowbase(m, p.B, p.l);
+    ep.M = nb * n_m;
+    ep.row0 = rowbase(m, p.B, p.l) + static_cast<long long>(b0) * n_m;
     ep.lengths = lengths;
     ep.width = m;
     ep.n_w = n_m;
+    ep.b0 = b0;
     if (m >= 2) {
       ep.LQ = LQ;
       ep.LQS = LQS;
       constexpr int kEpiDgrad = sizeof(CT) == 2 ? EPI_DGRAD_H : EPI_DGRAD;
-      FI_TRY((run_gemm<T, false, true, kEpiDgrad>(opGall, opWnnMN, ep.M, p.Np, 2 * p.Np,
-                                                   static_cast<int>(ep.row0), ep, st)));
-    } else {
-      ep.dunary = dunary;
-      ep.vec4 = (p.P % 4 == 0 && reinterpret_cast<uintptr_t>(dunary) % 16 == 0 &&
-                 reinterpret_cast<uintptr_t>(unary) % 16 == 0);
-      ep.unary = unary;
-      ep.P = p.P;
-      ep.lmax = p.l;
-      FI_TRY((run_gemm<T, false, true, EPI_DUNARY>(opGall, opWnpMN, ep.M, p.Pp, 2 * p.Np, 0, ep,
-                                                    st)));
+      return run_gemm<T, false, true, kEpiDgrad>(opGall, opWnnMN, ep.M, p.Np, 2 * p.Np,
+                                                  static_cast<int>(ep.row0), ep, s);
     }
+    ep.dunary = dunary;
+    ep.vec4 = (p.P % 4 == 0 && reinterpret_cast<uintptr_t>(dunary) % 16 == 0 &&
+               reinterpret_cast<uintptr_t>(unary) % 16 == 0);
+    ep.unary = unary;
+    ep.P = p.P;
+    ep.lmax = p.l;
+    return run_gemm<T, false, true, EPI_DUNARY>(opGall, opWnpMN, ep.M, p.Pp, 2 * p.Np,
+                                                 static_cast<int>(ep.row0), ep, s);
+  };
+
+  {
+    Halves h;
+    FI_TRY(make_halves(p, st, &h));
+    GemmStagesScope gs(dual_gemm_stages(h));
+    FI_TRY(gather(p.l - 1, h.b0[0], h.nb[0], h.st[0]));
+    if (h.n > 1) {  // the second stream trails the first by one launch
+      FI_TRY(stream_wait(h.st[1], h.st[0]));
+      FI_TRY(gather(p.l - 1, h.b0[1], h.nb[1], h.st[1]));
+    }
+    for (int m = p.l - 1; m >= 1; --m) {
+      for (int k = 0; k < h.n; ++k) {
+        FI_TRY(dgrad(m, h.b0[k], h.nb[k], h.st[k]));
+        if (m > 1) FI_TRY(gather(m - 1, h.b0[k], h.nb[k], h.st[k]));
+      }
+    }
+    if (h.n > 1) FI_TRY(stream_wait(st, h.st[1]));
   }
 
   // weight gradients: dW = G^T E summed over every span, then * exp(table)

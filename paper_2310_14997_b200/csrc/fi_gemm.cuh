@@ -44,6 +44,7 @@ struct GemmShape {
   int a_row0;     // K-major A: first row coordinate inside the tensor map
   int num_m, num_n, num_k;  // tiles of (128 or 256 for pairs) x bn x BK
   int bn;         // N tile (runtime, <= the kernel's BN bound, multiple of 32)
+  int stages;     // smem ring depth (runtime, <= GemmCfg::STAGES)
 };
 
 struct GemmEpi {
@@ -60,6 +61,7 @@ struct GemmEpi {
   const int* lengths;
   int width;
   int n_w;
+  int b0;             // first sentence of this launch's row range (DGRAD top-span check)
   // EPI_DUNARY
   float* dunary;
   const float* unary;
@@ -234,11 +236,12 @@ __global__ void __launch_bounds__(256, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const int NS = sh.stages;
   uint8_t* smA = smem;
-  uint8_t* smB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smB + C::STAGES * C::B_BYTES);
-  uint64_t* empty = full + C::STAGES;
-  uint64_t* tfull = empty + C::STAGES;
+  uint8_t* smB = smem + NS * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smB + NS * C::B_BYTES);
+  uint64_t* empty = full + NS;
+  uint64_t* tfull = empty + NS;
   uint64_t* tempty = tfull + 2;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -259,7 +262,7 @@ __global__ void __launch_bounds__(256, 1)
       tma_prefetch_desc(&tmA2);
       tma_prefetch_desc(&tmB2);
     }
-    for (int s = 0; s < C::STAGES; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -323,7 +326,7 @@ __global__ void __launch_bounds__(256, 1)
             for (int j = 0; j < bn_cta / C::ATOM; ++j)
               load(b_dst + j * C::BK * 128, mb, n0 + j * C::ATOM, kb * C::BK);
           }
-          if (++stage == C::STAGES) {
+          if (++stage == NS) {
             stage = 0;
             phase ^= 1;
           }
@@ -370,7 +373,7 @@ __global__ void __launch_bounds__(256, 1)
           }
           if constexpr (PAIR) umma_commit2(&empty[stage]);
           else umma_commit(&empty[stage]);
-          if (++stage == C::STAGES) {
+          if (++stage == NS) {
             stage = 0;
             phase ^= 1;
           }
@@ -424,10 +427,11 @@ __global__ void __launch_bounds__(256, 1)
         } else if constexpr (EPI == EPI_DGRAD_H) {
           rowptr = reinterpret_cast<float*>(reinterpret_cast<__half*>(ep.LQ) + grow * ep.Np);
         } else if constexpr (EPI == EPI_DUNARY) {
+          // width-1 rows: grow = b * lmax + i (rowbase(1) = 0)
           xv = static_cast<float>(ep.X[grow]);
-          const int b = lrow / ep.lmax, i = lrow % ep.lmax;
+          const int b = static_cast<int>(grow / ep.lmax), i = static_cast<int>(grow % ep.lmax);
           aux = i < ep.lengths[b];
-          rowptr = ep.dunary + static_cast<long long>(lrow) * ep.P;
+          rowptr = ep.dunary + grow * ep.P;
         } else if constexpr (EPI == EPI_WGRAD) {
           aux = lrow >= ep.Np;  // 0 -> left table, 1 -> right table
           const int arow = aux ? lrow - ep.Np : lrow;
@@ -441,11 +445,12 @@ __global__ void __launch_bounds__(256, 1)
       if constexpr (EPI == EPI_DGRAD || EPI == EPI_DGRAD_H) {
         // the seed kernel owns the top span of each sentence (inside.py:400-404)
         if (ok) {
-          const int b = lrow / ep.n_w, i = lrow % ep.n_w;
+          const int b = ep.b0 + lrow / ep.n_w, i = lrow % ep.n_w;
           if (i == 0 && ep.lengths[b] == ep.width) ok = false;
         }
       }
-      const int erow = (EPI == EPI_WGRAD && aux) ? lrow - ep.Np : lrow;
+      const int erow = (EPI == EPI_WGRAD && aux) ? lrow - ep.Np
+                       : EPI == EPI_DUNARY ? static_cast<int>(grow) : lrow;
       // epilogue of one 32-column chunk j of this tile (skips the N tail; the
       // forward's [a | b] columns split at Np, possibly inside a tile)
       auto emit = [&](int j, const float (&v)[32]) {

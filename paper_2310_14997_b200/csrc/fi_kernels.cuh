@@ -287,6 +287,7 @@ struct SplitArgs {
   const float* root;
   const int* lengths;
   int B, lmax, N, Np, w, cols_per_cta;
+  int b0, nb;        // this launch's sentences [b0, b0 + nb)
 };
 
 struct SplitTerm {
@@ -344,7 +345,7 @@ __global__ void __launch_bounds__(288) k_split_fwd_bulk(SplitArgs a, int stages)
   const int w = a.w;
   const int nsplit = w - 1;
   const int n_w = a.lmax - w + 1;
-  const int local = blockIdx.y;
+  const int local = a.b0 * n_w + blockIdx.y;
   const int b = local / n_w, i = local % n_w;
   const int len = a.lengths[b];
   const long long row = rowbase(w, a.B, a.lmax) + local;
@@ -559,7 +560,7 @@ __global__ void __launch_bounds__(288, 3) k_split_fwd_pers(SplitArgs a, int stag
   const int w = a.w;
   const int nsplit = w - 1;
   const int n_w = a.lmax - w + 1;
-  const int nrows = a.B * n_w;
+  const int nrows = a.nb * n_w;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ncons = blockDim.x - 32;
   const int cpc = a.Np;  // one CTA per row
@@ -589,7 +590,8 @@ __global__ void __launch_bounds__(288, 3) k_split_fwd_pers(SplitArgs a, int stag
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     long long g0 = 0;  // stages used before this row (identical count in the consumers)
-    for (int local = blockIdx.x; local < nrows; local += gridDim.x) {
+    for (int kk = blockIdx.x; kk < nrows; kk += gridDim.x) {
+      const int local = a.b0 * n_w + kk;
       const int b = local / n_w, i = local % n_w;
       const bool dead = i + w > a.lengths[b];
       double ub = -1.0e300;
@@ -648,7 +650,8 @@ __global__ void __launch_bounds__(288, 3) k_split_fwd_pers(SplitArgs a, int stag
   const int ci = threadIdx.x - 32;
   const int col0 = ci * 4;
   long long g0 = 0;
-  for (int local = blockIdx.x; local < nrows; local += gridDim.x) {
+  for (int kk = blockIdx.x; kk < nrows; kk += gridDim.x) {
+      const int local = a.b0 * n_w + kk;
     const int b = local / n_w, i = local % n_w;
     const int len = a.lengths[b];
     const long long row = rowbase(w, a.B, a.lmax) + local;
@@ -821,6 +824,7 @@ struct GatherArgs {
   const int* lengths;
   const float* g;
   int B, lmax, Np, m, cols_per_cta;
+  int b0, nb;        // this launch's sentences [b0, b0 + nb)
 };
 
 struct GatherTerm {
@@ -836,7 +840,7 @@ __global__ void __launch_bounds__(288) k_gather_bwd_bulk(GatherArgs a, int stage
   extern __shared__ __align__(128) uint8_t dsm[];
   const int m = a.m;
   const int n_m = a.lmax - m + 1;
-  const int local = blockIdx.y;
+  const int local = a.b0 * n_m + blockIdx.y;
   const int b = local / n_m, i = local % n_m;
   const int len = a.lengths[b];
   const long long row = rowbase(m, a.B, a.lmax) + local;
