@@ -279,24 +279,51 @@ int num_sms() {
   return cached[dev] > 0 ? cached[dev] : 148;
 }
 
+// Hot-path launches go through cudaLaunchKernelEx with programmatic
+// dependent launch (PDL): a kernel may be scheduled while its predecessor
+// is still finishing, runs its prologue (barrier init, TMEM alloc, tensor
+// map prefetch), then blocks in griddepcontrol.wait until the predecessor's
+// writes are visible.  Persistent kernels trigger their dependents right
+// after their own wait (so the chain stays transitive); grid-stride ones
+// never trigger early.  FI_PDL=0 disables the attribute.
+bool use_pdl() {
+  static const int v = env_int("FI_PDL", 1);
+  return v != 0;
+}
+
 template <typename K, typename... Args>
-int launch_cluster(K kern, int cluster, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-                   Args... args) {
+int launch_ex(K kern, int cluster, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+              Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cluster;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  if (cluster > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = cluster;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  if (use_pdl()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = n;
   FI_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
   ++g_launches;
   return FI_OK;
+}
+
+template <typename K, typename... Args>
+int launch_cluster(K kern, int cluster, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                   Args... args) {
+  return launch_ex(kern, cluster, grid, block, smem, st, args...);
 }
 
 // GEMM smem ring depth for launches enqueued by this thread: 0 = the deepest
@@ -355,8 +382,7 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
     FI_TRY(launch_cluster(kern, 2, dim3(grid), dim3(256), smem_bytes, st, ta, tb, ta2, tb2,
                           sh, ep));
   } else {
-    kern<<<grid, 256, smem_bytes, st>>>(ta, tb, ta2, tb2, sh, ep);
-    ++g_launches;
+    FI_TRY(launch_ex(kern, 1, dim3(grid), dim3(256), smem_bytes, st, ta, tb, ta2, tb2, sh, ep));
   }
   FI_CUDA(cudaGetLastError());
   return FI_OK;
@@ -564,15 +590,14 @@ int forward_impl(const Plan& p, const float* L, const float* R, const float* roo
   {  // K1: exp of the child tables, once per call
     ProfScope prof(FI_PROF_PREP, st);
     FI_CUDA(cudaMemsetAsync(wsum, 0, 16, st));
-    k_prep_weights<T><<<2 * p.Np, 256, 0, st>>>(L, R, wnn, wnp, wsum, p.N, p.P, p.Np, p.Pp,
-                                                p.wnn_lo, p.wnp_lo);
-    ++g_launches;
+    FI_TRY(launch_ex(k_prep_weights<T>, 1, dim3(2 * p.Np), dim3(256), 0, st, L, R, wnn, wnp, wsum,
+                     p.N, p.P, p.Np, p.Pp, p.wnn_lo, p.wnp_lo));
     FI_CUDA(cudaGetLastError());
   }
   {
   ProfScope prof(FI_PROF_PREP, st);
-  k_prep_width1<T><<<p.B * p.l, 256, 0, st>>>(unary, lengths, e1, X, p.l, p.P, p.Pp, p.e1_lo);
-  ++g_launches;
+  FI_TRY(launch_ex(k_prep_width1<T>, 1, dim3(p.B * p.l), dim3(256), 0, st, unary, lengths, e1, X,
+                   p.l, p.P, p.Pp, p.e1_lo));
   FI_CUDA(cudaGetLastError());
   }
 
@@ -647,8 +672,7 @@ int forward_impl(const Plan& p, const float* L, const float* R, const float* roo
         FI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 + cons, smem));
         occ = occ < 1 ? 1 : occ;
         const int grid = nrows < occ * num_sms() ? nrows : occ * num_sms();
-        kern<<<grid, 32 + cons, smem, s>>>(sa, stages, nprod);
-        ++g_launches;
+        FI_TRY(launch_ex(kern, 1, dim3(grid), dim3(32 + cons), smem, s, sa, stages, nprod));
         FI_CUDA(cudaGetLastError());
         return FI_OK;
       });
@@ -712,10 +736,9 @@ int backward_impl(const Plan& p, const float* L, const float* R, const float* ro
   {
   ProfScope prof(FI_PROF_SEED, st);
   (void)logZ;  // the fp64-consistent log2 Z - x† (TOPZ) is used instead
-  k_seed_bwd<sizeof(CT) == 2><<<(p.Np + 255) / 256, 256, 0, st>>>(root, TOP, TOPZ, g, lengths, LQ,
-                                                                  LQS, droot, flag,
-                                                 p.B, p.l, p.N, p.Np);
-  ++g_launches;
+  FI_TRY(launch_ex(k_seed_bwd<sizeof(CT) == 2>, 1, dim3((p.Np + 255) / 256), dim3(256), 0, st,
+                   root, static_cast<const float*>(TOP), static_cast<const float*>(TOPZ), g,
+                   lengths, static_cast<void*>(LQ), LQS, droot, flag, p.B, p.l, p.N, p.Np));
   FI_CUDA(cudaGetLastError());
   }
 
@@ -758,11 +781,10 @@ int backward_impl(const Plan& p, const float* L, const float* R, const float* ro
       } else {
         FI_TRY(set_smem(k_gather_bwd_bulk<T, CT, V>, smem));
         static const int nprod = env_int("FI_GNPROD", 4);
-        k_gather_bwd_bulk<T, CT, V><<<grid, 32 + dc.threads, smem, s>>>(ga, stages, nprod);
-        return FI_OK;
+        return launch_ex(k_gather_bwd_bulk<T, CT, V>, 1, grid, dim3(32 + dc.threads), smem, s, ga,
+                         stages, nprod);
       }
     }));
-    ++g_launches;
     FI_CUDA(cudaGetLastError());
     return FI_OK;
   };

@@ -281,6 +281,8 @@ __global__ void __launch_bounds__(256, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tslot;
+  pdl_wait();     // operands written by the previous kernel are visible from here
+  pdl_trigger();  // persistent: every CTA is resident, so the next kernel may queue
 
   if (warp == 0) {
     if (lane == 0) {

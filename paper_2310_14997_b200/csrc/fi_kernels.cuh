@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(256) k_prep_weights(
     const float* __restrict__ L, const float* __restrict__ R, T* __restrict__ wnn,
     T* __restrict__ wnp, float* __restrict__ wsum, int N, int P, int Np, int Pp,
     long long wnn_lo, long long wnp_lo) {
+  pdl_wait();
   __shared__ float red[33];
   const int row = blockIdx.x;  // 0 .. 2Np-1
   const bool right = row >= Np;
@@ -195,6 +196,7 @@ __global__ void __launch_bounds__(256) k_prep_width1(const float* __restrict__ u
                                                      const int* __restrict__ lengths,
                                                      T* __restrict__ e1, double* __restrict__ X,
                                                      int lmax, int P, int Pp, long long e1_lo) {
+  pdl_wait();
   __shared__ float red[33];
   const int r = blockIdx.x;  // = b * lmax + i = chart_row(1, b, i)
   const int b = r / lmax, i = r % lmax;
@@ -337,6 +339,7 @@ __device__ __forceinline__ void ring_init(BulkRing& r, int consumer_warps) {
 
 template <typename T, typename CT, int V>
 __global__ void __launch_bounds__(288) k_split_fwd_bulk(SplitArgs a, int stages) {
+  pdl_wait();  // inputs of the previous kernel visible from here
   constexpr bool kHalf = sizeof(CT) == 2;
   extern __shared__ __align__(128) uint8_t dsm[];
   __shared__ float red[33];
@@ -582,6 +585,8 @@ __global__ void __launch_bounds__(288, 3) k_split_fwd_pers(SplitArgs a, int stag
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_wait();     // a / b / X of earlier widths are visible from here
+  pdl_trigger();  // persistent: the next kernel may queue behind this one
   const float lnn = a.wsum[0] > 0.f ? log2f(a.wsum[0]) : 0.f;
   const float rnn = a.wsum[1] > 0.f ? log2f(a.wsum[1]) : 0.f;
   const float lnp = a.wsum[2] > 0.f ? log2f(a.wsum[2]) : 0.f;
@@ -768,6 +773,7 @@ __global__ void k_seed_bwd(const float* __restrict__ root, const float* __restri
                            const int* __restrict__ lengths, void* __restrict__ LQv,
                            float* __restrict__ LQS, float* __restrict__ droot,
                            int* __restrict__ flag, int B, int lmax, int N, int Np) {
+  pdl_wait();
   // blockDim is a multiple of 32 and Np of 256: each warp owns one 32-column chunk
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= Np) return;
@@ -835,6 +841,7 @@ struct GatherTerm {
 
 template <typename T, typename CT, int V>
 __global__ void __launch_bounds__(288) k_gather_bwd_bulk(GatherArgs a, int stages, int nprod) {
+  pdl_wait();  // inputs of the previous kernel visible from here
   constexpr bool kHalf = sizeof(CT) == 2;
   nprod = nprod < 1 ? 1 : (nprod > stages ? stages : (nprod > 32 ? 32 : nprod));
   extern __shared__ __align__(128) uint8_t dsm[];

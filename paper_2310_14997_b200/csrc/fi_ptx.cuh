@@ -134,6 +134,15 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 }
 
 
+// ------------------------------------------- programmatic dependent launch
+// Block until the predecessor grid (PDL launch) has completed and its writes
+// are visible; a no-op for a normally launched kernel.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Let the stream's next (PDL-launched) kernel be scheduled.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ------------------------------------------------------------ CTA pairs
 // cta_group::2 variants: a cluster of two CTAs on one TPC runs one MMA with
 // M = 256 (128 accumulator rows in each CTA's TMEM) whose B operand is split
