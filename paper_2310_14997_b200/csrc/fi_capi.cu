@@ -102,6 +102,8 @@ int set_err(int code, const char* fmt, ...) {
     if (r_ != FI_OK) return r_; \
   } while (0)
 
+constexpr long long kKPartRows = 4096;  // split-K partials: ksplit x M <= this (times the GEMM's N)
+
 // ------------------------------------------------------------------ layout
 struct Decomp {
   int clusters, threads, v, cols_per_cta, stages;
@@ -111,7 +113,7 @@ struct Plan {
   int N, P, B, l, Np, Pp, esz;
   Decomp dsplit, dgather;
   long long rows;
-  size_t wnn, wnp, e1, eall, gall, a, b, o, lq, lqs, x, top, topz, wsum, flag, total;
+  size_t wnn, wnp, e1, eall, gall, a, b, o, lq, lqs, x, top, topz, wsum, flag, kpart, total;
   // element offsets of the lo planes of the GEMM operands (fp32 mode only)
   long long wnn_lo, wnp_lo, e1_lo, eall_lo, gall_lo;
   bool store_o, tf32, split, half_chart;
@@ -217,6 +219,7 @@ int make_plan(const fi_shape* s, Plan* p) {
   p->topz = take(4ull * p->B);
   p->wsum = take(16);
   p->flag = take(256);
+  p->kpart = take(4ull * kKPartRows * 2 * p->Np);  // split-K partials (<= ksplit x M x 2Np)
   p->total = off;
   return FI_OK;
 }
@@ -326,6 +329,23 @@ int launch_cluster(K kern, int cluster, dim3 grid, dim3 block, size_t smem, cuda
   return launch_ex(kern, cluster, grid, block, smem, st, args...);
 }
 
+// Split-K partial tiles of the GEMMs enqueued by this thread (a workspace
+// region set by the ABI entry points; thread-local, so calls on different
+// threads / streams never share it).  Null: no split-K.
+struct KPartScratch {
+  float* ptr = nullptr;
+  size_t floats = 0;
+};
+thread_local KPartScratch g_kpart;
+struct KPartScope {
+  KPartScratch saved;
+  KPartScope(float* p, size_t n) : saved(g_kpart) {
+    g_kpart.ptr = p;
+    g_kpart.floats = n;
+  }
+  ~KPartScope() { g_kpart = saved; }
+};
+
 // GEMM smem ring depth for launches enqueued by this thread: 0 = the deepest
 // ring that fits (one CTA per SM); the dual-stream sweep (see forward_impl)
 // caps it so a bandwidth-kernel CTA can share each SM with a GEMM CTA.
@@ -333,7 +353,7 @@ thread_local int g_gemm_stages = 0;
 
 template <typename T, int BN, bool AMN, bool BMN, int EPI, bool SPLIT, int CHUNK, bool PAIR>
 int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_row0,
-                const GemmEpi& ep, cudaStream_t st, int bn) {
+                const GemmEpi& ep, cudaStream_t st, int bn, int ksplit) {
   using Cf = GemmCfg<T, BN>;
   constexpr int NCTA = PAIR ? 2 : 1;
   CUtensorMap ta, tb, ta2, tb2;
@@ -359,6 +379,13 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
   sh.bn = bn;
   sh.stages = (g_gemm_stages > 1 && g_gemm_stages < Cf::STAGES) ? g_gemm_stages : Cf::STAGES;
   const size_t smem_bytes = static_cast<size_t>(sh.stages) * Cf::STAGE_BYTES + 1024 + 256;
+  sh.ksplit = 1;
+  sh.part = nullptr;
+  if (ksplit > 1 && CHUNK == 0 && g_kpart.ptr &&
+      static_cast<size_t>(ksplit) * M * N <= g_kpart.floats) {
+    sh.ksplit = ksplit;
+    sh.part = g_kpart.ptr;
+  }
   sh.num_m = (M + Cf::BM * NCTA - 1) / (Cf::BM * NCTA);
   sh.num_n = (N + bn - 1) / bn;
   sh.num_k = (K + Cf::BK - 1) / Cf::BK;
@@ -373,7 +400,8 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
     attr_done[dev & 63] = true;
   }
   const int slots = num_sms() / NCTA;  // persistent: one CTA (pair) per SM (pair)
-  const int grid = (tiles < slots ? tiles : slots) * NCTA;
+  const int units = tiles * sh.ksplit;
+  const int grid = (units < slots ? units : slots) * NCTA;
   if (grid <= 0) return FI_OK;
   ProfScope prof(EPI == EPI_FWD || EPI == EPI_FWD_H ? FI_PROF_GEMM_FWD
                  : EPI == EPI_WGRAD ? FI_PROF_GEMM_WGRAD
@@ -385,6 +413,12 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
     FI_TRY(launch_ex(kern, 1, dim3(grid), dim3(256), smem_bytes, st, ta, tb, ta2, tb2, sh, ep));
   }
   FI_CUDA(cudaGetLastError());
+  if (sh.ksplit > 1) {  // sum the partials in order and run the epilogue
+    const long long chunks = static_cast<long long>(M) * (N / 32);
+    FI_TRY(launch_ex(k_gemm_fixup<EPI>, 1, dim3(static_cast<unsigned>((chunks + 255) / 256)),
+                     dim3(256), 0, st, static_cast<const float*>(sh.part), sh.ksplit, M, N, ep));
+    FI_CUDA(cudaGetLastError());
+  }
   return FI_OK;
 }
 
@@ -407,17 +441,20 @@ int gemm_env(const char* name, int dflt) {
 struct GemmChoice {
   int bn;
   bool pair;
+  int ksplit;
 };
 
 double gemm_t_single(int bn) { return 0.77 + 0.23 * bn / 256.0; }
 double gemm_t_pair(int bn) { return 0.56 + 0.20 * bn / 256.0; }
 
 GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int step_single,
-                       int step_pair) {
+                       int step_pair, bool allow_ksplit) {
   static const int force_pair = gemm_env("FI_GEMM_PAIR", -1);
   static const int force_bn = gemm_env("FI_GEMM_BN", 0);
-  GemmChoice best{0, false};
-  double best_cost = 1e300;
+  static const int force_ks = gemm_env("FI_GEMM_KSPLIT", 0);  // 1: never split K
+  GemmChoice best{0, false, 1};
+  double best_cost = 1e300;  // microseconds
+  const double us_per_kiter = 0.55;  // one 128 x 256 bf16 k-iteration on one SM (measured)
   for (int pair = 0; pair < 2; ++pair) {
     if (force_pair >= 0 && pair != force_pair) continue;
     const int step = pair ? step_pair : step_single;
@@ -426,11 +463,24 @@ GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int step_sin
     for (int bn = bn_max / step * step; bn >= 64 && bn >= step; bn -= step) {
       if (force_bn && bn != force_bn) continue;
       const long long T = mt * ((N + bn - 1) / bn);
-      const double t = pair ? gemm_t_pair(bn) : gemm_t_single(bn);
-      const double cost = static_cast<double>((T + slots - 1) / slots) * k_iters * t;
-      if (cost < best_cost * 0.995) {
-        best_cost = cost;
-        best = {bn, pair != 0};
+      const double t = us_per_kiter * (pair ? gemm_t_pair(bn) : gemm_t_single(bn));
+      auto feasible = [&](int ks) {
+        return ks == 1 || (allow_ksplit && force_ks != 1 && T * ks <= slots && k_iters / ks >= 4 &&
+                           static_cast<double>(ks) * M * N <= static_cast<double>(g_kpart.floats));
+      };
+      const bool forced = force_ks > 1 && feasible(force_ks);
+      for (int ks = 1; ks <= 8; ++ks) {
+        if (!feasible(ks)) break;
+        if (forced && ks != force_ks) continue;
+        const long long units = T * ks;
+        double cost = static_cast<double>((units + slots - 1) / slots) *
+                      ((k_iters + ks - 1) / ks) * t;
+        if (ks > 1)  // partial write + fixup read (~5 TB/s) + the fixup launch
+          cost += 4.0 + 2.0 * ks * static_cast<double>(M) * N * 4.0 / 5.0e6;
+        if (cost < best_cost * 0.995) {
+          best_cost = cost;
+          best = {bn, pair != 0, ks};
+        }
       }
     }
   }
@@ -452,13 +502,13 @@ int run_gemm_s(const Operand& A, const Operand& B, int M, int N, int K, int a_ro
   // MN-major B is staged in whole 128-B atoms per CTA
   const int step1 = BMN ? (ATOM > 32 ? ATOM : 32) : 32;
   const int step2 = BMN ? 2 * ATOM : 32;
-  const GemmChoice c = choose_gemm(M, N, k_iters, kBnMax, step1, step2);
+  const GemmChoice c = choose_gemm(M, N, k_iters, kBnMax, step1, step2, kChunk == 0);
   if (c.bn == 0) return set_err(FI_ERR_ARG, "no GEMM tile for N=%d (FI_GEMM_BN?)", N);
   if (c.pair)
     return launch_gemm<T, kBnMax, AMN, BMN, EPI, SPLIT, kChunk, true>(A, B, M, N, K, a_row0, ep,
-                                                                      st, c.bn);
+                                                                      st, c.bn, c.ksplit);
   return launch_gemm<T, kBnMax, AMN, BMN, EPI, SPLIT, kChunk, false>(A, B, M, N, K, a_row0, ep,
-                                                                     st, c.bn);
+                                                                     st, c.bn, c.ksplit);
 }
 
 // Dispatch on the split (fp32 / bf16x3) mode; tf32 operands are never split.
@@ -910,6 +960,7 @@ int fi_inside_forward(const fi_shape* shape, const float* L, const float* R, con
   FI_TRY(check_ptrs({L, R, root, unary, lengths, log_z, ws}));
   FI_TRY(load_encode());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  KPartScope kps(at<float>(ws, p.kpart), static_cast<size_t>(kKPartRows) * 2 * p.Np);
   if (p.tf32) {
     if (p.half_chart) return forward_impl<float, __half>(p, L, R, root, unary, lengths, log_z, ws, st);
     return forward_impl<float, float>(p, L, R, root, unary, lengths, log_z, ws, st);
@@ -928,6 +979,7 @@ int fi_inside_backward(const fi_shape* shape, const float* L, const float* R, co
   FI_TRY(check_ptrs({L, R, root, unary, lengths, log_z, grad_log_z, dL, dR, droot, dunary, ws}));
   FI_TRY(load_encode());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  KPartScope kps(at<float>(ws, p.kpart), static_cast<size_t>(kKPartRows) * 2 * p.Np);
 #define FI_BWD(T, CT)                                                                      \
   return backward_impl<T, CT>(p, L, R, root, unary, lengths, log_z, grad_log_z, dL, dR, droot, \
                               dunary, ws, st)
@@ -1030,6 +1082,15 @@ int fi_test_gemm(int32_t dtype, int32_t a_mn, int32_t b_mn, int32_t M, int32_t N
   if (M < 1 || N < 64 || N % 64 || K < 1)
     return set_err(FI_ERR_ARG, "test GEMM needs M>=1, N%%64==0, K>=1");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t kfloats = 8ull * M * N;  // room for any split-K the chooser picks
+  void* scratch = nullptr;
+  FI_CUDA(cudaMallocAsync(&scratch, kfloats * 4, st));
+  struct Free {
+    void* p;
+    cudaStream_t s;
+    ~Free() { cudaFreeAsync(p, s); }
+  } free_scratch{scratch, st};
+  KPartScope kps(static_cast<float*>(scratch), kfloats);
   GemmEpi ep = {};
   ep.M = M;
   ep.C = C;

@@ -45,6 +45,12 @@ struct GemmShape {
   int num_m, num_n, num_k;  // tiles of (128 or 256 for pairs) x bn x BK
   int bn;         // N tile (runtime, <= the kernel's BN bound, multiple of 32)
   int stages;     // smem ring depth (runtime, <= GemmCfg::STAGES)
+  // split-K (ksplit > 1, small M): work unit u = (tile u / ksplit, K part
+  // u % ksplit); each unit stores its raw fp32 partial tile at
+  // part[(kpart * M + row) * N + col] and k_gemm_fixup sums the parts in
+  // order (deterministic) and applies the epilogue.
+  int ksplit;
+  float* part;
 };
 
 struct GemmEpi {
@@ -215,6 +221,82 @@ __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int lrow, long long
   }
 }
 
+// Per-row epilogue state: where row `lrow` of this GEMM goes and what the
+// fused transform needs (shared by the GEMM epilogue and the split-K fixup).
+struct EpiRow {
+  float* rowptr;    // row base (EPI_FWD/_H: the a row)
+  float* rowptr_b;  // EPI_FWD/_H: the b row
+  long long grow;   // global chart row
+  float xv;
+  int aux, erow;
+  bool ok;
+};
+
+template <int EPI>
+__device__ __forceinline__ EpiRow epi_row(const GemmEpi& ep, int lrow) {
+  EpiRow r;
+  r.grow = ep.row0 + lrow;
+  r.xv = 0.f;
+  r.aux = 0;
+  r.rowptr = nullptr;
+  r.rowptr_b = nullptr;
+  const bool row_ok = lrow < ep.M;
+  const long long grow = r.grow;
+  if (row_ok) {
+    if constexpr (EPI == EPI_FWD) {
+      r.rowptr = ep.outA + grow * ep.Np;
+      r.rowptr_b = ep.outB + grow * ep.Np;
+    } else if constexpr (EPI == EPI_FWD_H) {
+      r.rowptr = reinterpret_cast<float*>(reinterpret_cast<__half*>(ep.outA) + grow * ep.Np);
+      r.rowptr_b = reinterpret_cast<float*>(reinterpret_cast<__half*>(ep.outB) + grow * ep.Np);
+    } else if constexpr (EPI == EPI_DGRAD) {
+      r.rowptr = ep.LQ + grow * ep.Np;
+    } else if constexpr (EPI == EPI_DGRAD_H) {
+      r.rowptr = reinterpret_cast<float*>(reinterpret_cast<__half*>(ep.LQ) + grow * ep.Np);
+    } else if constexpr (EPI == EPI_DUNARY) {
+      // width-1 rows: grow = b * lmax + i (rowbase(1) = 0)
+      r.xv = static_cast<float>(ep.X[grow]);
+      const int b = static_cast<int>(grow / ep.lmax), i = static_cast<int>(grow % ep.lmax);
+      r.aux = i < ep.lengths[b];
+      r.rowptr = ep.dunary + grow * ep.P;
+    } else if constexpr (EPI == EPI_WGRAD) {
+      r.aux = lrow >= ep.Np;  // 0 -> left table, 1 -> right table
+      const int arow = r.aux ? lrow - ep.Np : lrow;
+      r.rowptr = (r.aux ? ep.dR : ep.dL) + static_cast<long long>(arow) * ep.ld_lr;
+      if (arow >= ep.n_nt) r.rowptr = nullptr;
+    } else {
+      r.rowptr = ep.C + static_cast<long long>(lrow) * ep.ldc;
+    }
+  }
+  r.ok = row_ok && r.rowptr != nullptr;
+  if constexpr (EPI == EPI_DGRAD || EPI == EPI_DGRAD_H) {
+    // the seed kernel owns the top span of each sentence (inside.py:400-404)
+    if (r.ok) {
+      const int b = ep.b0 + lrow / ep.n_w, i = lrow % ep.n_w;
+      if (i == 0 && ep.lengths[b] == ep.width) r.ok = false;
+    }
+  }
+  r.erow = (EPI == EPI_WGRAD && r.aux) ? lrow - ep.Np
+           : EPI == EPI_DUNARY ? static_cast<int>(grow) : lrow;
+  return r;
+}
+
+// Epilogue of one 32-column chunk starting at GEMM column `col` (skips the N
+// tail; the forward's [a | b] columns split at Np, possibly inside a tile).
+template <int EPI>
+__device__ __forceinline__ void epi_emit(const GemmEpi& ep, const EpiRow& r, int col, int N,
+                                         const float (&v)[32]) {
+  if (col >= N) return;
+  float* rp = r.rowptr;
+  if constexpr (EPI == EPI_FWD || EPI == EPI_FWD_H) {
+    if (col >= ep.Np) {
+      col -= ep.Np;
+      rp = r.rowptr_b;
+    }
+  }
+  epi_chunk<EPI>(ep, r.erow, r.grow, col, v, r.xv, r.ok, rp, r.aux);
+}
+
 // SPLIT (fp32 mode, bf16x3): each operand is stored as hi + lo bf16 planes
 // (x = hi + lo to ~2^-17 relative) and the K loop runs three passes,
 // lo*hi, hi*lo, then hi*hi (small terms first), into the same accumulator.
@@ -249,6 +331,8 @@ __global__ void __launch_bounds__(256, 1)
   const int lane = threadIdx.x & 31;
   const int num_tiles = sh.num_m * sh.num_n;
   const int k_iters = SPLIT ? 3 * sh.num_k : sh.num_k;
+  const int ks = sh.ksplit > 1 ? sh.ksplit : 1;
+  const int nunits = num_tiles * ks;
   const int bn = sh.bn;                       // runtime N tile <= BN
   const int bn_cta = bn / NCTA;               // B rows staged by this CTA
   const uint32_t rank = PAIR ? cluster_rank() : 0;
@@ -290,12 +374,14 @@ __global__ void __launch_bounds__(256, 1)
       int stage = 0;
       uint32_t phase = 0;
       const uint32_t stage_tx = NCTA * (C::A_BYTES + bn_cta * 128);
-      for (int tile = tile0; tile < num_tiles; tile += tstep) {
+      for (int u = tile0; u < nunits; u += tstep) {
+        const int tile = u / ks, kpart = u - tile * ks;
+        const int k0 = k_iters * kpart / ks, k1 = k_iters * (kpart + 1) / ks;
         const int m_blk = tile % sh.num_m;
         const int n_blk = tile / sh.num_m;
         const int m0 = m_blk * (C::BM * NCTA) + rank * C::BM;  // this CTA's A rows
         const int n0 = n_blk * bn + rank * bn_cta;              // this CTA's B rows
-        for (int it = 0; it < k_iters; ++it) {
+        for (int it = k0; it < k1; ++it) {
           const int pass = SPLIT ? it / sh.num_k : 0;
           const int kb = SPLIT ? it - pass * sh.num_k : it;
           const CUtensorMap* ma = (SPLIT && pass == 0) ? &tmA2 : &tmA;
@@ -352,11 +438,13 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      const int cl = CHUNK > 0 ? CHUNK : k_iters;
-      for (int tile = tile0; tile < num_tiles; tile += tstep) {
+      for (int u = tile0; u < nunits; u += tstep) {
+        const int kpart = u % ks;
+        const int k0 = k_iters * kpart / ks, k1 = k_iters * (kpart + 1) / ks;
+        const int cl = CHUNK > 0 ? CHUNK : k1 - k0;
         uint32_t d_tmem = tmem_base;
-        for (int kb = 0; kb < k_iters; ++kb) {
-          const int kc = kb % cl;
+        for (int kb = k0; kb < k1; ++kb) {
+          const int kc = (kb - k0) % cl;
           if (kc == 0) {  // start a chunk in a drained accumulator
             mbar_wait(&tempty[acc], acc_phase ^ 1);
             tc_fence_after();
@@ -379,7 +467,7 @@ __global__ void __launch_bounds__(256, 1)
             stage = 0;
             phase ^= 1;
           }
-          if (kc == cl - 1 || kb == k_iters - 1) {
+          if (kc == cl - 1 || kb == k1 - 1) {
             if constexpr (PAIR) umma_commit2(&tfull[acc]);
             else umma_commit(&tfull[acc]);
             acc ^= 1;
@@ -406,66 +494,26 @@ __global__ void __launch_bounds__(256, 1)
         else mbar_arrive(&tempty[a]);
       }
     };
-    for (int tile = tile0; tile < num_tiles; tile += tstep) {
+    for (int u = tile0; u < nunits; u += tstep) {
+      const int tile = u / ks, kpart = u - tile * ks;
+      const int k0 = k_iters * kpart / ks, k1 = k_iters * (kpart + 1) / ks;
       const int m_blk = tile % sh.num_m;
       const int n_blk = tile / sh.num_m;
       const int lrow = m_blk * (C::BM * NCTA) + rank * C::BM + r;  // row within this GEMM
-      const long long grow = ep.row0 + lrow;
-      const bool row_ok = lrow < ep.M;
-      float xv = 0.f;
-      float* rowptr = nullptr;  // row base (EPI_FWD/_H: the a row; b row below)
-      float* rowptr_b = nullptr;
-      int aux = 0;
+      const EpiRow er = epi_row<EPI>(ep, lrow);
       const int col_base = n_blk * bn;
-      if (row_ok) {
-        if constexpr (EPI == EPI_FWD) {
-          rowptr = ep.outA + grow * ep.Np;
-          rowptr_b = ep.outB + grow * ep.Np;
-        } else if constexpr (EPI == EPI_FWD_H) {
-          rowptr = reinterpret_cast<float*>(reinterpret_cast<__half*>(ep.outA) + grow * ep.Np);
-          rowptr_b = reinterpret_cast<float*>(reinterpret_cast<__half*>(ep.outB) + grow * ep.Np);
-        } else if constexpr (EPI == EPI_DGRAD) {
-          rowptr = ep.LQ + grow * ep.Np;
-        } else if constexpr (EPI == EPI_DGRAD_H) {
-          rowptr = reinterpret_cast<float*>(reinterpret_cast<__half*>(ep.LQ) + grow * ep.Np);
-        } else if constexpr (EPI == EPI_DUNARY) {
-          // width-1 rows: grow = b * lmax + i (rowbase(1) = 0)
-          xv = static_cast<float>(ep.X[grow]);
-          const int b = static_cast<int>(grow / ep.lmax), i = static_cast<int>(grow % ep.lmax);
-          aux = i < ep.lengths[b];
-          rowptr = ep.dunary + grow * ep.P;
-        } else if constexpr (EPI == EPI_WGRAD) {
-          aux = lrow >= ep.Np;  // 0 -> left table, 1 -> right table
-          const int arow = aux ? lrow - ep.Np : lrow;
-          rowptr = (aux ? ep.dR : ep.dL) + static_cast<long long>(arow) * ep.ld_lr;
-          if (arow >= ep.n_nt) rowptr = nullptr;
-        } else {
-          rowptr = ep.C + static_cast<long long>(lrow) * ep.ldc;
-        }
-      }
-      bool ok = row_ok && rowptr != nullptr;
-      if constexpr (EPI == EPI_DGRAD || EPI == EPI_DGRAD_H) {
-        // the seed kernel owns the top span of each sentence (inside.py:400-404)
-        if (ok) {
-          const int b = ep.b0 + lrow / ep.n_w, i = lrow % ep.n_w;
-          if (i == 0 && ep.lengths[b] == ep.width) ok = false;
-        }
-      }
-      const int erow = (EPI == EPI_WGRAD && aux) ? lrow - ep.Np
-                       : EPI == EPI_DUNARY ? static_cast<int>(grow) : lrow;
-      // epilogue of one 32-column chunk j of this tile (skips the N tail; the
-      // forward's [a | b] columns split at Np, possibly inside a tile)
       auto emit = [&](int j, const float (&v)[32]) {
-        int col = col_base + j * 32;
-        if (col >= sh.N) return;
-        float* rp = rowptr;
-        if constexpr (EPI == EPI_FWD || EPI == EPI_FWD_H) {
-          if (col >= ep.Np) {
-            col -= ep.Np;
-            rp = rowptr_b;
-          }
+        if (ks > 1) {  // split-K: raw fp32 partial, summed + transformed by k_gemm_fixup
+          const int col = col_base + j * 32;
+          if (col >= sh.N || lrow >= ep.M) return;
+          float4* dst = reinterpret_cast<float4*>(
+              sh.part + (static_cast<long long>(kpart) * ep.M + lrow) * sh.N + col);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          return;
         }
-        epi_chunk<EPI>(ep, erow, grow, col, v, xv, ok, rp, aux);
+        epi_emit<EPI>(ep, er, col_base + j * 32, sh.N, v);
       };
       const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
       if constexpr (CHUNK == 0) {
@@ -488,7 +536,7 @@ __global__ void __launch_bounds__(256, 1)
         for (int j = 0; j < BN / 32; ++j)
 #pragma unroll
           for (int t = 0; t < 32; ++t) sum[j][t] = 0.f;
-        const int nchunks = (k_iters + CHUNK - 1) / CHUNK;
+        const int nchunks = (k1 - k0 + CHUNK - 1) / CHUNK;
         for (int c = 0; c < nchunks; ++c) {
           mbar_wait(&tfull[acc], acc_phase);
           tc_fence_after();
@@ -521,6 +569,35 @@ __global__ void __launch_bounds__(256, 1)
     if constexpr (PAIR) tmem_dealloc2<C::TMEM_COLS>(tmem_base);
     else tmem_dealloc<C::TMEM_COLS>(tmem_base);
   }
+}
+
+// Split-K fixup: sum the ksplit raw partials of every (row, 32-column chunk)
+// in part order and run the launch's epilogue.  One thread per chunk.
+template <int EPI>
+__global__ void __launch_bounds__(256) k_gemm_fixup(const float* __restrict__ part, int ksplit,
+                                                    int M, int N, GemmEpi ep) {
+  pdl_wait();
+  const int nch = N / 32;
+  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= static_cast<long long>(M) * nch) return;
+  const int lrow = static_cast<int>(t / nch), col = static_cast<int>(t % nch) * 32;
+  float v[32];
+#pragma unroll
+  for (int q = 0; q < 32; ++q) v[q] = 0.f;
+  for (int k = 0; k < ksplit; ++k) {
+    const float4* src =
+        reinterpret_cast<const float4*>(part + (static_cast<long long>(k) * M + lrow) * N + col);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 w = __ldcg(src + q);
+      v[4 * q] += w.x;
+      v[4 * q + 1] += w.y;
+      v[4 * q + 2] += w.z;
+      v[4 * q + 3] += w.w;
+    }
+  }
+  const EpiRow er = epi_row<EPI>(ep, lrow);
+  epi_emit<EPI>(ep, er, col, N, v);
 }
 
 }  // namespace fi
