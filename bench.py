@@ -306,6 +306,23 @@ def roofline_block(prof: dict, steps: int, n: int, batch: int, length: int, esz:
             "per_class": per_class}
 
 
+def init_dist(world: int, local: int):
+    """One process per GPU over NCCL (FI_DIST_BACKEND=gloo with ranks sharing
+    devices exercises the multi-rank code path on a single-GPU box)."""
+    import torch
+    import torch.distributed as dist
+    backend = os.environ.get("FI_DIST_BACKEND", "nccl")
+    dev_idx = local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(dev_idx)
+    dev = torch.device("cuda", dev_idx)
+    if world > 1:
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    return dev
+
+
 # -------------------------------------------------------------- our arm
 def run_ours(args, world, rank, local):
     import torch
@@ -314,10 +331,7 @@ def run_ours(args, world, rank, local):
     from paper_2310_14997_b200.grammar import GrammarDims, random_grammar
     from paper_2310_14997_b200.ops import inside
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    dev = init_dist(world, local)
     cfg = CONFIGS[args.config]
     n, length = cfg["n"], cfg["length"]
     batch = args.batch or cfg["batch"]
@@ -458,10 +472,7 @@ def run_train(args, world, rank, local):
     from paper_2310_14997_b200 import _lib, neural
     from paper_2310_14997_b200.grammar import GrammarDims
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    dev = init_dist(world, local)
     cfg = CONFIGS[args.config]
     n, length = cfg["n"], cfg["length"]
     batch = args.batch or cfg["batch"]
