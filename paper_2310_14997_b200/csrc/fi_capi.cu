@@ -24,6 +24,11 @@
 #include <cudaTypedefs.h>
 
 #include "../../include/flashinside.h"
+#ifndef FI_FP32_CHUNK
+#define FI_FP32_CHUNK 16  // fp32 mode: K-iterations per round-to-nearest accumulation chunk
+                          // (8 / 16 / 32 measured: worst config-2 error 2.0e-6 / 2.5e-6 /
+                          // 1.1e-5 of the 1e-4 bound, 54.3 / 52.9 / 52.6 ms at config 3)
+#endif
 #include "fi_gemm.cuh"
 #include "fi_kernels.cuh"
 #include "fi_decode.cuh"
@@ -498,7 +503,7 @@ int run_gemm_s(const Operand& A, const Operand& B, int M, int N, int K, int a_ro
   // fp32 mode: chunked round-to-nearest accumulation (8 K-iterations per
   // TMEM chunk) to bound the tensor-core truncation bias; N tile <= 128.
   constexpr int kBnMax = SPLIT ? 128 : 256;
-  constexpr int kChunk = SPLIT ? 8 : 0;
+  constexpr int kChunk = SPLIT ? FI_FP32_CHUNK : 0;
   // MN-major B is staged in whole 128-B atoms per CTA
   const int step1 = BMN ? (ATOM > 32 ? ATOM : 32) : 32;
   const int step2 = BMN ? 2 * ATOM : 32;
