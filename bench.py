@@ -333,7 +333,7 @@ def run_ours(args, world, rank, local):
 
     dev = init_dist(world, local)
     cfg = CONFIGS[args.config]
-    n, length = cfg["n"], cfg["length"]
+    n, length = cfg["n"], args.length or cfg["length"]
     batch = args.batch or cfg["batch"]
     if args.scaling == "strong":
         if batch % world:
@@ -474,7 +474,7 @@ def run_train(args, world, rank, local):
 
     dev = init_dist(world, local)
     cfg = CONFIGS[args.config]
-    n, length = cfg["n"], cfg["length"]
+    n, length = cfg["n"], args.length or cfg["length"]
     batch = args.batch or cfg["batch"]
     dims = GrammarDims(n, n, VOCAB)
     ts = neural.TrainStep(neural.init_params(dims, 512, 0, device=dev),
@@ -577,7 +577,7 @@ def run_reference(args, world, rank):
     except ImportError:
         pass
     cfg = CONFIGS[args.config]
-    n, length = cfg["n"], cfg["length"]
+    n, length = cfg["n"], args.length or cfg["length"]
     g = random_grammar(GrammarDims(n, n, VOCAB), seed=0)
     rng = np.random.default_rng(1)
     sample = 1  # sentences per step: a bounded sample of the batch
@@ -617,6 +617,8 @@ def main(argv=None):
     ap.add_argument("--workload", choices=["inside", "train"], default="inside",
                     help="inside: the op's fwd+bwd (headline); train: the full GPU training step")
     ap.add_argument("--config", type=int, choices=sorted(CONFIGS), default=3)
+    ap.add_argument("--length", type=int, default=None,
+                    help="sentence length override (config 4: the 10..60 sweep at |N|=4096)")
     ap.add_argument("--batch", type=int, default=None, help="sentences per GPU (weak) / "
                     "global (strong); default: the config's batch")
     ap.add_argument("--gemm-dtype", choices=["bf16", "tf32", "fp32"], default="bf16")
