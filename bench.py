@@ -382,6 +382,25 @@ def run_ours(args, world, rank, local):
     for _ in range(args.warmup):
         step(L, R, root, unary)
     barrier()
+    graph, graph_launches = None, 0
+    use_graph = args.graph == 1 or (args.graph < 0 and world == 1)
+    if use_graph and (world == 1 or os.environ.get("FI_DIST_BACKEND", "nccl") == "nccl"):
+        # one fwd+bwd(+all-reduce) step captured as a CUDA graph and replayed:
+        # the ~160 dependent launches of a step become one graph launch
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            for _ in range(2):
+                step(L, R, root, unary)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        c0 = lib.fi_launch_count()
+        with torch.cuda.graph(graph):
+            g_out = step(L, R, root, unary)
+        graph_launches = int(lib.fi_launch_count() - c0)
+        for _ in range(2):
+            graph.replay()
+        barrier()
     clocks = ClockSampler(local)
     clocks.start()
     launch0 = lib.fi_launch_count()
@@ -389,12 +408,19 @@ def run_ours(args, world, rank, local):
     barrier()
     e0.record()
     for _ in range(args.steps):
-        _, loss, *_ = step(L, R, root, unary)
+        if graph is not None:
+            graph.replay()
+        else:
+            _, loss, *_ = step(L, R, root, unary)
     e1.record()
     barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
-    gpu_launches = int(lib.fi_launch_count() - launch0)
+    if graph is not None:
+        loss = g_out[1]
+        gpu_launches = graph_launches * args.steps
+    else:
+        gpu_launches = int(lib.fi_launch_count() - launch0)
     loss_val = float(loss.item())
     if world > 1:
         t = torch.tensor([ms], device=dev)
@@ -444,6 +470,7 @@ def run_ours(args, world, rank, local):
                        "n_nt": n, "n_pt": n, "length": length, "batch_per_gpu": batch,
                        "global_batch": batch * world, "gemm_dtype": args.gemm_dtype,
                        "chart_dtype": "fp16" if chart_esz == 2 else "fp32",
+                       "launch": "cuda-graph replay" if graph is not None else "eager",
                        "parallelism": f"dp{world}",
                        "l2": "working set ~4 GB chart per step >> 126 MB L2 (no flush needed)"},
             "clocks": clk,
@@ -624,6 +651,9 @@ def main(argv=None):
     ap.add_argument("--gemm-dtype", choices=["bf16", "tf32", "fp32"], default="bf16")
     ap.add_argument("--chart-dtype", choices=["auto", "fp32", "fp16"], default="auto")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--graph", type=int, default=-1,
+                    help="1: time CUDA-graph replays of the captured step; 0: eager launches; "
+                         "-1 (default): graphs on one GPU, eager under torchrun")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)
