@@ -107,7 +107,9 @@ int set_err(int code, const char* fmt, ...) {
     if (r_ != FI_OK) return r_; \
   } while (0)
 
-constexpr long long kKPartRows = 4096;  // split-K partials: ksplit x M <= this (times the GEMM's N)
+// split-K partial tiles: ksplit x split tiles <= the CTA slots, so at most
+// one (256 x 256 or 128 x 256) fp32 tile per slot
+constexpr long long kKPartFloats = 160LL * 256 * 256;
 
 // ------------------------------------------------------------------ layout
 struct Decomp {
@@ -224,7 +226,7 @@ int make_plan(const fi_shape* s, Plan* p) {
   p->topz = take(4ull * p->B);
   p->wsum = take(16);
   p->flag = take(256);
-  p->kpart = take(4ull * kKPartRows * 2 * p->Np);  // split-K partials (<= ksplit x M x 2Np)
+  p->kpart = take(4ull * kKPartFloats);  // split-K partial tiles
   p->total = off;
   return FI_OK;
 }
@@ -358,7 +360,7 @@ thread_local int g_gemm_stages = 0;
 
 template <typename T, int BN, bool AMN, bool BMN, int EPI, bool SPLIT, int CHUNK, bool PAIR>
 int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_row0,
-                const GemmEpi& ep, cudaStream_t st, int bn, int ksplit) {
+                const GemmEpi& ep, cudaStream_t st, int bn, int ksplit, int tail) {
   using Cf = GemmCfg<T, BN>;
   constexpr int NCTA = PAIR ? 2 : 1;
   CUtensorMap ta, tb, ta2, tb2;
@@ -384,17 +386,23 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
   sh.bn = bn;
   sh.stages = (g_gemm_stages > 1 && g_gemm_stages < Cf::STAGES) ? g_gemm_stages : Cf::STAGES;
   const size_t smem_bytes = static_cast<size_t>(sh.stages) * Cf::STAGE_BYTES + 1024 + 256;
-  sh.ksplit = 1;
-  sh.part = nullptr;
-  if (ksplit > 1 && CHUNK == 0 && g_kpart.ptr &&
-      static_cast<size_t>(ksplit) * M * N <= g_kpart.floats) {
-    sh.ksplit = ksplit;
-    sh.part = g_kpart.ptr;
-  }
+
   sh.num_m = (M + Cf::BM * NCTA - 1) / (Cf::BM * NCTA);
   sh.num_n = (N + bn - 1) / bn;
   sh.num_k = (K + Cf::BK - 1) / Cf::BK;
   const int tiles = sh.num_m * sh.num_n;
+  sh.ksplit = 1;
+  sh.part = nullptr;
+  sh.tile_begin = 0;
+  sh.tile_end = 0;
+  const long long tsplit = tail > 0 ? tail : tiles;
+  if (ksplit > 1 && CHUNK == 0 && g_kpart.ptr &&
+      static_cast<size_t>(ksplit) * tsplit * Cf::BM * NCTA * bn <= g_kpart.floats) {
+    sh.ksplit = ksplit;
+    sh.part = g_kpart.ptr;
+  } else {
+    tail = 0;  // no split-K available: whole tiles only
+  }
   auto kern = k_gemm<T, BN, AMN, BMN, EPI, SPLIT, CHUNK, PAIR>;
   static bool attr_done[64] = {false};
   int dev = 0;
@@ -405,39 +413,56 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
     attr_done[dev & 63] = true;
   }
   const int slots = num_sms() / NCTA;  // persistent: one CTA (pair) per SM (pair)
-  const int units = tiles * sh.ksplit;
-  const int grid = (units < slots ? units : slots) * NCTA;
-  if (grid <= 0) return FI_OK;
   ProfScope prof(EPI == EPI_FWD || EPI == EPI_FWD_H ? FI_PROF_GEMM_FWD
                  : EPI == EPI_WGRAD ? FI_PROF_GEMM_WGRAD
                  : EPI == EPI_STORE ? FI_PROF_PREP : FI_PROF_GEMM_DGRAD, st);  // DGRAD(_H), DUNARY
-  if constexpr (PAIR) {
-    FI_TRY(launch_cluster(kern, 2, dim3(grid), dim3(256), smem_bytes, st, ta, tb, ta2, tb2,
-                          sh, ep));
-  } else {
-    FI_TRY(launch_ex(kern, 1, dim3(grid), dim3(256), smem_bytes, st, ta, tb, ta2, tb2, sh, ep));
+  auto go = [&](const GemmShape& g) -> int {
+    const int units = ((g.tile_end > 0 ? g.tile_end : tiles) - g.tile_begin) * g.ksplit;
+    const int grid = (units < slots ? units : slots) * NCTA;
+    if (grid <= 0) return FI_OK;
+    if constexpr (PAIR) {
+      FI_TRY(launch_cluster(kern, 2, dim3(grid), dim3(256), smem_bytes, st, ta, tb, ta2, tb2, g,
+                            ep));
+    } else {
+      FI_TRY(launch_ex(kern, 1, dim3(grid), dim3(256), smem_bytes, st, ta, tb, ta2, tb2, g, ep));
+    }
+    FI_CUDA(cudaGetLastError());
+    return FI_OK;
+  };
+  if (sh.ksplit > 1 && tail > 0 && tail < tiles) {  // whole waves first, then the K-split tail
+    GemmShape head = sh;
+    head.ksplit = 1;
+    head.part = nullptr;
+    head.tile_end = tiles - tail;
+    FI_TRY(go(head));
+    sh.tile_begin = tiles - tail;
   }
-  FI_CUDA(cudaGetLastError());
+  FI_TRY(go(sh));
   if (sh.ksplit > 1) {  // sum the partials in order and run the epilogue
-    const long long chunks = static_cast<long long>(M) * (N / 32);
+    const int tile_rows = Cf::BM * NCTA;
+    const long long chunks =
+        static_cast<long long>(tiles - sh.tile_begin) * tile_rows * (bn / 32);
     FI_TRY(launch_ex(k_gemm_fixup<EPI>, 1, dim3(static_cast<unsigned>((chunks + 255) / 256)),
-                     dim3(256), 0, st, static_cast<const float*>(sh.part), sh.ksplit, M, N, ep));
+                     dim3(256), 0, st, static_cast<const float*>(sh.part), sh.ksplit, M, N,
+                     sh.num_m, tile_rows, bn, sh.tile_begin, tiles, ep));
     FI_CUDA(cudaGetLastError());
   }
   return FI_OK;
 }
 
-// Tile shape per launch from a cost model in units of one single-CTA
-// 128 x 256 k-iteration: ceil(T / slots) * k_iters * t, with
-//   single CTA  T = ceil(M/128) ceil(N/bn) over 148 slots, t = 0.77 + 0.23 bn/256
-//   CTA pair    T = ceil(M/256) ceil(N/bn) over  74 slots, t = t_pair(bn)
-// fitted to B200 measurements (scripts/gemm_bn_sweep.py): a k-iteration's
-// cost is dominated by the operand bytes each SM pulls through L2 (A rows +
-// B rows, the pair halving B), not by the tensor pipe, so narrow N tiles
-// are nearly as expensive as wide ones and pairs win whenever the M tiles
-// fill.  The N tile is free in steps of 32 (K-major B) or of one 128-B
-// atom per CTA (MN-major B), so the tile count can be matched to whole
-// waves.  FI_GEMM_PAIR=0/1 and FI_GEMM_BN force the choice for A/B runs.
+// Tile shape per launch from a cost model in microseconds: a wave of
+// persistent tiles costs k_iters x 0.55 us x t(bn) with
+//   single CTA  T = ceil(M/128) ceil(N/bn) tiles over 148 slots, t = 0.77 + 0.23 bn/256
+//   CTA pair    T = ceil(M/256) ceil(N/bn) tiles over  74 slots, t = 0.965 t_single
+// fitted to B200 measurements (scripts/gemm_bn_sweep.py, whole waves, long
+// K): a k-iteration has a large fixed part (A-tile staging, issue), so
+// narrow N tiles are nearly as expensive as wide ones, and a pair tile (two
+// SMs, 256 rows) costs 3.5% less per row than two single tiles.  The N tile
+// is free in steps of 32 (K-major B) or of one 128-B atom per CTA (MN-major
+// B) so tile counts can land on whole waves; split-K options (whole GEMM,
+// or only the partial last wave) add their partial-tile traffic and
+// fix-up launch.  FI_GEMM_PAIR / FI_GEMM_BN / FI_GEMM_KSPLIT / FI_GEMM_NOTAIL
+// force choices for A/B runs; FI_GEMM_LOG=1 prints them.
 int gemm_env(const char* name, int dflt) {
   const char* e = getenv(name);
   return e ? atoi(e) : dflt;
@@ -447,44 +472,64 @@ struct GemmChoice {
   int bn;
   bool pair;
   int ksplit;
+  int tail;  // > 0: whole waves, then the last `tail` tiles split ksplit ways over K
 };
 
 double gemm_t_single(int bn) { return 0.77 + 0.23 * bn / 256.0; }
-double gemm_t_pair(int bn) { return 0.56 + 0.20 * bn / 256.0; }
+double gemm_t_pair(int bn) { return 0.965 * gemm_t_single(bn); }  // per pair k-iteration
 
 GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int step_single,
                        int step_pair, bool allow_ksplit) {
   static const int force_pair = gemm_env("FI_GEMM_PAIR", -1);
   static const int force_bn = gemm_env("FI_GEMM_BN", 0);
   static const int force_ks = gemm_env("FI_GEMM_KSPLIT", 0);  // 1: never split K
-  GemmChoice best{0, false, 1};
+  static const int no_tail = gemm_env("FI_GEMM_NOTAIL", 0);
+  GemmChoice best{0, false, 1, 0};
   double best_cost = 1e300;  // microseconds
   const double us_per_kiter = 0.55;  // one 128 x 256 bf16 k-iteration on one SM (measured)
   for (int pair = 0; pair < 2; ++pair) {
     if (force_pair >= 0 && pair != force_pair) continue;
     const int step = pair ? step_pair : step_single;
     const int slots = num_sms() / (pair ? 2 : 1);
-    const long long mt = (M + (pair ? 255 : 127)) / (pair ? 256 : 128);
+    const int tile_rows = pair ? 256 : 128;
+    const long long mt = (M + tile_rows - 1) / tile_rows;
     for (int bn = bn_max / step * step; bn >= 64 && bn >= step; bn -= step) {
       if (force_bn && bn != force_bn) continue;
       const long long T = mt * ((N + bn - 1) / bn);
       const double t = us_per_kiter * (pair ? gemm_t_pair(bn) : gemm_t_single(bn));
-      auto feasible = [&](int ks) {
-        return ks == 1 || (allow_ksplit && force_ks != 1 && T * ks <= slots && k_iters / ks >= 4 &&
-                           static_cast<double>(ks) * M * N <= static_cast<double>(g_kpart.floats));
+      // split-K over `units` tiles of which `r` are split: feasibility and fixup cost
+      auto ks_ok = [&](long long r, int ks) {
+        return allow_ksplit && force_ks != 1 && r * ks <= slots && k_iters / ks >= 4 &&
+               static_cast<double>(ks) * r * tile_rows * bn <= static_cast<double>(g_kpart.floats);
       };
-      const bool forced = force_ks > 1 && feasible(force_ks);
-      for (int ks = 1; ks <= 8; ++ks) {
-        if (!feasible(ks)) break;
-        if (forced && ks != force_ks) continue;
-        const long long units = T * ks;
-        double cost = static_cast<double>((units + slots - 1) / slots) *
-                      ((k_iters + ks - 1) / ks) * t;
-        if (ks > 1)  // partial write + fixup read (~5 TB/s) + the fixup launch
-          cost += 4.0 + 2.0 * ks * static_cast<double>(M) * N * 4.0 / 5.0e6;
+      // partial write + read at ~3 TB/s effective, plus the extra launches and
+      // their drain (fitted: a tail that saves less than ~12 us is not worth it)
+      auto fixup_us = [&](long long r, int ks) {
+        return 12.0 + 2.0 * ks * static_cast<double>(r) * tile_rows * bn * 4.0 / 3.0e6;
+      };
+      auto consider = [&](double cost, int ks, int tail) {
         if (cost < best_cost * 0.995) {
           best_cost = cost;
-          best = {bn, pair != 0, ks};
+          best = {bn, pair != 0, ks, tail};
+        }
+      };
+      // whole tiles, optionally all split over K (small M: fewer tiles than slots)
+      const bool forced = force_ks > 1 && ks_ok(T, force_ks);
+      for (int ks = 1; ks <= 8; ++ks) {
+        if (ks > 1 && !ks_ok(T, ks)) break;
+        if (forced && ks != force_ks) continue;
+        double cost = static_cast<double>((T * ks + slots - 1) / slots) * ((k_iters + ks - 1) / ks) * t;
+        if (ks > 1) cost += fixup_us(T, ks);
+        consider(cost, ks, 0);
+      }
+      // whole waves, then the partial last wave split over K (no tail gap)
+      const long long r = T % slots;
+      if (!no_tail && T > slots && r > 0 && force_ks != 1) {
+        for (int ks = 2; ks <= 8; ++ks) {
+          if (!ks_ok(r, ks)) break;
+          const double cost = static_cast<double>(T / slots) * k_iters * t +
+                              static_cast<double>((k_iters + ks - 1) / ks) * t + fixup_us(r, ks);
+          consider(cost, ks, static_cast<int>(r));
         }
       }
     }
@@ -508,12 +553,16 @@ int run_gemm_s(const Operand& A, const Operand& B, int M, int N, int K, int a_ro
   const int step1 = BMN ? (ATOM > 32 ? ATOM : 32) : 32;
   const int step2 = BMN ? 2 * ATOM : 32;
   const GemmChoice c = choose_gemm(M, N, k_iters, kBnMax, step1, step2, kChunk == 0);
+  static const int log_choice = env_int("FI_GEMM_LOG", 0);
+  if (log_choice)
+    fprintf(stderr, "[fi gemm] EPI=%d M=%d N=%d K=%d -> bn=%d pair=%d ksplit=%d tail=%d\n", EPI, M,
+            N, K, c.bn, static_cast<int>(c.pair), c.ksplit, c.tail);
   if (c.bn == 0) return set_err(FI_ERR_ARG, "no GEMM tile for N=%d (FI_GEMM_BN?)", N);
   if (c.pair)
     return launch_gemm<T, kBnMax, AMN, BMN, EPI, SPLIT, kChunk, true>(A, B, M, N, K, a_row0, ep,
-                                                                      st, c.bn, c.ksplit);
+                                                                      st, c.bn, c.ksplit, c.tail);
   return launch_gemm<T, kBnMax, AMN, BMN, EPI, SPLIT, kChunk, false>(A, B, M, N, K, a_row0, ep,
-                                                                     st, c.bn, c.ksplit);
+                                                                     st, c.bn, c.ksplit, c.tail);
 }
 
 // Dispatch on the split (fp32 / bf16x3) mode; tf32 operands are never split.
@@ -965,7 +1014,7 @@ int fi_inside_forward(const fi_shape* shape, const float* L, const float* R, con
   FI_TRY(check_ptrs({L, R, root, unary, lengths, log_z, ws}));
   FI_TRY(load_encode());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  KPartScope kps(at<float>(ws, p.kpart), static_cast<size_t>(kKPartRows) * 2 * p.Np);
+  KPartScope kps(at<float>(ws, p.kpart), static_cast<size_t>(kKPartFloats));
   if (p.tf32) {
     if (p.half_chart) return forward_impl<float, __half>(p, L, R, root, unary, lengths, log_z, ws, st);
     return forward_impl<float, float>(p, L, R, root, unary, lengths, log_z, ws, st);
@@ -984,7 +1033,7 @@ int fi_inside_backward(const fi_shape* shape, const float* L, const float* R, co
   FI_TRY(check_ptrs({L, R, root, unary, lengths, log_z, grad_log_z, dL, dR, droot, dunary, ws}));
   FI_TRY(load_encode());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  KPartScope kps(at<float>(ws, p.kpart), static_cast<size_t>(kKPartRows) * 2 * p.Np);
+  KPartScope kps(at<float>(ws, p.kpart), static_cast<size_t>(kKPartFloats));
 #define FI_BWD(T, CT)                                                                      \
   return backward_impl<T, CT>(p, L, R, root, unary, lengths, log_z, grad_log_z, dL, dR, droot, \
                               dunary, ws, st)
@@ -1087,7 +1136,7 @@ int fi_test_gemm(int32_t dtype, int32_t a_mn, int32_t b_mn, int32_t M, int32_t N
   if (M < 1 || N < 64 || N % 64 || K < 1)
     return set_err(FI_ERR_ARG, "test GEMM needs M>=1, N%%64==0, K>=1");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const size_t kfloats = 8ull * M * N;  // room for any split-K the chooser picks
+  const size_t kfloats = static_cast<size_t>(kKPartFloats);
   void* scratch = nullptr;
   FI_CUDA(cudaMallocAsync(&scratch, kfloats * 4, st));
   struct Free {

@@ -45,12 +45,17 @@ struct GemmShape {
   int num_m, num_n, num_k;  // tiles of (128 or 256 for pairs) x bn x BK
   int bn;         // N tile (runtime, <= the kernel's BN bound, multiple of 32)
   int stages;     // smem ring depth (runtime, <= GemmCfg::STAGES)
-  // split-K (ksplit > 1, small M): work unit u = (tile u / ksplit, K part
-  // u % ksplit); each unit stores its raw fp32 partial tile at
-  // part[(kpart * M + row) * N + col] and k_gemm_fixup sums the parts in
-  // order (deterministic) and applies the epilogue.
+  // split-K (ksplit > 1): work unit u = (tile tile_begin + u / ksplit, K part
+  // u % ksplit); each unit stores its raw fp32 partial tile, dense
+  // (tile_rows x bn), at part + ((kpart * T_split + tile - tile_begin) *
+  // tile_rows * bn); k_gemm_fixup sums the parts in order (deterministic)
+  // and applies the epilogue.
   int ksplit;
   float* part;
+  // tiles [tile_begin, tile_end) only (tile_end 0: all; a "waves + split-K
+  // tail" GEMM is two launches over one shape: whole waves, then the tail
+  // split over K)
+  int tile_begin, tile_end;
 };
 
 struct GemmEpi {
@@ -332,7 +337,9 @@ __global__ void __launch_bounds__(256, 1)
   const int num_tiles = sh.num_m * sh.num_n;
   const int k_iters = SPLIT ? 3 * sh.num_k : sh.num_k;
   const int ks = sh.ksplit > 1 ? sh.ksplit : 1;
-  const int nunits = num_tiles * ks;
+  const int tb = sh.tile_begin;
+  const int tile_e = sh.tile_end > 0 ? sh.tile_end : num_tiles;
+  const int nunits = (tile_e - tb) * ks;
   const int bn = sh.bn;                       // runtime N tile <= BN
   const int bn_cta = bn / NCTA;               // B rows staged by this CTA
   const uint32_t rank = PAIR ? cluster_rank() : 0;
@@ -375,7 +382,8 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t phase = 0;
       const uint32_t stage_tx = NCTA * (C::A_BYTES + bn_cta * 128);
       for (int u = tile0; u < nunits; u += tstep) {
-        const int tile = u / ks, kpart = u - tile * ks;
+        const int tu = u / ks, kpart = u - tu * ks;
+        const int tile = tb + tu;
         const int k0 = k_iters * kpart / ks, k1 = k_iters * (kpart + 1) / ks;
         const int m_blk = tile % sh.num_m;
         const int n_blk = tile / sh.num_m;
@@ -495,7 +503,8 @@ __global__ void __launch_bounds__(256, 1)
       }
     };
     for (int u = tile0; u < nunits; u += tstep) {
-      const int tile = u / ks, kpart = u - tile * ks;
+      const int tu = u / ks, kpart = u - tu * ks;
+      const int tile = tb + tu;
       const int k0 = k_iters * kpart / ks, k1 = k_iters * (kpart + 1) / ks;
       const int m_blk = tile % sh.num_m;
       const int n_blk = tile / sh.num_m;
@@ -504,10 +513,10 @@ __global__ void __launch_bounds__(256, 1)
       const int col_base = n_blk * bn;
       auto emit = [&](int j, const float (&v)[32]) {
         if (ks > 1) {  // split-K: raw fp32 partial, summed + transformed by k_gemm_fixup
-          const int col = col_base + j * 32;
-          if (col >= sh.N || lrow >= ep.M) return;
+          constexpr int tile_rows = C::BM * NCTA;
+          const long long tsplit = tile_e - tb;
           float4* dst = reinterpret_cast<float4*>(
-              sh.part + (static_cast<long long>(kpart) * ep.M + lrow) * sh.N + col);
+              sh.part + ((kpart * tsplit + tu) * tile_rows + rank * C::BM + r) * bn + j * 32);
 #pragma unroll
           for (int q = 0; q < 8; ++q)
             dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
@@ -572,21 +581,30 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 // Split-K fixup: sum the ksplit raw partials of every (row, 32-column chunk)
-// in part order and run the launch's epilogue.  One thread per chunk.
+// of the tiles [tile_begin, T) in part order and run the launch's epilogue.
+// One thread per chunk; a tile is tile_rows x bn (bn a multiple of 32).
 template <int EPI>
 __global__ void __launch_bounds__(256) k_gemm_fixup(const float* __restrict__ part, int ksplit,
-                                                    int M, int N, GemmEpi ep) {
+                                                    int M, int N, int num_m, int tile_rows,
+                                                    int bn, int tile_begin, int num_tiles,
+                                                    GemmEpi ep) {
   pdl_wait();
-  const int nch = N / 32;
+  const int per_tile = tile_rows * (bn / 32);
   const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= static_cast<long long>(M) * nch) return;
-  const int lrow = static_cast<int>(t / nch), col = static_cast<int>(t % nch) * 32;
+  if (t >= static_cast<long long>(num_tiles - tile_begin) * per_tile) return;
+  const int tile = tile_begin + static_cast<int>(t / per_tile);
+  const int within = static_cast<int>(t % per_tile);
+  const int lrow = (tile % num_m) * tile_rows + within / (bn / 32);
+  const int col = (tile / num_m) * bn + (within % (bn / 32)) * 32;
+  if (lrow >= M || col >= N) return;
+  const long long tsplit = num_tiles - tile_begin;
   float v[32];
 #pragma unroll
   for (int q = 0; q < 32; ++q) v[q] = 0.f;
   for (int k = 0; k < ksplit; ++k) {
-    const float4* src =
-        reinterpret_cast<const float4*>(part + (static_cast<long long>(k) * M + lrow) * N + col);
+    const float4* src = reinterpret_cast<const float4*>(
+        part + ((k * tsplit + tile - tile_begin) * tile_rows) * bn +
+        static_cast<long long>(within / (bn / 32)) * bn + (within % (bn / 32)) * 32);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const float4 w = __ldcg(src + q);
