@@ -133,18 +133,37 @@ int env_int(const char* name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 
-int make_decomp(int Np, int c, const char* env_c, const char* env_s, int stages, Decomp* d) {
-  const int want = env_int(env_c, c);
-  if (want >= 1 && want <= 8 && Np % (want * 256) == 0) c = want;
+// An exact column decomposition of a Np-wide row: c CTAs x `threads`
+// consumers (a multiple of 32, <= 256) x v in {1, 2, 4} groups of 4 columns,
+// c * threads * 4 * v == Np.  Returns false if this c admits none.
+bool decomp_for(int Np, int c, Decomp* d) {
+  if (c < 1 || c > 8 || Np % c) return false;
   const int cols = Np / c;
-  d->clusters = c;
-  d->threads = cols / 4 < 256 ? cols / 4 : 256;
-  d->v = cols / (4 * d->threads);
-  d->cols_per_cta = cols;
+  for (int v : {1, 2, 4}) {
+    if (cols % (4 * v)) continue;
+    const int threads = cols / (4 * v);
+    if (threads % 32 == 0 && threads <= 256) {
+      d->clusters = c;
+      d->threads = threads;
+      d->v = v;
+      d->cols_per_cta = cols;
+      return true;
+    }
+  }
+  return false;
+}
+
+// The valid decomposition whose CTA count is closest to `c` (the FI_*
+// override first, if valid).
+int make_decomp(int Np, int c, const char* env_c, const char* env_s, int stages, Decomp* d) {
+  const int want = env_int(env_c, 0);
+  bool ok = want > 0 && decomp_for(Np, want, d);
+  for (int delta = 0; !ok && delta < 8; ++delta)
+    ok = decomp_for(Np, c + delta, d) || decomp_for(Np, c - delta, d);
+  if (!ok)
+    return set_err(FI_ERR_UNSUPPORTED, "no column decomposition for Np=%d (C near %d)", Np, c);
   const int st = env_int(env_s, stages);
   d->stages = st < 2 ? 2 : (st > 16 ? 16 : st);
-  if (d->v != 1 && d->v != 2 && d->v != 4)
-    return set_err(FI_ERR_UNSUPPORTED, "unsupported column decomposition (Np=%d, C=%d)", Np, c);
   return FI_OK;
 }
 
@@ -169,7 +188,9 @@ int make_plan(const fi_shape* s, Plan* p) {
   p->P = s->n_pt;
   p->B = s->batch;
   p->l = s->max_len;
-  p->Np = p->N <= 1024 ? static_cast<int>(align_up(p->N, 256)) : static_cast<int>(align_up(p->N, 1024));
+  // padded symbol count: multiple of 256 / 1024 / 2048 so the bandwidth
+  // kernels always find an exact column decomposition (make_decomp)
+  p->Np = static_cast<int>(align_up(p->N, p->N <= 1024 ? 256 : p->N <= 8192 ? 1024 : 2048));
   p->Pp = static_cast<int>(align_up(p->P, 256));
   p->tf32 = s->gemm_dtype == FI_GEMM_TF32;
   p->split = s->gemm_dtype == FI_GEMM_FP32;
@@ -186,13 +207,9 @@ int make_plan(const fi_shape* s, Plan* p) {
   // fp32 chart split C = 2 / gather C = 4, fp16 chart split C = 1 / gather
   // C = 2).  FI_CLUSTER / FI_GCLUSTER / FI_STAGES / FI_GSTAGES override.
   const int cesz = p->half_chart ? 2 : 4;
-  auto pick_c = [&](int bytes) {
+  auto pick_c = [&](int bytes) {  // target CTAs per row; make_decomp finds the nearest exact one
     int c = p->Np * cesz / bytes;
-    const int cmin = (p->Np + 4095) / 4096;  // V <= 4
-    c = c < cmin ? cmin : c;
-    c = c < 1 ? 1 : (c > 8 ? 8 : c);
-    while (c > 1 && p->Np % (c * 256)) --c;
-    return c;
+    return c < 1 ? 1 : (c > 8 ? 8 : c);
   };
   FI_TRY(make_decomp(p->Np, pick_c(8192), "FI_CLUSTER", "FI_STAGES", 4, &p->dsplit));
   FI_TRY(make_decomp(p->Np, pick_c(4096), "FI_GCLUSTER", "FI_GSTAGES", 6, &p->dgather));
@@ -758,8 +775,12 @@ int forward_impl(const Plan& p, const float* L, const float* R, const float* roo
     static const int pers = env_int("FI_SPLIT_PERS", 1);
     if (pers && p.Np <= 8192) {
       // persistent one-CTA-per-row kernel: ~72 KB of ring per CTA (2-3 CTAs/SM)
-      const int cons = p.Np / 4 < 256 ? p.Np / 4 : 256;
-      const int V = p.Np / (4 * cons);
+      // one CTA per row: Np = 4 * cons * V with cons <= 256 a multiple of 32
+      int V = 1;
+      while (V < 8 && (p.Np / (4 * V) > 256 || (p.Np / (4 * V)) % 32)) V *= 2;
+      const int cons = p.Np / (4 * V);
+      if (4 * cons * V != p.Np || cons % 32 || cons > 256)
+        return set_err(FI_ERR_UNSUPPORTED, "no one-CTA row decomposition for Np=%d", p.Np);
       const size_t stage_bytes = 2ull * p.Np * sizeof(CT);
       static const int env_st = env_int("FI_PSTAGES", 0);
       int stages = env_st ? env_st : static_cast<int>(73728 / stage_bytes);
@@ -775,7 +796,14 @@ int forward_impl(const Plan& p, const float* L, const float* R, const float* roo
         int occ = 0;
         FI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 + cons, smem));
         occ = occ < 1 ? 1 : occ;
-        const int grid = nrows < occ * num_sms() ? nrows : occ * num_sms();
+        // every CTA gets the same number of rows (no partial last round)
+        static const int balance = env_int("FI_SPLIT_BALANCE", 0);  // measured slightly slower
+        const int slots = occ * num_sms();
+        int grid = nrows < slots ? nrows : slots;
+        if (balance) {
+          const int per = (nrows + slots - 1) / slots;
+          grid = (nrows + per - 1) / per;
+        }
         FI_TRY(launch_ex(kern, 1, dim3(grid), dim3(32 + cons), smem, s, sa, stages, nprod));
         FI_CUDA(cudaGetLastError());
         return FI_OK;

@@ -114,3 +114,29 @@ def test_config2_size_gradients(gemm_dtype, chart_dtype, grad):
     np.testing.assert_allclose(got["log_z"], want["log_z"], rtol=rtol)
     for k in ("dL", "dR", "droot", "dunary"):
         assert_close(k, got[k], want[k], rtol)
+
+
+@pytest.mark.parametrize("N,P,lmax,lengths", [(300, 200, 7, [7, 5]), (3000, 1000, 6, [6, 4]),
+                                             (5000, 700, 5, [5, 3])])
+def test_odd_symbol_counts(N, P, lmax, lengths):
+    """Symbol counts that pad to 512 / 3072 / 5120 columns: every kernel's
+    column decomposition must cover the padded row exactly (bf16 bound)."""
+    root, left, right, emit, unary, lens, _ = make_case(N, P, 16, 2, lmax, 11, lengths)
+    grad = np.array([-0.5, -0.5])  # the training loss's sign (see test_config2_size_gradients)
+    want = O.inside_batch(left, right, root, unary, lens, grad)
+    got = run_op(root, left, right, unary, lens, grad, "bf16")
+    np.testing.assert_allclose(got["log_z"], want["log_z"], rtol=2e-3)
+    for k in ("dL", "dR", "droot", "dunary"):
+        assert_close(k, got[k], want[k], 2e-3)
+
+
+def test_beyond_8192_symbols_identities():
+    """N = 9000 (Np = 10240: the cluster split kernel, 5-CTA rows): log Z of a
+    length-3 sentence against the oracle and the outside-pass identities."""
+    N, P, l = 9000, 64, 3
+    root, left, right, emit, unary, lens, _ = make_case(N, P, 8, 1, l, 12)
+    want = O.inside_batch(left, right, root, unary, lens, backward=False)["log_z"]
+    got = run_op(root, left, right, unary, lens, np.array([1.0]), "bf16")
+    np.testing.assert_allclose(got["log_z"], want, rtol=2e-3)
+    assert got["droot"].sum() == pytest.approx(1.0, rel=2e-3)
+    np.testing.assert_allclose(got["dunary"][0].sum(-1), np.ones(l), rtol=2e-3)
