@@ -8,6 +8,7 @@ the reference-side binding shown in INTEGRATION.md.
 from __future__ import annotations
 
 import ctypes
+import os
 from ctypes import POINTER, Structure, c_float, c_int32, c_int64, c_size_t, c_void_p, c_char_p
 
 from . import _build
@@ -110,7 +111,8 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
     if not _build.LIB_PATH.exists():
         raise RuntimeError(f"FlashInside engine library missing: {_build.LIB_PATH} "
                            "(run __graft_entry__.build()); there is no CPU fallback")
-    lib = ctypes.CDLL(str(_build.LIB_PATH))
+    # FI_LIB_PATH: load another build of the same C ABI (A/B timing runs)
+    lib = ctypes.CDLL(os.environ.get("FI_LIB_PATH") or str(_build.LIB_PATH))
     for name, res, args in SIGNATURES:
         fn = getattr(lib, name)
         fn.restype = res

@@ -374,6 +374,8 @@ struct KPartScope {
 // ring that fits (one CTA per SM); the dual-stream sweep (see forward_impl)
 // caps it so a bandwidth-kernel CTA can share each SM with a GEMM CTA.
 thread_local int g_gemm_stages = 0;
+constexpr int kGemmSmemMax = 227 * 1024;  // opt-in dynamic shared memory per CTA
+constexpr int kGemmStagesMax = 12;        // barrier block (256 B) holds 2 x 12 + 4 mbarriers
 
 template <typename T, int BN, bool AMN, bool BMN, int EPI, bool SPLIT, int CHUNK, bool PAIR>
 int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_row0,
@@ -401,8 +403,18 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
   sh.K = K;
   sh.a_row0 = a_row0;
   sh.bn = bn;
-  sh.stages = (g_gemm_stages > 1 && g_gemm_stages < Cf::STAGES) ? g_gemm_stages : Cf::STAGES;
-  const size_t smem_bytes = static_cast<size_t>(sh.stages) * Cf::STAGE_BYTES + 1024 + 256;
+  // ring depth: as many (A + this CTA's share of B) stages as fit in 227 KB
+  // (a pair CTA stages half the N tile, so pairs run deeper rings)
+  sh.b_stage = bn / NCTA * 128;
+  static const int env_bstride = env_int("FI_GEMM_BSTRIDE", 0);  // A/B experiments (bytes)
+  if (env_bstride > sh.b_stage) sh.b_stage = env_bstride;
+  const int stage_bytes = Cf::A_BYTES + sh.b_stage;
+  int max_stages = (kGemmSmemMax - 1024 - 256) / stage_bytes;
+  max_stages = max_stages > kGemmStagesMax ? kGemmStagesMax : max_stages;
+  static const int env_stages = env_int("FI_GEMM_STAGES", 0);  // A/B experiments
+  const int cap = g_gemm_stages > 1 ? g_gemm_stages : env_stages;
+  sh.stages = (cap > 1 && cap < max_stages) ? cap : max_stages;
+  const size_t smem_bytes = static_cast<size_t>(sh.stages) * stage_bytes + 1024 + 256;
 
   sh.num_m = (M + Cf::BM * NCTA - 1) / (Cf::BM * NCTA);
   sh.num_n = (N + bn - 1) / bn;
@@ -426,7 +438,7 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
   cudaGetDevice(&dev);
   if (!attr_done[dev & 63]) {
     FI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Cf::SMEM_BYTES));
+                                 kGemmSmemMax));
     attr_done[dev & 63] = true;
   }
   const int slots = num_sms() / NCTA;  // persistent: one CTA (pair) per SM (pair)
@@ -493,10 +505,19 @@ struct GemmChoice {
 };
 
 double gemm_t_single(int bn) { return 0.77 + 0.23 * bn / 256.0; }
-double gemm_t_pair(int bn) { return 0.965 * gemm_t_single(bn); }  // per pair k-iteration
+// Per pair k-iteration.  Above 256 the pair tile issues two MMAs per K step
+// and stages 48 KB per CTA instead of 32 KB: measured 1.476x the 256 time
+// for 2x the work at bn = 512 (a 256-wide tile is bound by the per-SM
+// L2->shared fill rate, ~70 GB/s, not by the tensor core).
+double gemm_t_pair(int bn) {
+  return bn > 256 ? 0.965 * (1.0 + 0.476 * (bn - 256) / 256.0) : 0.965 * gemm_t_single(bn);
+}
+// Tiles above 256 fill TMEM with one accumulator, so the epilogue is not
+// overlapped with the next tile's main loop: its cost per wave (model units).
+double gemm_epi_serial(int bn) { return bn > 256 ? 6.0 * bn / 512.0 : 0.0; }
 
-GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int step_single,
-                       int step_pair, bool allow_ksplit) {
+GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int bn_max_pair,
+                       int step_single, int step_pair, bool allow_ksplit) {
   static const int force_pair = gemm_env("FI_GEMM_PAIR", -1);
   static const int force_bn = gemm_env("FI_GEMM_BN", 0);
   static const int force_ks = gemm_env("FI_GEMM_KSPLIT", 0);  // 1: never split K
@@ -510,13 +531,15 @@ GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int step_sin
     const int slots = num_sms() / (pair ? 2 : 1);
     const int tile_rows = pair ? 256 : 128;
     const long long mt = (M + tile_rows - 1) / tile_rows;
-    for (int bn = bn_max / step * step; bn >= 64 && bn >= step; bn -= step) {
+    const int bmax = pair ? bn_max_pair : bn_max;
+    for (int bn = bmax / step * step; bn >= 64 && bn >= step; bn -= step) {
+      if (bn > 256 && bn % 64) continue;  // two sub-tiles: 256 + a multiple of 64
       if (force_bn && bn != force_bn) continue;
       const long long T = mt * ((N + bn - 1) / bn);
       const double t = us_per_kiter * (pair ? gemm_t_pair(bn) : gemm_t_single(bn));
       // split-K over `units` tiles of which `r` are split: feasibility and fixup cost
       auto ks_ok = [&](long long r, int ks) {
-        return allow_ksplit && force_ks != 1 && r * ks <= slots && k_iters / ks >= 4 &&
+        return allow_ksplit && force_ks != 1 && bn <= 256 && r * ks <= slots && k_iters / ks >= 4 &&
                static_cast<double>(ks) * r * tile_rows * bn <= static_cast<double>(g_kpart.floats);
       };
       // partial write + read at ~3 TB/s effective, plus the extra launches and
@@ -535,7 +558,8 @@ GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int step_sin
       for (int ks = 1; ks <= 8; ++ks) {
         if (ks > 1 && !ks_ok(T, ks)) break;
         if (forced && ks != force_ks) continue;
-        double cost = static_cast<double>((T * ks + slots - 1) / slots) * ((k_iters + ks - 1) / ks) * t;
+        double cost = static_cast<double>((T * ks + slots - 1) / slots) *
+                      (((k_iters + ks - 1) / ks) * t + gemm_epi_serial(bn));
         if (ks > 1) cost += fixup_us(T, ks);
         consider(cost, ks, 0);
       }
@@ -564,22 +588,29 @@ int run_gemm_s(const Operand& A, const Operand& B, int M, int N, int K, int a_ro
   const int k_iters = (SPLIT ? 3 : 1) * ((K + BK - 1) / BK);
   // fp32 mode: chunked round-to-nearest accumulation (8 K-iterations per
   // TMEM chunk) to bound the tensor-core truncation bias; N tile <= 128.
-  constexpr int kBnMax = SPLIT ? 128 : 256;
+  // pair tiles up to 256 x 512 for bf16 (two N = 256 MMAs per K step; the
+  // accumulator then fills TMEM, single-buffered)
+  constexpr int kBnMax = SPLIT ? 128 : (sizeof(T) == 2 ? 512 : 256);
+  constexpr int kBnSingle = kBnMax > 256 ? 256 : kBnMax;
   constexpr int kChunk = SPLIT ? FI_FP32_CHUNK : 0;
   // MN-major B is staged in whole 128-B atoms per CTA
   const int step1 = BMN ? (ATOM > 32 ? ATOM : 32) : 32;
   const int step2 = BMN ? 2 * ATOM : 32;
-  const GemmChoice c = choose_gemm(M, N, k_iters, kBnMax, step1, step2, kChunk == 0);
+  const GemmChoice c = choose_gemm(M, N, k_iters, kBnSingle, kBnMax, step1, step2, kChunk == 0);
   static const int log_choice = env_int("FI_GEMM_LOG", 0);
   if (log_choice)
     fprintf(stderr, "[fi gemm] EPI=%d M=%d N=%d K=%d -> bn=%d pair=%d ksplit=%d tail=%d\n", EPI, M,
             N, K, c.bn, static_cast<int>(c.pair), c.ksplit, c.tail);
   if (c.bn == 0) return set_err(FI_ERR_ARG, "no GEMM tile for N=%d (FI_GEMM_BN?)", N);
-  if (c.pair)
-    return launch_gemm<T, kBnMax, AMN, BMN, EPI, SPLIT, kChunk, true>(A, B, M, N, K, a_row0, ep,
-                                                                      st, c.bn, c.ksplit, c.tail);
-  return launch_gemm<T, kBnMax, AMN, BMN, EPI, SPLIT, kChunk, false>(A, B, M, N, K, a_row0, ep,
-                                                                     st, c.bn, c.ksplit, c.tail);
+  if (c.pair) {
+    if (c.bn > kBnSingle)  // 256 x 512-class pair tiles: two MMAs per K step
+      return launch_gemm<T, kBnMax, AMN, BMN, EPI, SPLIT, kChunk, true>(A, B, M, N, K, a_row0, ep,
+                                                                        st, c.bn, c.ksplit, c.tail);
+    return launch_gemm<T, kBnSingle, AMN, BMN, EPI, SPLIT, kChunk, true>(A, B, M, N, K, a_row0, ep,
+                                                                         st, c.bn, c.ksplit, c.tail);
+  }
+  return launch_gemm<T, kBnSingle, AMN, BMN, EPI, SPLIT, kChunk, false>(A, B, M, N, K, a_row0, ep,
+                                                                        st, c.bn, c.ksplit, c.tail);
 }
 
 // Dispatch on the split (fp32 / bf16x3) mode; tf32 operands are never split.

@@ -44,7 +44,8 @@ struct GemmShape {
   int a_row0;     // K-major A: first row coordinate inside the tensor map
   int num_m, num_n, num_k;  // tiles of (128 or 256 for pairs) x bn x BK
   int bn;         // N tile (runtime, <= the kernel's BN bound, multiple of 32)
-  int stages;     // smem ring depth (runtime, <= GemmCfg::STAGES)
+  int stages;     // smem ring depth (runtime: as many as fit in shared memory)
+  int b_stage;    // bytes of one B stage in this CTA (128 B of K x bn / NCTA rows)
   // split-K (ksplit > 1): work unit u = (tile tile_begin + u / ksplit, K part
   // u % ksplit); each unit stores its raw fp32 partial tile, dense
   // (tile_rows x bn), at part + ((kpart * T_split + tile - tile_begin) *
@@ -104,7 +105,10 @@ struct GemmCfg {
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (200 * 1024 / STAGE_BYTES) > 8 ? 8 : (200 * 1024 / STAGE_BYTES);
-  static constexpr int TMEM_COLS = 2 * BN;         // double-buffered accumulator
+  // accumulator columns: two buffers of BN (double-buffered) up to BN = 256;
+  // BN = 512 (pair tiles 256 x 512) fills TMEM with one buffer
+  static constexpr int TMEM_COLS = 2 * BN > 512 ? 512 : 2 * BN;
+  static constexpr int TMEM_HALF = TMEM_COLS / 2;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr bool TF32 = (kElt == 4);
 };
@@ -326,7 +330,7 @@ __global__ void __launch_bounds__(256, 1)
   const int NS = sh.stages;
   uint8_t* smA = smem;
   uint8_t* smB = smem + NS * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smB + NS * C::B_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smB + NS * sh.b_stage);
   uint64_t* empty = full + NS;
   uint64_t* tfull = empty + NS;
   uint64_t* tempty = tfull + 2;
@@ -342,6 +346,7 @@ __global__ void __launch_bounds__(256, 1)
   const int nunits = (tile_e - tb) * ks;
   const int bn = sh.bn;                       // runtime N tile <= BN
   const int bn_cta = bn / NCTA;               // B rows staged by this CTA
+  const int nbuf = bn <= C::TMEM_HALF ? 2 : 1;  // accumulator buffers in TMEM
   const uint32_t rank = PAIR ? cluster_rank() : 0;
   const int tile0 = PAIR ? blockIdx.x / 2 : blockIdx.x;
   const int tstep = PAIR ? gridDim.x / 2 : gridDim.x;
@@ -396,7 +401,7 @@ __global__ void __launch_bounds__(256, 1)
           const CUtensorMap* mb = (SPLIT && pass == 1) ? &tmB2 : &tmB;
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* a_dst = smA + stage * C::A_BYTES;
-          uint8_t* b_dst = smB + stage * C::B_BYTES;
+          uint8_t* b_dst = smB + stage * sh.b_stage;
           // completion is counted on the leader's full barrier (both CTAs' bytes)
           uint32_t fb = smem_u32(&full[stage]);
           if constexpr (PAIR) {
@@ -432,7 +437,10 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
       // ------------------------------------------------ MMA issuer (leader)
-      const uint32_t idesc = make_idesc<C::TF32>(bn, A_MN, B_MN, C::BM * NCTA);
+      // N tiles above 256 are two MMAs per K step (sub-tiles of 256 + the rest)
+      const uint32_t idesc0 = make_idesc<C::TF32>(bn > 256 ? 256 : bn, A_MN, B_MN, C::BM * NCTA);
+      const uint32_t idesc1 = make_idesc<C::TF32>(bn > 256 ? bn - 256 : 64, A_MN, B_MN, C::BM * NCTA);
+      constexpr uint32_t sub_b_off = 256 / NCTA * 128;  // B bytes of sub-tile 0 in this CTA
       constexpr uint32_t a_lbo = A_MN ? C::BK * 128 : 16;
       constexpr uint32_t b_lbo = B_MN ? C::BK * 128 : 16;
       // tf32 MN-major operands use the 32B-atom 128B swizzle (4-row groups)
@@ -456,18 +464,31 @@ __global__ void __launch_bounds__(256, 1)
           if (kc == 0) {  // start a chunk in a drained accumulator
             mbar_wait(&tempty[acc], acc_phase ^ 1);
             tc_fence_after();
-            d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+            d_tmem = tmem_base + static_cast<uint32_t>(acc * C::TMEM_HALF);
           }
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_base = smem_u32(smA + stage * C::A_BYTES);
-          const uint32_t b_base = smem_u32(smB + stage * C::B_BYTES);
+          const uint32_t b_base = smem_u32(smB + stage * sh.b_stage);
+          auto mma = [&](uint32_t dt, uint64_t ad, uint64_t bd, uint32_t id, uint32_t accum) {
+            if constexpr (PAIR) umma2<C::TF32>(dt, ad, bd, id, accum);
+            else umma<C::TF32>(dt, ad, bd, id, accum);
+          };
+          if constexpr (BN <= 256) {  // BN > 256 kernels run only N tiles above 256
 #pragma unroll
-          for (int k = 0; k < C::BK / C::UK; ++k) {
-            uint64_t ad = make_sdesc(a_base + k * a_kstep, a_lbo, a_sbo, a_lay);
-            uint64_t bd = make_sdesc(b_base + k * b_kstep, b_lbo, b_sbo, b_lay);
-            if constexpr (PAIR) umma2<C::TF32>(d_tmem, ad, bd, idesc, (kc | k) != 0 ? 1u : 0u);
-            else umma<C::TF32>(d_tmem, ad, bd, idesc, (kc | k) != 0 ? 1u : 0u);
+            for (int k = 0; k < C::BK / C::UK; ++k)
+              mma(d_tmem, make_sdesc(a_base + k * a_kstep, a_lbo, a_sbo, a_lay),
+                  make_sdesc(b_base + k * b_kstep, b_lbo, b_sbo, b_lay), idesc0,
+                  (kc | k) != 0 ? 1u : 0u);
+          } else {
+#pragma unroll
+            for (int k = 0; k < C::BK / C::UK; ++k) {
+              const uint64_t ad = make_sdesc(a_base + k * a_kstep, a_lbo, a_sbo, a_lay);
+              const uint32_t accum = (kc | k) != 0 ? 1u : 0u;
+              mma(d_tmem, ad, make_sdesc(b_base + k * b_kstep, b_lbo, b_sbo, b_lay), idesc0, accum);
+              mma(d_tmem + 256u, ad,
+                  make_sdesc(b_base + sub_b_off + k * b_kstep, b_lbo, b_sbo, b_lay), idesc1, accum);
+            }
           }
           if constexpr (PAIR) umma_commit2(&empty[stage]);
           else umma_commit(&empty[stage]);
@@ -478,8 +499,10 @@ __global__ void __launch_bounds__(256, 1)
           if (kc == cl - 1 || kb == k1 - 1) {
             if constexpr (PAIR) umma_commit2(&tfull[acc]);
             else umma_commit(&tfull[acc]);
-            acc ^= 1;
-            if (acc == 0) acc_phase ^= 1;
+            if (++acc == nbuf) {
+              acc = 0;
+              acc_phase ^= 1;
+            }
           }
         }
       }
@@ -511,24 +534,35 @@ __global__ void __launch_bounds__(256, 1)
       const int lrow = m_blk * (C::BM * NCTA) + rank * C::BM + r;  // row within this GEMM
       const EpiRow er = epi_row<EPI>(ep, lrow);
       const int col_base = n_blk * bn;
+      // tile column of TMEM column chunk j: with two sub-tiles in a pair, each
+      // CTA stages B rows [0, 128) of sub-tile 0 then the rest of its half,
+      // so sub-tile s's columns are [half 0 | half 1] of that range
+      auto tile_col = [&](int j) -> int {
+        const int c = j * 32;
+        if (!PAIR || BN <= 256) return c;
+        const int sb = c >> 8, w = c & 255;
+        const int hs = (sb ? bn - 256 : 256) / 2;
+        return (w / hs) * bn_cta + sb * 128 + w % hs;
+      };
       auto emit = [&](int j, const float (&v)[32]) {
+        const int tc = tile_col(j);
         if (ks > 1) {  // split-K: raw fp32 partial, summed + transformed by k_gemm_fixup
           constexpr int tile_rows = C::BM * NCTA;
           const long long tsplit = tile_e - tb;
           float4* dst = reinterpret_cast<float4*>(
-              sh.part + ((kpart * tsplit + tu) * tile_rows + rank * C::BM + r) * bn + j * 32);
+              sh.part + ((kpart * tsplit + tu) * tile_rows + rank * C::BM + r) * bn + tc);
 #pragma unroll
           for (int q = 0; q < 8; ++q)
             dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
           return;
         }
-        epi_emit<EPI>(ep, er, col_base + j * 32, sh.N, v);
+        epi_emit<EPI>(ep, er, col_base + tc, sh.N, v);
       };
       const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
       if constexpr (CHUNK == 0) {
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
-        const uint32_t t_row = t_lane + static_cast<uint32_t>(acc * BN);
+        const uint32_t t_row = t_lane + static_cast<uint32_t>(acc * C::TMEM_HALF);
 #pragma unroll 1
         for (int j = 0; j < bn / 32; ++j) {
           float v[32];
@@ -536,8 +570,10 @@ __global__ void __launch_bounds__(256, 1)
           emit(j, v);
         }
         release(acc);
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
+        if (++acc == nbuf) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
       } else {
         static_assert(BN <= 128, "chunked accumulation keeps BN fp32 sums per thread");
         float sum[BN / 32][32];
@@ -549,7 +585,7 @@ __global__ void __launch_bounds__(256, 1)
         for (int c = 0; c < nchunks; ++c) {
           mbar_wait(&tfull[acc], acc_phase);
           tc_fence_after();
-          const uint32_t t_row = t_lane + static_cast<uint32_t>(acc * BN);
+          const uint32_t t_row = t_lane + static_cast<uint32_t>(acc * C::TMEM_HALF);
 #pragma unroll
           for (int j = 0; j < BN / 32; ++j) {
             if (j < bn / 32) {

@@ -18,6 +18,13 @@ CASES = [  # M, N, K
     (128, 256, 8192),
     (4096, 2048, 512),
     (2496, 4096, 1024),
+    # pair tiles above 256 columns (two MMAs per K step, TMEM-filling
+    # accumulator): 512, 448, 384 (partial last N tile), 320
+    (2304, 8192, 4096),
+    (1600, 8192, 4096),
+    (1344, 8192, 4096),
+    (1216, 8192, 4096),
+    (1600, 4096, 8192),
 ]
 
 

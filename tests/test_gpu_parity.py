@@ -140,3 +140,29 @@ def test_beyond_8192_symbols_identities():
     np.testing.assert_allclose(got["log_z"], want, rtol=2e-3)
     assert got["droot"].sum() == pytest.approx(1.0, rel=2e-3)
     np.testing.assert_allclose(got["dunary"][0].sum(-1), np.ones(l), rtol=2e-3)
+
+
+def test_config3_width_batch_identities():
+    """|N| = 4096 with 64 sentences of length <= 24: the GEMMs run the wide
+    pair tiles (two MMAs per K step) in the forward, dgrad and wgrad.  log Z
+    of two sentences against the oracle forward; every gradient table
+    through identities of the inside-outside expectations (per sentence:
+    sum droot = 1, sum dL = sum dR = l - 1 binary nodes, each token's unary
+    posterior sums to 1)."""
+    N, P, V, B, lmax = 4096, 4096, 64, 64, 24
+    lengths = np.full(B, lmax)
+    lengths[::5] = 17
+    root, left, right, emit, unary, lens, _ = make_case(N, P, V, B, lmax, 5, lengths)
+    got = run_op(root, left, right, unary, lens, np.ones(B), "bf16")
+    for b in (0, B - 1):
+        want = O.inside_batch(left, right, root, unary[b:b + 1], lens[b:b + 1],
+                              backward=False)["log_z"]
+        np.testing.assert_allclose(got["log_z"][b], want[0], rtol=2e-3)
+    assert got["droot"].sum() == pytest.approx(B, rel=2e-3)
+    nodes = float((lens - 1).sum())
+    assert got["dL"].sum() == pytest.approx(nodes, rel=2e-3)
+    assert got["dR"].sum() == pytest.approx(nodes, rel=2e-3)
+    tok = got["dunary"].sum(-1)
+    for b in range(B):
+        np.testing.assert_allclose(tok[b, :lens[b]], 1.0, rtol=2e-3)
+        assert np.abs(tok[b, lens[b]:]).max(initial=0.0) == 0.0
