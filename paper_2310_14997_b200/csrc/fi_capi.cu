@@ -450,10 +450,11 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
     const int grid = (units < slots ? units : slots) * NCTA;
     if (grid <= 0) return FI_OK;
     if constexpr (PAIR) {
-      FI_TRY(launch_cluster(kern, 2, dim3(grid), dim3(256), smem_bytes, st, ta, tb, ta2, tb2, g,
-                            ep));
+      FI_TRY(launch_cluster(kern, 2, dim3(grid), dim3(gemm_threads<CHUNK>()), smem_bytes, st, ta,
+                            tb, ta2, tb2, g, ep));
     } else {
-      FI_TRY(launch_ex(kern, 1, dim3(grid), dim3(256), smem_bytes, st, ta, tb, ta2, tb2, g, ep));
+      FI_TRY(launch_ex(kern, 1, dim3(grid), dim3(gemm_threads<CHUNK>()), smem_bytes, st, ta, tb,
+                       ta2, tb2, g, ep));
     }
     FI_CUDA(cudaGetLastError());
     return FI_OK;

@@ -317,8 +317,15 @@ __device__ __forceinline__ void epi_emit(const GemmEpi& ep, const EpiRow& r, int
 // accumulator is handed to the epilogue warps, which add it into a
 // round-to-nearest fp32 register sum and hand it back (double-buffered), so
 // the bias is bounded by the chunk length whatever K is.  Requires BN <= 128.
+// Epilogue warps: one per TMEM lane quadrant (measured: a second set of 4
+// splitting the columns does not shorten the step).
+template <int CHUNK>
+constexpr int gemm_epi_warps() { return 4; }
+template <int CHUNK>
+constexpr int gemm_threads() { return 128 + 32 * gemm_epi_warps<CHUNK>(); }
+
 template <typename T, int BN, bool A_MN, bool B_MN, int EPI, bool SPLIT, int CHUNK, bool PAIR>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
            GemmShape sh, GemmEpi ep) {
@@ -364,7 +371,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4 * NCTA);
+      mbar_init(&tempty[a], gemm_epi_warps<CHUNK>() * NCTA);
     }
     fence_mbar_init();
   }
@@ -510,6 +517,7 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp >= 4) {
     // -------------------------------------------------- epilogue
     const int quad = warp & 3;
+    const int ehalf = (warp - 4) >> 2;  // which chunk pairs this warp drains (CHUNK == 0)
     const int r = quad * 32 + lane;  // accumulator row (TMEM lane)
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -563,11 +571,19 @@ __global__ void __launch_bounds__(256, 1)
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         const uint32_t t_row = t_lane + static_cast<uint32_t>(acc * C::TMEM_HALF);
+        const int nch = bn / 32;
 #pragma unroll 1
-        for (int j = 0; j < bn / 32; ++j) {
+        constexpr int kHalves = gemm_epi_warps<CHUNK>() / 4;
+        for (int j = 2 * ehalf; j + 1 < nch; j += 2 * kHalves) {
+          float v0[32], v1[32];
+          tmem_ld32x2(t_row + j * 32, t_row + j * 32 + 32, v0, v1);
+          emit(j, v0);
+          emit(j + 1, v1);
+        }
+        if ((nch & 1) && ((nch - 1) / 2) % kHalves == ehalf) {
           float v[32];
-          tmem_ld32(t_row + j * 32, v);
-          emit(j, v);
+          tmem_ld32(t_row + (nch - 1) * 32, v);
+          emit(nch - 1, v);
         }
         release(acc);
         if (++acc == nbuf) {
