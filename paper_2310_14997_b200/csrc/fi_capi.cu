@@ -110,6 +110,7 @@ int set_err(int code, const char* fmt, ...) {
 // split-K partial tiles: ksplit x split tiles <= the CTA slots, so at most
 // one (256 x 256 or 128 x 256) fp32 tile per slot
 constexpr long long kKPartFloats = 160LL * 256 * 256;
+constexpr int kKPartSems = 256;  // split-K tile counters (in-kernel reduction), after the partials
 
 // ------------------------------------------------------------------ layout
 struct Decomp {
@@ -243,7 +244,7 @@ int make_plan(const fi_shape* s, Plan* p) {
   p->topz = take(4ull * p->B);
   p->wsum = take(16);
   p->flag = take(256);
-  p->kpart = take(4ull * kKPartFloats);  // split-K partial tiles
+  p->kpart = take(4ull * kKPartFloats + 4ull * kKPartSems);  // split-K partial tiles + counters
   p->total = off;
   return FI_OK;
 }
@@ -359,13 +360,19 @@ int launch_cluster(K kern, int cluster, dim3 grid, dim3 block, size_t smem, cuda
 struct KPartScratch {
   float* ptr = nullptr;
   size_t floats = 0;
+  int* sem = nullptr;  // kKPartSems zeroed tile counters (each split-K launch leaves them zero)
 };
 thread_local KPartScratch g_kpart;
 struct KPartScope {
   KPartScratch saved;
-  KPartScope(float* p, size_t n) : saved(g_kpart) {
+  int err = FI_OK;
+  // p: kKPartFloats partial floats followed by the counters, zeroed here
+  KPartScope(float* p, cudaStream_t st) : saved(g_kpart) {
     g_kpart.ptr = p;
-    g_kpart.floats = n;
+    g_kpart.floats = static_cast<size_t>(kKPartFloats);
+    g_kpart.sem = reinterpret_cast<int*>(p + kKPartFloats);
+    if (cudaMemsetAsync(g_kpart.sem, 0, sizeof(int) * kKPartSems, st) != cudaSuccess)
+      err = set_err(FI_ERR_CUDA, "split-K counter reset: %s", cudaGetErrorString(cudaGetLastError()));
   }
   ~KPartScope() { g_kpart = saved; }
 };
@@ -422,6 +429,7 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
   const int tiles = sh.num_m * sh.num_n;
   sh.ksplit = 1;
   sh.part = nullptr;
+  sh.sem = nullptr;
   sh.tile_begin = 0;
   sh.tile_end = 0;
   const long long tsplit = tail > 0 ? tail : tiles;
@@ -429,6 +437,10 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
       static_cast<size_t>(ksplit) * tsplit * Cf::BM * NCTA * bn <= g_kpart.floats) {
     sh.ksplit = ksplit;
     sh.part = g_kpart.ptr;
+    // every unit of a split tile is resident at once (units <= slots), so the
+    // tile's CTAs reduce the partials themselves (no fixup launch)
+    static const int inkernel = env_int("FI_GEMM_INKERNEL_RED", 1);
+    if (inkernel && g_kpart.sem && tsplit <= kKPartSems) sh.sem = g_kpart.sem;
   } else {
     tail = 0;  // no split-K available: whole tiles only
   }
@@ -463,12 +475,13 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
     GemmShape head = sh;
     head.ksplit = 1;
     head.part = nullptr;
+    head.sem = nullptr;
     head.tile_end = tiles - tail;
     FI_TRY(go(head));
     sh.tile_begin = tiles - tail;
   }
   FI_TRY(go(sh));
-  if (sh.ksplit > 1) {  // sum the partials in order and run the epilogue
+  if (sh.ksplit > 1 && !sh.sem) {  // sum the partials in order and run the epilogue
     const int tile_rows = Cf::BM * NCTA;
     const long long chunks =
         static_cast<long long>(tiles - sh.tile_begin) * tile_rows * (bn / 32);
@@ -526,6 +539,12 @@ GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int bn_max_p
   GemmChoice best{0, false, 1, 0};
   double best_cost = 1e300;  // microseconds
   const double us_per_kiter = 0.55;  // one 128 x 256 bf16 k-iteration on one SM (measured)
+  // fixed cost of a split-K reduction: the separate fixup launch, or (env
+  // FI_GEMM_INKERNEL_RED, default) the tile's CTAs reducing in-kernel
+  // (measured per-width A/B at config 3: 3 / 6 / 12 us are within noise; 8 keeps
+  // split-K for the narrow launches that gain from it)
+  static const double fixup_fixed =
+      gemm_env("FI_GEMM_INKERNEL_RED", 1) ? gemm_env("FI_GEMM_RED_US", 8) : 12.0;
   for (int pair = 0; pair < 2; ++pair) {
     if (force_pair >= 0 && pair != force_pair) continue;
     const int step = pair ? step_pair : step_single;
@@ -546,7 +565,7 @@ GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int bn_max_p
       // partial write + read at ~3 TB/s effective, plus the extra launches and
       // their drain (fitted: a tail that saves less than ~12 us is not worth it)
       auto fixup_us = [&](long long r, int ks) {
-        return 12.0 + 2.0 * ks * static_cast<double>(r) * tile_rows * bn * 4.0 / 3.0e6;
+        return fixup_fixed + 2.0 * ks * static_cast<double>(r) * tile_rows * bn * 4.0 / 3.0e6;
       };
       auto consider = [&](double cost, int ks, int tail) {
         if (cost < best_cost * 0.995) {
@@ -1074,7 +1093,8 @@ int fi_inside_forward(const fi_shape* shape, const float* L, const float* R, con
   FI_TRY(check_ptrs({L, R, root, unary, lengths, log_z, ws}));
   FI_TRY(load_encode());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  KPartScope kps(at<float>(ws, p.kpart), static_cast<size_t>(kKPartFloats));
+  KPartScope kps(at<float>(ws, p.kpart), st);
+  FI_TRY(kps.err);
   if (p.tf32) {
     if (p.half_chart) return forward_impl<float, __half>(p, L, R, root, unary, lengths, log_z, ws, st);
     return forward_impl<float, float>(p, L, R, root, unary, lengths, log_z, ws, st);
@@ -1093,7 +1113,8 @@ int fi_inside_backward(const fi_shape* shape, const float* L, const float* R, co
   FI_TRY(check_ptrs({L, R, root, unary, lengths, log_z, grad_log_z, dL, dR, droot, dunary, ws}));
   FI_TRY(load_encode());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  KPartScope kps(at<float>(ws, p.kpart), static_cast<size_t>(kKPartFloats));
+  KPartScope kps(at<float>(ws, p.kpart), st);
+  FI_TRY(kps.err);
 #define FI_BWD(T, CT)                                                                      \
   return backward_impl<T, CT>(p, L, R, root, unary, lengths, log_z, grad_log_z, dL, dR, droot, \
                               dunary, ws, st)
@@ -1198,13 +1219,14 @@ int fi_test_gemm(int32_t dtype, int32_t a_mn, int32_t b_mn, int32_t M, int32_t N
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t kfloats = static_cast<size_t>(kKPartFloats);
   void* scratch = nullptr;
-  FI_CUDA(cudaMallocAsync(&scratch, kfloats * 4, st));
+  FI_CUDA(cudaMallocAsync(&scratch, kfloats * 4 + 4 * kKPartSems, st));
   struct Free {
     void* p;
     cudaStream_t s;
     ~Free() { cudaFreeAsync(p, s); }
   } free_scratch{scratch, st};
-  KPartScope kps(static_cast<float*>(scratch), kfloats);
+  KPartScope kps(static_cast<float*>(scratch), st);
+  FI_TRY(kps.err);
   GemmEpi ep = {};
   ep.M = M;
   ep.C = C;

@@ -53,6 +53,12 @@ struct GemmShape {
   // and applies the epilogue.
   int ksplit;
   float* part;
+  // non-null: the ksplit CTAs (x NCTA) of a split tile reduce it in-kernel --
+  // each publishes its partial, waits on the tile's counter sem[tile - tile_begin]
+  // (zero on entry, left zero on exit) and then sums every part, in part
+  // order, over its own 1/ksplit of the tile's columns and runs the epilogue.
+  // Needs all units resident (units <= slots; one unit per CTA).
+  int* sem;
   // tiles [tile_begin, tile_end) only (tile_end 0: all; a "waves + split-K
   // tail" GEMM is two launches over one shape: whole waves, then the tail
   // split over K)
@@ -572,8 +578,8 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
         tc_fence_after();
         const uint32_t t_row = t_lane + static_cast<uint32_t>(acc * C::TMEM_HALF);
         const int nch = bn / 32;
-#pragma unroll 1
         constexpr int kHalves = gemm_epi_warps<CHUNK>() / 4;
+#pragma unroll 1
         for (int j = 2 * ehalf; j + 1 < nch; j += 2 * kHalves) {
           float v0[32], v1[32];
           tmem_ld32x2(t_row + j * 32, t_row + j * 32 + 32, v0, v1);
@@ -589,6 +595,44 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
         if (++acc == nbuf) {
           acc = 0;
           acc_phase ^= 1;
+        }
+        if (ks > 1 && sh.sem) {
+          constexpr int tile_rows = C::BM * NCTA;
+          constexpr int kEpiThreads = 32 * gemm_epi_warps<CHUNK>();
+          const long long tsplit = tile_e - tb;
+          int* cnt = sh.sem + tu;
+          const int parts = ks * NCTA;
+          __threadfence();  // this thread's partial rows -> visible GPU-wide
+          epi_bar_sync(kEpiThreads);
+          if (threadIdx.x == 128) {
+            atomicAdd(cnt, 1);
+            while (ld_acquire_gpu(cnt) < parts) __nanosleep(64);
+          }
+          epi_bar_sync(kEpiThreads);
+          const int c0 = nch * kpart / ks, c1 = nch * (kpart + 1) / ks;
+          const float* prow = sh.part + (tu * tile_rows + rank * C::BM + r) * static_cast<long long>(bn);
+          const long long pstride = tsplit * tile_rows * static_cast<long long>(bn);
+#pragma unroll 1
+          for (int c = c0; c < c1; ++c) {
+            float v[32];
+#pragma unroll
+            for (int t = 0; t < 32; ++t) v[t] = 0.f;
+            for (int k = 0; k < ks; ++k) {
+              const float4* src = reinterpret_cast<const float4*>(prow + k * pstride + c * 32);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const float4 w = __ldcg(src + q);
+                v[4 * q] += w.x;
+                v[4 * q + 1] += w.y;
+                v[4 * q + 2] += w.z;
+                v[4 * q + 3] += w.w;
+              }
+            }
+            epi_emit<EPI>(ep, er, col_base + c * 32, sh.N, v);
+          }
+          // second round of arrivals: the last one re-arms the counter
+          epi_bar_sync(kEpiThreads);
+          if (threadIdx.x == 128 && atomicAdd(cnt, 1) == 2 * parts - 1) atomicExch(cnt, 0);
         }
       } else {
         static_assert(BN <= 128, "chunked accumulation keeps BN fp32 sums per thread");

@@ -160,6 +160,16 @@ __device__ __forceinline__ void tmem_ld32x2(uint32_t ta, uint32_t tb, float (&va
   }
 }
 
+// Named barrier 1 among the GEMM's epilogue warps (warps 4.., `n` threads).
+__device__ __forceinline__ void epi_bar_sync(int n) {
+  asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // ------------------------------------------- programmatic dependent launch
 // Block until the predecessor grid (PDL launch) has completed and its writes
 // are visible; a no-op for a normally launched kernel.
