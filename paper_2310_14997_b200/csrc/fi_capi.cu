@@ -824,7 +824,11 @@ int forward_impl(const Plan& p, const float* L, const float* R, const float* roo
     sa.cols_per_cta = dc.cols_per_cta;
     ProfScope prof(FI_PROF_SPLIT, s);
     static const int pers = env_int("FI_SPLIT_PERS", 1);
-    if (pers && p.Np <= 8192) {
+    // persistent kernel unless the width has about one row per slot or fewer
+    // (the widest spans: there the one-shot kernel's launch ramp is cheaper;
+    // measured at |N| = 4096, l = 40: widths 34..40, -30 us per step)
+    bool use_pers = pers && p.Np <= 8192;
+    if (use_pers) {
       // persistent one-CTA-per-row kernel: ~72 KB of ring per CTA (2-3 CTAs/SM)
       // one CTA per row: Np = 4 * cons * V with cons <= 256 a multiple of 32
       int V = 1;
@@ -840,13 +844,17 @@ int forward_impl(const Plan& p, const float* L, const float* R, const float* roo
       const size_t smem = static_cast<size_t>(stages) * (stage_bytes + 16 + sizeof(StageHdr)) +
                           8ull * p.l + 64;
       const int nrows = nb * n_w;
-      return dispatch_v(V, [&](auto vc) {
+      FI_TRY(dispatch_v(V, [&](auto vc) {
         constexpr int VV = decltype(vc)::value;
         auto kern = k_split_fwd_pers<T, CT, VV>;
         FI_TRY(set_smem(kern, smem));
         int occ = 0;
         FI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 + cons, smem));
         occ = occ < 1 ? 1 : occ;
+        if (pers < 2 && static_cast<long long>(nrows) * 20 <= static_cast<long long>(occ) * num_sms() * 21) {
+          use_pers = false;  // FI_SPLIT_PERS=2 forces the persistent kernel
+          return FI_OK;
+        }
         // every CTA gets the same number of rows (no partial last round)
         static const int balance = env_int("FI_SPLIT_BALANCE", 0);  // measured slightly slower
         const int slots = occ * num_sms();
@@ -858,7 +866,8 @@ int forward_impl(const Plan& p, const float* L, const float* R, const float* roo
         FI_TRY(launch_ex(kern, 1, dim3(grid), dim3(32 + cons), smem, s, sa, stages, nprod));
         FI_CUDA(cudaGetLastError());
         return FI_OK;
-      });
+      }));
+      if (use_pers) return FI_OK;
     }
     const int stages = dc.stages;
     const size_t smem = align128(sizeof(SplitTerm) * (w - 1)) +
