@@ -1,8 +1,8 @@
+# Round-end measurement, part B: full ncu captures of the dgrad and wgrad GEMMs
+# (launch IDs from part A's pick10.txt, passed as arguments).
 mkdir -p gpurun_out
-SECONDS=0
-timeout 900 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err
-echo "bench wall ${SECONDS}s"
-python scripts/bj.py final < gpurun_out/bench_final.json
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gemm -s 99 -c 1 -o gpurun_out/prof_gemm_fwd python scripts/profile_step.py --steps 2 > /dev/null 2>&1; echo "ncu gemm rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_gemm<" -s 150 -c 1 -o gpurun_out/prof_gemm_dgrad python scripts/profile_step.py --steps 2 > /dev/null 2>&1; echo "ncu gemm rc=$?"
+P='python scripts/profile_step.py --steps 2'
+cap() { timeout 900 ncu --set full --clock-control none --import-source on -s $2 -c 1 -o gpurun_out/prof_$1 $P > /dev/null 2>&1; echo "ncu $1 rc=$?"; }
+cap gemm_dgrad $1
+cap gemm_wgrad $2
 du -sh gpurun_out

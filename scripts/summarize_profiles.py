@@ -127,6 +127,13 @@ def traffic(kernels: list[dict], n: int, batch: int, length: int, esz: int,
             d["algorithmic_bytes"] = fn(n, batch, length, width, esz, chart_esz)
             d["dram_over_algorithmic"] = d["dram_bytes"] / d["algorithmic_bytes"]
             d["achieved_gbs_under_ncu"] = d["algorithmic_bytes"] / (k["time_ms"] * 1e-3) / 1e9
+        if cls in ("gemm_fwd", "gemm_dgrad") and widths.get("gemm"):
+            # the captured launch's width: M = batch * (l - w + 1) rows, K x N = N x 2N
+            w = widths["gemm"]
+            flops = 2.0 * batch * (length - w + 1) * (2 * n) * n
+            d["width"] = w
+            d["algorithmic_tflop"] = flops / 1e12
+            d["achieved_tflops_under_ncu"] = flops / (k["time_ms"] * 1e-3) / 1e12
         out[cls] = d
     return out
 
@@ -141,6 +148,7 @@ def main():
     ap.add_argument("--chart-esz", type=int, default=2, help="a/b chart bytes (fp16 2, fp32 4)")
     ap.add_argument("--split-width", type=int, default=20, help="width of the captured split launch")
     ap.add_argument("--gather-width", type=int, default=20, help="child width of the captured gather")
+    ap.add_argument("--gemm-width", type=int, default=0, help="width of the captured fwd / dgrad GEMM launches")
     ap.add_argument("--launches")
     ap.add_argument("--reps", nargs="*", default=[])
     args = ap.parse_args()
@@ -158,7 +166,8 @@ def main():
         for k in kernels:
             print(json.dumps(k))
         tr = traffic(kernels, args.n, args.batch, args.length, args.esz, args.chart_esz,
-                     {"split_fwd": args.split_width, "gather_bwd": args.gather_width})
+                     {"split_fwd": args.split_width, "gather_bwd": args.gather_width,
+                      "gemm": args.gemm_width})
         (prof / "ncu_traffic.json").write_text(json.dumps(tr, indent=1))
         print(json.dumps(tr, indent=1))
 
