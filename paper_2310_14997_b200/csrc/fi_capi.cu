@@ -244,7 +244,8 @@ int make_plan(const fi_shape* s, Plan* p) {
   p->topz = take(4ull * p->B);
   p->wsum = take(16);
   p->flag = take(256);
-  p->kpart = take(4ull * kKPartFloats + 4ull * kKPartSems);  // split-K partial tiles + counters
+  // split-K partial tiles + counters, one region per concurrent stream (dual sweep)
+  p->kpart = take(2 * (4ull * kKPartFloats + 4ull * kKPartSems));
   p->total = off;
   return FI_OK;
 }
@@ -361,20 +362,37 @@ struct KPartScratch {
   float* ptr = nullptr;
   size_t floats = 0;
   int* sem = nullptr;  // kKPartSems zeroed tile counters (each split-K launch leaves them zero)
+  float* region[2] = {nullptr, nullptr};  // per-stream regions (dual sweep: one per half)
 };
 thread_local KPartScratch g_kpart;
+constexpr long long kKPartRegion = kKPartFloats + kKPartSems;  // floats per region
 struct KPartScope {
   KPartScratch saved;
   int err = FI_OK;
-  // p: kKPartFloats partial floats followed by the counters, zeroed here
-  KPartScope(float* p, cudaStream_t st) : saved(g_kpart) {
-    g_kpart.ptr = p;
+  // p: `regions` x (kKPartFloats partial floats + the counters, zeroed here)
+  KPartScope(float* p, cudaStream_t st, int regions) : saved(g_kpart) {
+    for (int k = 0; k < 2; ++k) g_kpart.region[k] = p + (k < regions ? k : 0) * kKPartRegion;
+    select(0);
+    for (int k = 0; k < regions && err == FI_OK; ++k)
+      if (cudaMemsetAsync(p + k * kKPartRegion + kKPartFloats, 0, sizeof(int) * kKPartSems, st) !=
+          cudaSuccess)
+        err = set_err(FI_ERR_CUDA, "split-K counter reset: %s",
+                      cudaGetErrorString(cudaGetLastError()));
+  }
+  static void select(int k) {
+    g_kpart.ptr = g_kpart.region[k];
     g_kpart.floats = static_cast<size_t>(kKPartFloats);
-    g_kpart.sem = reinterpret_cast<int*>(p + kKPartFloats);
-    if (cudaMemsetAsync(g_kpart.sem, 0, sizeof(int) * kKPartSems, st) != cudaSuccess)
-      err = set_err(FI_ERR_CUDA, "split-K counter reset: %s", cudaGetErrorString(cudaGetLastError()));
+    g_kpart.sem = reinterpret_cast<int*>(g_kpart.region[k] + kKPartFloats);
   }
   ~KPartScope() { g_kpart = saved; }
+};
+struct KPartSelect {  // launches of one half of a dual sweep use that half's region
+  float* saved;
+  explicit KPartSelect(int k) : saved(g_kpart.ptr) { KPartScope::select(k); }
+  ~KPartSelect() {
+    g_kpart.ptr = saved;
+    g_kpart.sem = reinterpret_cast<int*>(saved + kKPartFloats);
+  }
 };
 
 // GEMM smem ring depth for launches enqueued by this thread: 0 = the deepest
@@ -713,13 +731,22 @@ struct Halves {
   cudaStream_t st[2] = {nullptr, nullptr};
 };
 
+// FI_DUAL_ROWS = R > 0: launches of at most R rows (the narrow end of each
+// sweep: wide spans in the forward, wide children first in the backward)
+// run as two half-batch chains on two streams, so one half's bandwidth
+// kernel overlaps the other half's GEMM where neither fills the GPU alone.
+// (FI_DUAL = 1: every width, measured slower -- contention.)
+long long dual_rows() {
+  static const long long r = env_int("FI_DUAL", 0) ? (1LL << 40) : env_int("FI_DUAL_ROWS", 0);
+  return r;
+}
+
 int make_halves(const Plan& p, cudaStream_t st, Halves* h) {
-  static const int dual = env_int("FI_DUAL", 0);  // measured slower (contention), opt-in
   h->st[0] = st;
   h->b0[0] = 0;
   h->nb[0] = p.B;
   h->n = 1;
-  if (!dual || p.B < 2) return FI_OK;
+  if (dual_rows() <= 0 || p.B < 2) return FI_OK;
   int err = 0;
   cudaStream_t s2 = aux_stream(err);
   if (err || !s2) return set_err(FI_ERR_CUDA, "cannot create the auxiliary stream");
@@ -728,7 +755,10 @@ int make_halves(const Plan& p, cudaStream_t st, Halves* h) {
   h->nb[0] = p.B / 2;
   h->b0[1] = p.B / 2;
   h->nb[1] = p.B - p.B / 2;
-  return stream_wait(s2, st);  // the second stream starts after everything before
+  return FI_OK;  // the caller makes the second stream wait when its dual phase starts
+}
+bool dual_width(const Halves& h, const Plan& p, int w) {
+  return h.n > 1 && static_cast<long long>(p.B) * (p.l - w + 1) <= dual_rows();
 }
 
 struct GemmStagesScope {  // cap the GEMM ring for this thread's launches
@@ -888,20 +918,26 @@ int forward_impl(const Plan& p, const float* L, const float* R, const float* roo
 
   Halves h;
   FI_TRY(make_halves(p, st, &h));
-  GemmStagesScope gs(dual_gemm_stages(h));
-  // width 1 GEMMs; the second stream trails the first by one launch
-  FI_TRY(gemm(1, h.b0[0], h.nb[0], h.st[0]));
-  if (h.n > 1) {
-    FI_TRY(stream_wait(h.st[1], h.st[0]));
-    FI_TRY(gemm(1, h.b0[1], h.nb[1], h.st[1]));
-  }
+  FI_TRY(gemm(1, 0, p.B, st));
+  bool dual = false;  // from the first narrow width on, two half-batch chains
   for (int w = 2; w <= p.l; ++w) {
-    for (int k = 0; k < h.n; ++k) {
+    if (!dual && dual_width(h, p, w)) {
+      FI_TRY(stream_wait(h.st[1], st));
+      dual = true;
+    }
+    if (!dual) {
+      FI_TRY(split(w, 0, p.B, st));
+      if (w < p.l) FI_TRY(gemm(w, 0, p.B, st));
+      continue;
+    }
+    GemmStagesScope gs(dual_gemm_stages(h));
+    for (int k = 0; k < 2; ++k) {
+      KPartSelect kp(k);
       FI_TRY(split(w, h.b0[k], h.nb[k], h.st[k]));
       if (w < p.l) FI_TRY(gemm(w, h.b0[k], h.nb[k], h.st[k]));
     }
   }
-  if (h.n > 1) FI_TRY(stream_wait(st, h.st[1]));  // join: the caller's stream sees all
+  if (dual) FI_TRY(stream_wait(st, h.st[1]));  // join: the caller's stream sees all
   return FI_OK;
 }
 
@@ -1012,19 +1048,34 @@ int backward_impl(const Plan& p, const float* L, const float* R, const float* ro
   {
     Halves h;
     FI_TRY(make_halves(p, st, &h));
-    GemmStagesScope gs(dual_gemm_stages(h));
-    FI_TRY(gather(p.l - 1, h.b0[0], h.nb[0], h.st[0]));
-    if (h.n > 1) {  // the second stream trails the first by one launch
-      FI_TRY(stream_wait(h.st[1], h.st[0]));
-      FI_TRY(gather(p.l - 1, h.b0[1], h.nb[1], h.st[1]));
+    // the narrow (wide-child) launches come first: two half-batch chains
+    // until the child width's rows exceed the threshold, then one
+    bool dual = dual_width(h, p, p.l - 1);
+    if (dual) {
+      FI_TRY(stream_wait(h.st[1], st));
+      GemmStagesScope gs(dual_gemm_stages(h));
+      for (int k = 0; k < 2; ++k) FI_TRY(gather(p.l - 1, h.b0[k], h.nb[k], h.st[k]));
+    } else {
+      FI_TRY(gather(p.l - 1, 0, p.B, st));
     }
     for (int m = p.l - 1; m >= 1; --m) {
-      for (int k = 0; k < h.n; ++k) {
+      if (dual && !dual_width(h, p, m)) {
+        FI_TRY(stream_wait(st, h.st[1]));  // join before the first full-batch launch
+        dual = false;
+      }
+      if (!dual) {
+        FI_TRY(dgrad(m, 0, p.B, st));
+        if (m > 1) FI_TRY(gather(m - 1, 0, p.B, st));
+        continue;
+      }
+      GemmStagesScope gs(dual_gemm_stages(h));
+      for (int k = 0; k < 2; ++k) {
+        KPartSelect kp(k);
         FI_TRY(dgrad(m, h.b0[k], h.nb[k], h.st[k]));
         if (m > 1) FI_TRY(gather(m - 1, h.b0[k], h.nb[k], h.st[k]));
       }
     }
-    if (h.n > 1) FI_TRY(stream_wait(st, h.st[1]));
+    if (dual) FI_TRY(stream_wait(st, h.st[1]));
   }
 
   // weight gradients: dW = G^T E summed over every span, then * exp(table)
@@ -1102,7 +1153,7 @@ int fi_inside_forward(const fi_shape* shape, const float* L, const float* R, con
   FI_TRY(check_ptrs({L, R, root, unary, lengths, log_z, ws}));
   FI_TRY(load_encode());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  KPartScope kps(at<float>(ws, p.kpart), st);
+  KPartScope kps(at<float>(ws, p.kpart), st, 2);
   FI_TRY(kps.err);
   if (p.tf32) {
     if (p.half_chart) return forward_impl<float, __half>(p, L, R, root, unary, lengths, log_z, ws, st);
@@ -1122,7 +1173,7 @@ int fi_inside_backward(const fi_shape* shape, const float* L, const float* R, co
   FI_TRY(check_ptrs({L, R, root, unary, lengths, log_z, grad_log_z, dL, dR, droot, dunary, ws}));
   FI_TRY(load_encode());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  KPartScope kps(at<float>(ws, p.kpart), st);
+  KPartScope kps(at<float>(ws, p.kpart), st, 2);
   FI_TRY(kps.err);
 #define FI_BWD(T, CT)                                                                      \
   return backward_impl<T, CT>(p, L, R, root, unary, lengths, log_z, grad_log_z, dL, dR, droot, \
@@ -1228,13 +1279,13 @@ int fi_test_gemm(int32_t dtype, int32_t a_mn, int32_t b_mn, int32_t M, int32_t N
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t kfloats = static_cast<size_t>(kKPartFloats);
   void* scratch = nullptr;
-  FI_CUDA(cudaMallocAsync(&scratch, kfloats * 4 + 4 * kKPartSems, st));
+  FI_CUDA(cudaMallocAsync(&scratch, 4 * kKPartRegion, st));
   struct Free {
     void* p;
     cudaStream_t s;
     ~Free() { cudaFreeAsync(p, s); }
   } free_scratch{scratch, st};
-  KPartScope kps(static_cast<float*>(scratch), st);
+  KPartScope kps(static_cast<float*>(scratch), st, 1);
   FI_TRY(kps.err);
   GemmEpi ep = {};
   ep.M = M;
