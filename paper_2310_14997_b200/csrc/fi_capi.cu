@@ -1277,7 +1277,6 @@ int fi_test_gemm(int32_t dtype, int32_t a_mn, int32_t b_mn, int32_t M, int32_t N
   if (M < 1 || N < 64 || N % 64 || K < 1)
     return set_err(FI_ERR_ARG, "test GEMM needs M>=1, N%%64==0, K>=1");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const size_t kfloats = static_cast<size_t>(kKPartFloats);
   void* scratch = nullptr;
   FI_CUDA(cudaMallocAsync(&scratch, 4 * kKPartRegion, st));
   struct Free {
