@@ -557,12 +557,15 @@ GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int bn_max_p
   GemmChoice best{0, false, 1, 0};
   double best_cost = 1e300;  // microseconds
   const double us_per_kiter = 0.55;  // one 128 x 256 bf16 k-iteration on one SM (measured)
-  // fixed cost of a split-K reduction: the separate fixup launch, or (env
-  // FI_GEMM_INKERNEL_RED, default) the tile's CTAs reducing in-kernel
-  // (measured per-width A/B at config 3: 3 / 6 / 12 us are within noise; 8 keeps
-  // split-K for the narrow launches that gain from it)
-  static const double fixup_fixed =
-      gemm_env("FI_GEMM_INKERNEL_RED", 1) ? gemm_env("FI_GEMM_RED_US", 8) : 12.0;
+  // split-K reduction cost.  Whole-tile split (small M): fitted, partials at
+  // ~3 TB/s plus a fixed 8 us (12 with the separate fixup kernel,
+  // FI_GEMM_INKERNEL_RED=0).  Split tail of a multi-wave launch (the tile's
+  // CTAs reduce in-kernel): a handshake plus each CTA's own partial rows
+  // written and read at the per-SM fill rate (~60 GB/s: 2 x 128 x bn x 4 B)
+  // -- measured at config 3: 256 x 512 tails for the dgrad at M >= 2368
+  // (-10..-25 us each) and the wgrad (-0.18 ms), while 256 x 512 whole-tile
+  // splits at small M measured slower (kept to N tiles <= 256 there).
+  static const bool inkernel_red = gemm_env("FI_GEMM_INKERNEL_RED", 1) != 0;
   for (int pair = 0; pair < 2; ++pair) {
     if (force_pair >= 0 && pair != force_pair) continue;
     const int step = pair ? step_pair : step_single;
@@ -576,15 +579,16 @@ GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int bn_max_p
       const long long T = mt * ((N + bn - 1) / bn);
       const double t = us_per_kiter * (pair ? gemm_t_pair(bn) : gemm_t_single(bn));
       // split-K over `units` tiles of which `r` are split: feasibility and fixup cost
-      auto ks_ok = [&](long long r, int ks) {
-        return allow_ksplit && force_ks != 1 && bn <= 256 && r * ks <= slots && k_iters / ks >= 4 &&
+      auto ks_ok = [&](long long r, int ks, bool tail_split) {
+        return allow_ksplit && force_ks != 1 && (tail_split ? inkernel_red : bn <= 256) &&
+               r * ks <= slots && k_iters / ks >= 4 &&
                static_cast<double>(ks) * r * tile_rows * bn <= static_cast<double>(g_kpart.floats);
       };
-      // partial write + read at ~3 TB/s effective, plus the extra launches and
-      // their drain (fitted: a tail that saves less than ~12 us is not worth it)
-      auto fixup_us = [&](long long r, int ks) {
-        return fixup_fixed + 2.0 * ks * static_cast<double>(r) * tile_rows * bn * 4.0 / 3.0e6;
+      auto fixup_us = [&](long long r, int ks) {  // whole-tile split
+        return (inkernel_red ? 8.0 : 12.0) +
+               2.0 * ks * static_cast<double>(r) * tile_rows * bn * 4.0 / 3.0e6;
       };
+      const double tail_red_us = 3.0 + 2.0 * 128 * bn * 4.0 / 60.0e3;
       auto consider = [&](double cost, int ks, int tail) {
         if (cost < best_cost * 0.995) {
           best_cost = cost;
@@ -592,9 +596,9 @@ GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int bn_max_p
         }
       };
       // whole tiles, optionally all split over K (small M: fewer tiles than slots)
-      const bool forced = force_ks > 1 && ks_ok(T, force_ks);
+      const bool forced = force_ks > 1 && ks_ok(T, force_ks, false);
       for (int ks = 1; ks <= 8; ++ks) {
-        if (ks > 1 && !ks_ok(T, ks)) break;
+        if (ks > 1 && !ks_ok(T, ks, false)) break;
         if (forced && ks != force_ks) continue;
         double cost = static_cast<double>((T * ks + slots - 1) / slots) *
                       (((k_iters + ks - 1) / ks) * t + gemm_epi_serial(bn));
@@ -605,9 +609,11 @@ GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int bn_max_p
       const long long r = T % slots;
       if (!no_tail && T > slots && r > 0 && force_ks != 1) {
         for (int ks = 2; ks <= 8; ++ks) {
-          if (!ks_ok(r, ks)) break;
-          const double cost = static_cast<double>(T / slots) * k_iters * t +
-                              static_cast<double>((k_iters + ks - 1) / ks) * t + fixup_us(r, ks);
+          if (!ks_ok(r, ks, true)) break;
+          // (+3 us: the tail is a second launch)
+          const double cost = static_cast<double>(T / slots) * (k_iters * t + gemm_epi_serial(bn)) +
+                              static_cast<double>((k_iters + ks - 1) / ks) * t +
+                              gemm_epi_serial(bn) + tail_red_us + 3.0;
           consider(cost, ks, static_cast<int>(r));
         }
       }
