@@ -25,6 +25,9 @@ CASES = [  # M, N, K
     (1344, 8192, 4096),
     (1216, 8192, 4096),
     (1600, 4096, 8192),
+    # whole waves of 256 x 512 tiles + a split-K tail reduced in-kernel
+    (2432, 4096, 8192),
+    (8192, 4096, 2560),
 ]
 
 
