@@ -8,8 +8,13 @@
 // i.e. the K index is the outer, strided dimension).  One elected thread
 // issues tcgen05.mma (K=16 for bf16 / 8 for tf32) into one of two TMEM
 // accumulators, so the epilogue of tile t overlaps the main loop of tile
-// t+1.  The epilogue reads TMEM with tcgen05.ld and applies one of the
-// inside-algorithm transforms (see EpiMode) before writing to HBM.
+// t+1 (N tiles up to 256).  N tiles of 320..512 (BN = 512 kernels, pairs
+// only) issue two MMAs per K step (sub-tiles of 256 + the rest) into one
+// TMEM-filling accumulator: 25% fewer operand bytes per flop than 256-wide
+// tiles, which are bound by the per-SM L2 -> shared fill rate, at the cost
+// of a serialized epilogue.  The epilogue reads TMEM with tcgen05.ld and
+// applies one of the inside-algorithm transforms (see EpiMode) before
+// writing to HBM.
 //
 // PAIR: a cluster of two CTAs (one TPC) computes a 256 x bn tile with
 // tcgen05.mma.cta_group::2 -- each CTA stages its own 128 rows of A and
@@ -49,8 +54,9 @@ struct GemmShape {
   // split-K (ksplit > 1): work unit u = (tile tile_begin + u / ksplit, K part
   // u % ksplit); each unit stores its raw fp32 partial tile, dense
   // (tile_rows x bn), at part + ((kpart * T_split + tile - tile_begin) *
-  // tile_rows * bn); k_gemm_fixup sums the parts in order (deterministic)
-  // and applies the epilogue.
+  // tile_rows * bn); the parts are summed in order (deterministic) by the
+  // tile's own CTAs (sem != null, below) or by k_gemm_fixup, which then
+  // apply the epilogue.
   int ksplit;
   float* part;
   // non-null: the ksplit CTAs (x NCTA) of a split tile reduce it in-kernel --
@@ -237,7 +243,7 @@ __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int lrow, long long
 }
 
 // Per-row epilogue state: where row `lrow` of this GEMM goes and what the
-// fused transform needs (shared by the GEMM epilogue and the split-K fixup).
+// fused transform needs (shared by the GEMM epilogue and the split-K reductions).
 struct EpiRow {
   float* rowptr;    // row base (EPI_FWD/_H: the a row)
   float* rowptr_b;  // EPI_FWD/_H: the b row
@@ -560,7 +566,7 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
       };
       auto emit = [&](int j, const float (&v)[32]) {
         const int tc = tile_col(j);
-        if (ks > 1) {  // split-K: raw fp32 partial, summed + transformed by k_gemm_fixup
+        if (ks > 1) {  // split-K: raw fp32 partial, summed + transformed below / by k_gemm_fixup
           constexpr int tile_rows = C::BM * NCTA;
           const long long tsplit = tile_e - tb;
           float4* dst = reinterpret_cast<float4*>(
@@ -676,7 +682,8 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
   }
 }
 
-// Split-K fixup: sum the ksplit raw partials of every (row, 32-column chunk)
+// Split-K fixup (FI_GEMM_INKERNEL_RED=0, or more split tiles than counters):
+// sum the ksplit raw partials of every (row, 32-column chunk)
 // of the tiles [tile_begin, T) in part order and run the launch's epilogue.
 // One thread per chunk; a tile is tile_rows x bn (bn a multiple of 32).
 template <int EPI>
