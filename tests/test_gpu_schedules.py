@@ -1,0 +1,54 @@
+"""The engine's opt-in launch schedules (environment switches read once per
+process, so each runs in a fresh interpreter) give the same results as the
+default schedule: the oracle at a small size and, for the split-K / dual
+paths, at |N| = 1024 against the float64 oracle."""
+
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parent.parent
+
+CHILD = r"""
+import json, sys
+import numpy as np
+sys.path[:0] = ['.', 'tests']
+from test_gpu_parity import make_case, run_op, rel_err
+from oracle import flashinside_oracle as O
+out = {}
+for name, (N, P, V, B, lmax, seed, lengths) in {
+        "small": (64, 64, 64, 8, 20, 0, None),
+        "n1024": (1024, 1024, 64, 6, 14, 3, [14, 9, 14, 12, 5, 14])}.items():
+    root, left, right, emit, unary, lens, _ = make_case(N, P, V, B, lmax, seed, lengths)
+    grad = -np.ones(B) / B
+    want = O.inside_batch(left, right, root, unary, lens, grad)
+    got = run_op(root, left, right, unary, lens, grad, "bf16")
+    out[name] = {k: rel_err(got[k], want[k]) for k in ("dL", "dR", "droot", "dunary")}
+    out[name]["log_z"] = float(np.abs(got["log_z"] / want["log_z"] - 1).max())
+print(json.dumps(out))
+"""
+
+
+@pytest.mark.parametrize("env", [
+    {"FI_DUAL_ROWS": "48"},                       # narrow launches as two half-batch chains
+    {"FI_DUAL": "1"},                             # every launch as two chains
+    {"FI_GEMM_INKERNEL_RED": "0", "FI_GEMM_KSPLIT": "2"},  # split-K through the fixup kernel
+    {"FI_GEMM_KSPLIT": "4"},                      # split-K reduced in-kernel
+    {"FI_SPLIT_PERS": "0"},                       # one-shot split kernel at every width
+    {"FI_SPLIT_PERS": "2"},                       # persistent split kernel at every width
+    {"FI_PDL": "0"},
+], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+def test_schedule_matches_oracle(env):
+    res = subprocess.run([sys.executable, "-c", CHILD], cwd=ROOT, capture_output=True, text=True,
+                         env={**os.environ, **env}, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    errs = json.loads(res.stdout.strip().splitlines()[-1])
+    for case, e in errs.items():
+        for k, v in e.items():
+            assert v < 2e-3, f"{env} {case} {k}: {v:.2e}"
