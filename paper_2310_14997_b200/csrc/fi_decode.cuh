@@ -154,6 +154,140 @@ __global__ void __launch_bounds__(256) k_trop_gemm(const float* __restrict__ A, 
   }
 }
 
+// Register-tiled tropical GEMM for the Viterbi projections, both tables in
+// one launch:  out[r, c] = max_k A[r, k] + W(c)[k]  with W(c) = W0 row c for
+// c < Nhalf (-> outA) and W1 row c - Nhalf (-> outB).  BM x 128 tiles,
+// K slices of 16 staged in shared memory as k-PAIRS ([k/2][row][k%2]; the
+// next slice prefetched into registers during the current one), 256 threads
+// with (BM/16) x 8 results each in 4 x 4 blocks (rows ty*4 (+BM/2), cols
+// tx*4 (+64)).  Two K steps of one result cost one packed FADD2 (the two
+// sums) and one three-input FMNMX3 (sm_100): 1 instruction per max-plus op
+// instead of 2.  `vec`: A, W rows 16-B aligned (float4 global loads).
+__device__ __forceinline__ float2 trop_add2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)),
+        "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float trop_max3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+template <int BM>
+__global__ void __launch_bounds__(256, BM == 64 ? 2 : 1) k_trop_gemm2(const float* __restrict__ A, int lda,
+                                                    const float* __restrict__ W0,
+                                                    const float* __restrict__ W1, int ldw, int M,
+                                                    int Nhalf, int K, float* __restrict__ outA,
+                                                    float* __restrict__ outB, int ldo, int vec) {
+  constexpr int BN = 128, BK = 16, KP = BK / 2;
+  constexpr int RB = BM / 64;            // row blocks of 4 per thread (1 or 2)
+  constexpr int NA = BM * BK / 4 / 256;  // float4 loads of A per thread per slice
+  constexpr int NW = BN * BK / 4 / 256;
+  __shared__ __align__(16) float sa[KP][2 * BM + 8];  // [k pair][row][k % 2]
+  __shared__ __align__(16) float sw[KP][2 * BN + 8];
+  const int Ncols = 2 * Nhalf;
+  const int r0 = blockIdx.y * BM, c0 = blockIdx.x * BN;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  float acc[4 * RB][8];
+#pragma unroll
+  for (int i = 0; i < 4 * RB; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = kNegInf;
+  float4 ra[NA], rw[NW];
+  auto ld4 = [&](const float* row, int gk, bool ok) -> float4 {
+    if (!ok) return make_float4(kNegInf, kNegInf, kNegInf, kNegInf);
+    if (vec && gk + 3 < K) return __ldg(reinterpret_cast<const float4*>(row + gk));
+    float4 v;
+    v.x = gk < K ? __ldg(row + gk) : kNegInf;
+    v.y = gk + 1 < K ? __ldg(row + gk + 1) : kNegInf;
+    v.z = gk + 2 < K ? __ldg(row + gk + 2) : kNegInf;
+    v.w = gk + 3 < K ? __ldg(row + gk + 3) : kNegInf;
+    return v;
+  };
+  auto gload = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < NA; ++q) {
+      const int e = threadIdx.x + q * 256, rr = e / 4, gk = k0 + (e % 4) * 4;
+      const int gr = r0 + rr;
+      ra[q] = ld4(A + static_cast<long long>(gr < M ? gr : 0) * lda, gk, gr < M);
+    }
+#pragma unroll
+    for (int q = 0; q < NW; ++q) {
+      const int e = threadIdx.x + q * 256, cc = e / 4, gk = k0 + (e % 4) * 4;
+      const int gc = c0 + cc;
+      const float* wr = gc < Nhalf ? W0 + static_cast<long long>(gc) * ldw
+                                   : W1 + static_cast<long long>(gc < Ncols ? gc - Nhalf : 0) * ldw;
+      rw[q] = ld4(wr, gk, gc < Ncols);
+    }
+  };
+  auto sstore = [&]() {  // four consecutive k of one row -> two k pairs
+#pragma unroll
+    for (int q = 0; q < NA; ++q) {
+      const int e = threadIdx.x + q * 256, rr = e / 4, kp = (e % 4) * 2;
+      *reinterpret_cast<float2*>(&sa[kp][2 * rr]) = make_float2(ra[q].x, ra[q].y);
+      *reinterpret_cast<float2*>(&sa[kp + 1][2 * rr]) = make_float2(ra[q].z, ra[q].w);
+    }
+#pragma unroll
+    for (int q = 0; q < NW; ++q) {
+      const int e = threadIdx.x + q * 256, cc = e / 4, kp = (e % 4) * 2;
+      *reinterpret_cast<float2*>(&sw[kp][2 * cc]) = make_float2(rw[q].x, rw[q].y);
+      *reinterpret_cast<float2*>(&sw[kp + 1][2 * cc]) = make_float2(rw[q].z, rw[q].w);
+    }
+  };
+  gload(0);
+  for (int k0 = 0; k0 < K; k0 += BK) {
+    __syncthreads();  // the previous slice is consumed
+    sstore();
+    __syncthreads();
+    if (k0 + BK < K) gload(k0 + BK);  // in flight during this slice
+#pragma unroll
+    for (int kp = 0; kp < KP; ++kp) {
+      float2 a[4 * RB], w[8];
+#pragma unroll
+      for (int rb = 0; rb < RB; ++rb) {
+        const float4* src = reinterpret_cast<const float4*>(&sa[kp][2 * (ty * 4 + rb * (BM / 2))]);
+        const float4 u = src[0], v = src[1];
+        a[4 * rb] = make_float2(u.x, u.y);
+        a[4 * rb + 1] = make_float2(u.z, u.w);
+        a[4 * rb + 2] = make_float2(v.x, v.y);
+        a[4 * rb + 3] = make_float2(v.z, v.w);
+      }
+#pragma unroll
+      for (int cb = 0; cb < 2; ++cb) {
+        const float4* src = reinterpret_cast<const float4*>(&sw[kp][2 * (tx * 4 + cb * 64)]);
+        const float4 u = src[0], v = src[1];
+        w[4 * cb] = make_float2(u.x, u.y);
+        w[4 * cb + 1] = make_float2(u.z, u.w);
+        w[4 * cb + 2] = make_float2(v.x, v.y);
+        w[4 * cb + 3] = make_float2(v.z, v.w);
+      }
+#pragma unroll
+      for (int i = 0; i < 4 * RB; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float2 t = trop_add2(a[i], w[j]);
+          acc[i][j] = trop_max3(acc[i][j], t.x, t.y);
+        }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4 * RB; ++i) {
+    const int r = r0 + ty * 4 + (i & 3) + (i >> 2) * (BM / 2);
+    if (r >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = c0 + tx * 4 + (j & 3) + (j >> 2) * 64;
+      if (c >= Ncols) continue;
+      if (c < Nhalf) outA[static_cast<long long>(r) * ldo + c] = acc[i][j];
+      else outB[static_cast<long long>(r) * ldo + c - Nhalf] = acc[i][j];
+    }
+  }
+}
+
 // vo[row(w, b, i), A] = max_m va[m][b, i, A] + vb[w-m][b, i+m, A]; padded spans -inf.
 __global__ void __launch_bounds__(256) k_vit_split(const float* __restrict__ VA,
                                                    const float* __restrict__ VB,
