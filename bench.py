@@ -47,9 +47,13 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clock / throttle-reason sampling during the timed region."""
+    """nvidia-smi clock / throttle-reason sampling during the timed region.
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    nvidia-smi polls every 20 ms with a host timestamp per line; only lines
+    stamped inside [mark(), stop()] count (the default run's timed region is
+    ~150 ms, so the sampler starts before it)."""
+
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
@@ -62,7 +66,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100", "-i", str(self.gpu)],
+                 "-lms", "20", "-i", str(self.gpu)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
@@ -71,7 +75,11 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self):
+        """Start of the timed region (lines read before it are dropped)."""
+        self.t_mark = time.time()
 
     def stop(self) -> dict:
         if self.proc is None:
@@ -81,10 +89,14 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
+        t_end = time.time()
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
+        t_mark = getattr(self, "t_mark", 0.0)
+        for t_read, ln in self.lines:
+            if not t_mark <= t_read <= t_end + 0.05:
+                continue
+            parts = [p.strip() for p in ln.split(",")][1:]  # drop the timestamp
             if len(parts) < 7:
                 continue
             try:
@@ -378,7 +390,10 @@ def run_ours(args, world, rank, local):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # ---- device-resident timed region
+    # ---- device-resident timed region (the clock sampler runs from the
+    # warm-up on; only its samples inside the timed region count)
+    clocks = ClockSampler(local)
+    clocks.start()
     for _ in range(args.warmup):
         step(L, R, root, unary)
     barrier()
@@ -401,11 +416,10 @@ def run_ours(args, world, rank, local):
         for _ in range(2):
             graph.replay()
         barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
     launch0 = lib.fi_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
+    clocks.mark()
     e0.record()
     for _ in range(args.steps):
         if graph is not None:
@@ -525,13 +539,14 @@ def run_train(args, world, rank, local):
             dist.barrier()
         torch.cuda.synchronize()
 
+    clocks = ClockSampler(local)
+    clocks.start()
     for _ in range(args.warmup):
         ts.step(tok, lengths, global_batch=batch * world)
     barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
     launch0 = lib.fi_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks.mark()
     e0.record()
     for _ in range(args.steps):
         loss = ts.step(tok, lengths, global_batch=batch * world)
