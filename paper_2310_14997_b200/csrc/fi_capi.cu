@@ -431,8 +431,6 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
   // ring depth: as many (A + this CTA's share of B) stages as fit in 227 KB
   // (a pair CTA stages half the N tile, so pairs run deeper rings)
   sh.b_stage = bn / NCTA * 128;
-  static const int env_bstride = env_int("FI_GEMM_BSTRIDE", 0);  // A/B experiments (bytes)
-  if (env_bstride > sh.b_stage) sh.b_stage = env_bstride;
   const int stage_bytes = Cf::A_BYTES + sh.b_stage;
   int max_stages = (kGemmSmemMax - 1024 - 256) / stage_bytes;
   max_stages = max_stages > kGemmStagesMax ? kGemmStagesMax : max_stages;
