@@ -796,8 +796,10 @@ int forward_impl(const Plan& p, const float* L, const float* R, const float* roo
   {  // K1: exp of the child tables, once per call
     ProfScope prof(FI_PROF_PREP, st);
     FI_CUDA(cudaMemsetAsync(wsum, 0, 16, st));
+    const int vec = (p.N % 4 == 0 && p.P % 4 == 0 && reinterpret_cast<uintptr_t>(L) % 16 == 0 &&
+                     reinterpret_cast<uintptr_t>(R) % 16 == 0) ? 1 : 0;
     FI_TRY(launch_ex(k_prep_weights<T>, 1, dim3(2 * p.Np), dim3(256), 0, st, L, R, wnn, wnp, wsum,
-                     p.N, p.P, p.Np, p.Pp, p.wnn_lo, p.wnp_lo));
+                     p.N, p.P, p.Np, p.Pp, p.wnn_lo, p.wnp_lo, vec));
     FI_CUDA(cudaGetLastError());
   }
   {

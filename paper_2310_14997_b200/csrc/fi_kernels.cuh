@@ -161,7 +161,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_prep_weights(
     const float* __restrict__ L, const float* __restrict__ R, T* __restrict__ wnn,
     T* __restrict__ wnp, float* __restrict__ wsum, int N, int P, int Np, int Pp,
-    long long wnn_lo, long long wnp_lo) {
+    long long wnn_lo, long long wnp_lo, int vec) {
   pdl_wait();
   __shared__ float red[33];
   const int row = blockIdx.x;  // 0 .. 2Np-1
@@ -169,15 +169,36 @@ __global__ void __launch_bounds__(256) k_prep_weights(
   const int a = right ? row - Np : row;
   const float* src = (right ? R : L) + static_cast<long long>(a) * (N + P);
   float snn = 0.f, snp = 0.f;
-  for (int c = threadIdx.x; c < Np; c += blockDim.x) {
-    const float v = (a < N && c < N) ? expf(src[c]) : 0.f;
-    snn += v;
-    store1s<T>(wnn + static_cast<long long>(row) * Np + c, wnn_lo, v);
-  }
-  for (int t = threadIdx.x; t < Pp; t += blockDim.x) {
-    const float v = (a < N && t < P) ? expf(src[N + t]) : 0.f;
-    snp += v;
-    store1s<T>(wnp + static_cast<long long>(row) * Pp + t, wnp_lo, v);
+  if (vec) {  // N, P multiples of 4 and 16-B rows: float4 in, 4-wide stores out
+    for (int c = 4 * threadIdx.x; c < Np; c += 4 * blockDim.x) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (a < N && c < N) {
+        v = ldg4(src + c);
+        v = make_float4(expf(v.x), expf(v.y), expf(v.z), expf(v.w));
+      }
+      snn += (v.x + v.y) + (v.z + v.w);
+      store4s<T>(wnn + static_cast<long long>(row) * Np + c, wnn_lo, v.x, v.y, v.z, v.w);
+    }
+    for (int t = 4 * threadIdx.x; t < Pp; t += 4 * blockDim.x) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (a < N && t < P) {
+        v = ldg4(src + N + t);
+        v = make_float4(expf(v.x), expf(v.y), expf(v.z), expf(v.w));
+      }
+      snp += (v.x + v.y) + (v.z + v.w);
+      store4s<T>(wnp + static_cast<long long>(row) * Pp + t, wnp_lo, v.x, v.y, v.z, v.w);
+    }
+  } else {
+    for (int c = threadIdx.x; c < Np; c += blockDim.x) {
+      const float v = (a < N && c < N) ? expf(src[c]) : 0.f;
+      snn += v;
+      store1s<T>(wnn + static_cast<long long>(row) * Np + c, wnn_lo, v);
+    }
+    for (int t = threadIdx.x; t < Pp; t += blockDim.x) {
+      const float v = (a < N && t < P) ? expf(src[N + t]) : 0.f;
+      snp += v;
+      store1s<T>(wnp + static_cast<long long>(row) * Pp + t, wnp_lo, v);
+    }
   }
   snn = block_reduce<false>(snn, red);
   snp = block_reduce<false>(snp, red);
