@@ -142,14 +142,16 @@ def test_beyond_8192_symbols_identities():
     np.testing.assert_allclose(got["dunary"][0].sum(-1), np.ones(l), rtol=2e-3)
 
 
-def test_config3_width_batch_identities():
-    """|N| = 4096 with 64 sentences of length <= 24: the GEMMs run the wide
-    pair tiles (two MMAs per K step) in the forward, dgrad and wgrad.  log Z
-    of two sentences against the oracle forward; every gradient table
-    through identities of the inside-outside expectations (per sentence:
-    sum droot = 1, sum dL = sum dR = l - 1 binary nodes, each token's unary
-    posterior sums to 1)."""
-    N, P, V, B, lmax = 4096, 4096, 64, 64, 24
+@pytest.mark.parametrize("N,P,lmax", [(4096, 4096, 24), (2300, 700, 18)])
+def test_config3_width_batch_identities(N, P, lmax):
+    """|N| = 4096 (and an odd |N| = 2300, Np = 3072: partial 384-wide
+    N tiles) with 64 sentences: the GEMMs run the wide pair tiles (two MMAs
+    per K step) and split-K tails in the forward, dgrad and wgrad.  log Z of
+    two sentences against the oracle forward; every gradient table through
+    identities of the inside-outside expectations (per sentence: sum droot =
+    1, sum dL = sum dR = l - 1 binary nodes, each token's unary posterior
+    sums to 1)."""
+    V, B = 64, 64
     lengths = np.full(B, lmax)
     lengths[::5] = 17
     root, left, right, emit, unary, lens, _ = make_case(N, P, V, B, lmax, 5, lengths)
