@@ -189,9 +189,10 @@ int make_plan(const fi_shape* s, Plan* p) {
   p->P = s->n_pt;
   p->B = s->batch;
   p->l = s->max_len;
-  // padded symbol count: multiple of 256 / 1024 / 2048 so the bandwidth
+  // padded symbol count: multiple of 256 / 512 / 1024 / 2048 so the bandwidth
   // kernels always find an exact column decomposition (make_decomp)
-  p->Np = static_cast<int>(align_up(p->N, p->N <= 1024 ? 256 : p->N <= 8192 ? 1024 : 2048));
+  p->Np = static_cast<int>(
+      align_up(p->N, p->N <= 1024 ? 256 : p->N <= 4096 ? 512 : p->N <= 8192 ? 1024 : 2048));
   p->Pp = static_cast<int>(align_up(p->P, 256));
   p->tf32 = s->gemm_dtype == FI_GEMM_TF32;
   p->split = s->gemm_dtype == FI_GEMM_FP32;

@@ -144,7 +144,7 @@ def test_beyond_8192_symbols_identities():
 
 @pytest.mark.parametrize("N,P,lmax", [(4096, 4096, 24), (2300, 700, 18)])
 def test_config3_width_batch_identities(N, P, lmax):
-    """|N| = 4096 (and an odd |N| = 2300, Np = 3072: partial 384-wide
+    """|N| = 4096 (and an odd |N| = 2300, Np = 2560: partial 384-wide
     N tiles) with 64 sentences: the GEMMs run the wide pair tiles (two MMAs
     per K step) and split-K tails in the forward, dgrad and wgrad.  log Z of
     two sentences against the oracle forward; every gradient table through
