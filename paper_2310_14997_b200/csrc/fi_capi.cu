@@ -431,8 +431,8 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
   sh.bn = bn;
   // ring depth: as many (A + this CTA's share of B) stages as fit in 227 KB
   // (a pair CTA stages half the N tile, so pairs run deeper rings)
-  sh.b_stage = bn / NCTA * 128;
-  const int stage_bytes = Cf::A_BYTES + sh.b_stage;
+  sh.b_stage = bn / NCTA * 128 * (SPLIT ? 2 : 1);  // SPLIT: hi and lo tiles per stage
+  const int stage_bytes = Cf::A_BYTES * (SPLIT ? 2 : 1) + sh.b_stage;
   int max_stages = (kGemmSmemMax - 1024 - 256) / stage_bytes;
   max_stages = max_stages > kGemmStagesMax ? kGemmStagesMax : max_stages;
   static const int env_stages = env_int("FI_GEMM_STAGES", 0);  // A/B experiments
@@ -628,7 +628,8 @@ int run_gemm_s(const Operand& A, const Operand& B, int M, int N, int K, int a_ro
   if (N % 64) return set_err(FI_ERR_ARG, "GEMM N=%d must be a multiple of 64", N);
   constexpr int BK = 128 / static_cast<int>(sizeof(T));
   constexpr int ATOM = 128 / static_cast<int>(sizeof(T));
-  const int k_iters = (SPLIT ? 3 : 1) * ((K + BK - 1) / BK);
+  // SPLIT: a K block stages 2x the operand bytes for 3 MMAs (cost-model units)
+  const int k_iters = (SPLIT ? 2 : 1) * ((K + BK - 1) / BK);
   // fp32 mode: chunked round-to-nearest accumulation (8 K-iterations per
   // TMEM chunk) to bound the tensor-core truncation bias; N tile <= 128.
   // pair tiles up to 256 x 512 for bf16 (two N = 256 MMAs per K step; the

@@ -319,8 +319,13 @@ __device__ __forceinline__ void epi_emit(const GemmEpi& ep, const EpiRow& r, int
 }
 
 // SPLIT (fp32 mode, bf16x3): each operand is stored as hi + lo bf16 planes
-// (x = hi + lo to ~2^-17 relative) and the K loop runs three passes,
-// lo*hi, hi*lo, then hi*hi (small terms first), into the same accumulator.
+// (x = hi + lo to ~2^-17 relative).  One ring stage holds the hi and lo
+// tiles of A and B for a K block and the MMA issuer runs its three products
+// from it: lo*hi and hi*lo into a "small" accumulator, hi*hi into a "big"
+// one (two TMEM accumulators per buffer, so the small terms never round
+// against the big sum); the epilogue adds small + big per chunk.  Staging
+// the four tiles once per K block moves 2/3 of the operand bytes of three
+// separate passes (the per-SM fill rate is the GEMM's limit).
 //
 // CHUNK > 0: the tensor core accumulates in fp32 with truncation, a
 // downward bias that grows with the number of MMA steps into one
@@ -347,8 +352,13 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   const int NS = sh.stages;
+  // SPLIT: A stage = [hi | lo] tiles; B stage (sh.b_stage) = [hi | lo] halves
+  constexpr int kAStage = (SPLIT ? 2 : 1) * C::A_BYTES;
+  constexpr int kTmemCols = SPLIT ? 4 * BN : C::TMEM_COLS;  // SPLIT: small + big per buffer
+  constexpr int kTmemHalf = kTmemCols / 2;
+  static_assert(kTmemCols <= 512, "TMEM holds 512 columns");
   uint8_t* smA = smem;
-  uint8_t* smB = smem + NS * C::A_BYTES;
+  uint8_t* smB = smem + NS * kAStage;
   uint64_t* full = reinterpret_cast<uint64_t*>(smB + NS * sh.b_stage);
   uint64_t* empty = full + NS;
   uint64_t* tfull = empty + NS;
@@ -358,14 +368,14 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int num_tiles = sh.num_m * sh.num_n;
-  const int k_iters = SPLIT ? 3 * sh.num_k : sh.num_k;
+  const int k_iters = sh.num_k;
   const int ks = sh.ksplit > 1 ? sh.ksplit : 1;
   const int tb = sh.tile_begin;
   const int tile_e = sh.tile_end > 0 ? sh.tile_end : num_tiles;
   const int nunits = (tile_e - tb) * ks;
   const int bn = sh.bn;                       // runtime N tile <= BN
   const int bn_cta = bn / NCTA;               // B rows staged by this CTA
-  const int nbuf = bn <= C::TMEM_HALF ? 2 : 1;  // accumulator buffers in TMEM
+  const int nbuf = SPLIT || bn <= C::TMEM_HALF ? 2 : 1;  // accumulator buffers in TMEM
   const uint32_t rank = PAIR ? cluster_rank() : 0;
   const int tile0 = PAIR ? blockIdx.x / 2 : blockIdx.x;
   const int tstep = PAIR ? gridDim.x / 2 : gridDim.x;
@@ -388,8 +398,8 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
     fence_mbar_init();
   }
   if (warp == 2) {
-    if constexpr (PAIR) tmem_alloc2<C::TMEM_COLS>(tslot);
-    else tmem_alloc<C::TMEM_COLS>(tslot);
+    if constexpr (PAIR) tmem_alloc2<kTmemCols>(tslot);
+    else tmem_alloc<kTmemCols>(tslot);
   }
   tc_fence_before();
   if constexpr (PAIR) cluster_sync_all();  // barrier inits visible to the peer
@@ -404,7 +414,7 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
       // ------------------------------------------------ TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      const uint32_t stage_tx = NCTA * (C::A_BYTES + bn_cta * 128);
+      const uint32_t stage_tx = NCTA * (kAStage + sh.b_stage);
       for (int u = tile0; u < nunits; u += tstep) {
         const int tu = u / ks, kpart = u - tu * ks;
         const int tile = tb + tu;
@@ -414,12 +424,9 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
         const int m0 = m_blk * (C::BM * NCTA) + rank * C::BM;  // this CTA's A rows
         const int n0 = n_blk * bn + rank * bn_cta;              // this CTA's B rows
         for (int it = k0; it < k1; ++it) {
-          const int pass = SPLIT ? it / sh.num_k : 0;
-          const int kb = SPLIT ? it - pass * sh.num_k : it;
-          const CUtensorMap* ma = (SPLIT && pass == 0) ? &tmA2 : &tmA;
-          const CUtensorMap* mb = (SPLIT && pass == 1) ? &tmB2 : &tmB;
+          const int kb = it;
           mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* a_dst = smA + stage * C::A_BYTES;
+          uint8_t* a_dst = smA + stage * kAStage;
           uint8_t* b_dst = smB + stage * sh.b_stage;
           // completion is counted on the leader's full barrier (both CTAs' bytes)
           uint32_t fb = smem_u32(&full[stage]);
@@ -433,18 +440,28 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
             if constexpr (PAIR) tma_load_2d_pair(dst, m, fb, c0, c1);
             else tma_load_2d(dst, m, &full[stage], c0, c1);
           };
-          if constexpr (!A_MN) {
-            load(a_dst, ma, kb * C::BK, sh.a_row0 + m0);
-          } else {
+          auto load_a = [&](uint8_t* dst, const CUtensorMap* ma) {
+            if constexpr (!A_MN) {
+              load(dst, ma, kb * C::BK, sh.a_row0 + m0);
+            } else {
 #pragma unroll
-            for (int j = 0; j < C::BM / C::ATOM; ++j)
-              load(a_dst + j * C::BK * 128, ma, m0 + j * C::ATOM, kb * C::BK);
-          }
-          if constexpr (!B_MN) {
-            load(b_dst, mb, kb * C::BK, n0);
-          } else {
-            for (int j = 0; j < bn_cta / C::ATOM; ++j)
-              load(b_dst + j * C::BK * 128, mb, n0 + j * C::ATOM, kb * C::BK);
+              for (int j = 0; j < C::BM / C::ATOM; ++j)
+                load(dst + j * C::BK * 128, ma, m0 + j * C::ATOM, kb * C::BK);
+            }
+          };
+          auto load_b = [&](uint8_t* dst, const CUtensorMap* mb) {
+            if constexpr (!B_MN) {
+              load(dst, mb, kb * C::BK, n0);
+            } else {
+              for (int j = 0; j < bn_cta / C::ATOM; ++j)
+                load(dst + j * C::BK * 128, mb, n0 + j * C::ATOM, kb * C::BK);
+            }
+          };
+          load_a(a_dst, &tmA);
+          load_b(b_dst, &tmB);
+          if constexpr (SPLIT) {  // the lo planes behind the hi tiles
+            load_a(a_dst + C::A_BYTES, &tmA2);
+            load_b(b_dst + sh.b_stage / 2, &tmB2);
           }
           if (++stage == NS) {
             stage = 0;
@@ -483,17 +500,30 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
           if (kc == 0) {  // start a chunk in a drained accumulator
             mbar_wait(&tempty[acc], acc_phase ^ 1);
             tc_fence_after();
-            d_tmem = tmem_base + static_cast<uint32_t>(acc * C::TMEM_HALF);
+            d_tmem = tmem_base + static_cast<uint32_t>(acc * kTmemHalf);
           }
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_base = smem_u32(smA + stage * C::A_BYTES);
+          const uint32_t a_base = smem_u32(smA + stage * kAStage);
           const uint32_t b_base = smem_u32(smB + stage * sh.b_stage);
           auto mma = [&](uint32_t dt, uint64_t ad, uint64_t bd, uint32_t id, uint32_t accum) {
             if constexpr (PAIR) umma2<C::TF32>(dt, ad, bd, id, accum);
             else umma<C::TF32>(dt, ad, bd, id, accum);
           };
-          if constexpr (BN <= 256) {  // BN > 256 kernels run only N tiles above 256
+          if constexpr (SPLIT) {  // small (lo*hi + hi*lo) at +0, big (hi*hi) at +BN
+            const uint32_t b_lo = static_cast<uint32_t>(sh.b_stage / 2);
+#pragma unroll
+            for (int k = 0; k < C::BK / C::UK; ++k) {
+              const uint64_t ah = make_sdesc(a_base + k * a_kstep, a_lbo, a_sbo, a_lay);
+              const uint64_t al = make_sdesc(a_base + C::A_BYTES + k * a_kstep, a_lbo, a_sbo, a_lay);
+              const uint64_t bh = make_sdesc(b_base + k * b_kstep, b_lbo, b_sbo, b_lay);
+              const uint64_t bl = make_sdesc(b_base + b_lo + k * b_kstep, b_lbo, b_sbo, b_lay);
+              const uint32_t accum = (kc | k) != 0 ? 1u : 0u;
+              mma(d_tmem, al, bh, idesc0, accum);
+              mma(d_tmem, ah, bl, idesc0, 1u);
+              mma(d_tmem + static_cast<uint32_t>(BN), ah, bh, idesc0, accum);
+            }
+          } else if constexpr (BN <= 256) {  // BN > 256 kernels run only N tiles above 256
 #pragma unroll
             for (int k = 0; k < C::BK / C::UK; ++k)
               mma(d_tmem, make_sdesc(a_base + k * a_kstep, a_lbo, a_sbo, a_lay),
@@ -582,7 +612,7 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
       if constexpr (CHUNK == 0) {
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
-        const uint32_t t_row = t_lane + static_cast<uint32_t>(acc * C::TMEM_HALF);
+        const uint32_t t_row = t_lane + static_cast<uint32_t>(acc * kTmemHalf);
         const int nch = bn / 32;
         constexpr int kHalves = gemm_epi_warps<CHUNK>() / 4;
 #pragma unroll 1
@@ -651,12 +681,19 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
         for (int c = 0; c < nchunks; ++c) {
           mbar_wait(&tfull[acc], acc_phase);
           tc_fence_after();
-          const uint32_t t_row = t_lane + static_cast<uint32_t>(acc * C::TMEM_HALF);
+          const uint32_t t_row = t_lane + static_cast<uint32_t>(acc * kTmemHalf);
 #pragma unroll
           for (int j = 0; j < BN / 32; ++j) {
             if (j < bn / 32) {
               float v[32];
-              tmem_ld32(t_row + j * 32, v);
+              if constexpr (SPLIT) {  // small + big, then into the running sum
+                float vb[32];
+                tmem_ld32x2(t_row + j * 32, t_row + BN + j * 32, v, vb);
+#pragma unroll
+                for (int t = 0; t < 32; ++t) v[t] += vb[t];
+              } else {
+                tmem_ld32(t_row + j * 32, v);
+              }
 #pragma unroll
               for (int t = 0; t < 32; ++t) sum[j][t] += v[t];
             }
@@ -677,8 +714,8 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
   else __syncthreads();
   tc_fence_after();
   if (warp == 2) {
-    if constexpr (PAIR) tmem_dealloc2<C::TMEM_COLS>(tmem_base);
-    else tmem_dealloc<C::TMEM_COLS>(tmem_base);
+    if constexpr (PAIR) tmem_dealloc2<kTmemCols>(tmem_base);
+    else tmem_dealloc<kTmemCols>(tmem_base);
   }
 }
 
