@@ -102,8 +102,19 @@ def _two_layer(x, w1, b1, w2, b2):
     return x + torch.relu(x @ w1.T + b1) @ w2.T + b2
 
 
-def grammar_tables(p: EmbeddingParams, tied: bool = False):
-    """(log_root (N,), log_left (N, N+P), log_right, log_emit (P, V)), differentiable."""
+def grammar_tables(p: EmbeddingParams, tied: bool = False, finite_flags: list | None = None):
+    """(log_root (N,), log_left (N, N+P), log_right, log_emit (P, V)), differentiable.
+
+    Non-finite activations raise ParamError (neuralparam.py); with
+    ``finite_flags`` the per-activation checks are appended there as device
+    booleans instead (no host sync: the caller checks them once)."""
+
+    def check(name, a):
+        if finite_flags is not None:
+            finite_flags.append((name, torch.isfinite(a).all()))
+        elif not torch.isfinite(a).all():
+            raise ParamError(f"non-finite activation in {name}")
+
     t = p.tensors
     n = p.dims.n_nt
     x_start = t["w_sym"][0:1]
@@ -117,16 +128,14 @@ def grammar_tables(p: EmbeddingParams, tied: bool = False):
     f5 = _two_layer(_two_layer(x_pt, t["f5.w1"], t["f5.b1"], t["f5.w2"], t["f5.b2"]),
                     t["f5.w3"], t["f5.b3"], t["f5.w4"], t["f5.b4"])
     for name, a in (("f1", f1), ("f2", f2), ("f3", f3), ("f5", f5)):
-        if not torch.isfinite(a).all():
-            raise ParamError(f"non-finite activation in {name}")
+        check(name, a)
     log_root = F.log_softmax((f1 @ t["u_nt"].T)[0], dim=-1)
     log_left = F.log_softmax(f3 @ f2.T, dim=-1)
     if tied:
         log_right = log_left
     else:
         f4 = _residual_relu(x_child, t["f4.w"], t["f4.b"])
-        if not torch.isfinite(f4).all():
-            raise ParamError("non-finite activation in f4")
+        check("f4", f4)
         log_right = F.log_softmax(f3 @ f4.T, dim=-1)
     log_emit = F.log_softmax(f5 @ t["u_voc"].T, dim=-1)
     return log_root, log_left, log_right, log_emit
@@ -247,9 +256,9 @@ class TrainStep:
         if self.state is None:
             self.state = AdamState.zeros({k: v.detach() for k, v in self.params.tensors.items()})
 
-    def tables(self):
+    def tables(self, finite_flags: list | None = None):
         if isinstance(self.params, EmbeddingParams):
-            return grammar_tables(self.params, self.config.tied)
+            return grammar_tables(self.params, self.config.tied, finite_flags)
         return direct_tables(self.params, self.config.tied)
 
     def loss_and_grads(self, tokens: torch.Tensor, lengths: torch.Tensor,
@@ -259,12 +268,17 @@ class TrainStep:
         inside fwd+bwd on the engine -> autograd through the tables)."""
         cfg = self.config
         xs = list(self.params.tensors.values())
+        # activation checks are deferred: queued on the device with the whole
+        # forward + backward, read once at the end (one host sync, no bubble
+        # in front of the engine); a non-finite activation raises ParamError
+        # before any parameter is updated, as in the reference
+        flags: list = []
         # the score-table GEMMs (N x d x (N+P)) run on TF32 tensor cores in the
         # fast modes; fp32 mode keeps exact fp32 products (parity mode)
         prev = torch.backends.cuda.matmul.allow_tf32
         torch.backends.cuda.matmul.allow_tf32 = cfg.gemm_dtype != "fp32"
         try:
-            log_root, log_left, log_right, log_emit = self.tables()
+            log_root, log_left, log_right, log_emit = self.tables(flags)
             unary = log_emit.T[tokens]                                 # inside.py:296-298
             log_z = inside(log_left.contiguous(), log_right.contiguous(), log_root.contiguous(),
                            unary.contiguous(), lengths, gemm_dtype=cfg.gemm_dtype)
@@ -273,6 +287,10 @@ class TrainStep:
             grads = torch.autograd.grad(loss, xs, allow_unused=True)  # tied: f4 unused
         finally:
             torch.backends.cuda.matmul.allow_tf32 = prev
+        if flags:
+            ok = torch.stack([f for _, f in flags]).cpu()
+            if not bool(ok.all()):
+                raise ParamError(f"non-finite activation in {flags[int((~ok).nonzero()[0])][0]}")
         return loss, [torch.zeros_like(x) if g is None else g for x, g in zip(xs, grads)]
 
     def step(self, tokens: torch.Tensor, lengths: torch.Tensor, global_batch: int | None = None,
