@@ -26,7 +26,26 @@ __global__ void __launch_bounds__(256) k_span_mass(const void* __restrict__ LQv,
   const bool ok = i + w <= lengths[b] && g[b] != 0.f;
   const float lg = ok ? log2f(fabsf(g[b])) : 0.f;
   float s = 0.f;
-  if (ok) {
+  if (ok && (N & 3) == 0) {  // 4 columns per thread: 8-B / 16-B loads
+    const float* orow = O + row * Np;
+    for (int c = 4 * threadIdx.x; c < N; c += 4 * blockDim.x) {
+      const float4 o = __ldg(reinterpret_cast<const float4*>(orow + c));
+      if constexpr (kHalfLQ) {
+        const uint2 u = __ldg(reinterpret_cast<const uint2*>(static_cast<const __half*>(LQv) +
+                                                             row * Np + c));
+        const float2 q01 = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+        const float2 q23 = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+        const float e = LQS[row * (Np / 32) + c / 32] - lg;
+        s += q01.x * exp2f(e + o.x) + q01.y * exp2f(e + o.y) + q23.x * exp2f(e + o.z) +
+             q23.y * exp2f(e + o.w);
+      } else {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(LQv) +
+                                                               row * Np + c));
+        s += exp2f(q.x + o.x - lg) + exp2f(q.y + o.y - lg) + exp2f(q.z + o.z - lg) +
+             exp2f(q.w + o.w - lg);
+      }
+    }
+  } else if (ok) {
     for (int c = threadIdx.x; c < N; c += blockDim.x) {
       if constexpr (kHalfLQ) {
         const float q = __half2float(static_cast<const __half*>(LQv)[row * Np + c]);
