@@ -1283,8 +1283,8 @@ int fi_viterbi(const fi_shape* shape, const float* L, const float* R, const floa
   for (int w = 2; w <= p.l; ++w) {
     const int n_w = p.l - w + 1;
     const long long r0 = rowbase(w, p.B, p.l);
-    k_vit_split<<<dim3((p.Np + 255) / 256, p.B * n_w), 256, 0, st>>>(va, vb, vo, lengths, p.B,
-                                                                      p.l, w, p.Np);
+    k_vit_split<<<dim3((p.Np / 4 + 255) / 256, p.B * n_w), 256, 0, st>>>(va, vb, vo, lengths, p.B,
+                                                                          p.l, w, p.Np);
     ++g_launches;
     FI_CUDA(cudaGetLastError());
     if (w < p.l) {  // parse.py:66-71 over the nonterminal block

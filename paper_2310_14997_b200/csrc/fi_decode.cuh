@@ -317,17 +317,21 @@ __global__ void __launch_bounds__(256) k_vit_split(const float* __restrict__ VA,
   const int n_w = lmax - w + 1;
   const int b = local / n_w, i = local % n_w;
   const long long row = rowbase(w, B, lmax) + local;
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = 4 * (blockIdx.x * blockDim.x + threadIdx.x);  // 4 columns per thread (Np % 4 == 0)
   if (c >= Np) return;
-  float best = kNegInf;
+  float4 best = make_float4(kNegInf, kNegInf, kNegInf, kNegInf);
   if (i + w <= lengths[b]) {
     for (int m = 1; m < w; ++m) {
-      const float s = VA[chart_row(m, b, i, B, lmax) * Np + c] +
-                      VB[chart_row(w - m, b, i + m, B, lmax) * Np + c];
-      best = fmaxf(best, s);
+      const float4 x = __ldg(reinterpret_cast<const float4*>(VA + chart_row(m, b, i, B, lmax) * Np + c));
+      const float4 y =
+          __ldg(reinterpret_cast<const float4*>(VB + chart_row(w - m, b, i + m, B, lmax) * Np + c));
+      best.x = fmaxf(best.x, x.x + y.x);
+      best.y = fmaxf(best.y, x.y + y.y);
+      best.z = fmaxf(best.z, x.z + y.z);
+      best.w = fmaxf(best.w, x.w + y.w);
     }
   }
-  VO[row * Np + c] = best;
+  *reinterpret_cast<float4*>(VO + row * Np + c) = best;
 }
 
 // Per sentence: root argmax, then the derivation top-down.  Output per
