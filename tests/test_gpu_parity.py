@@ -168,3 +168,25 @@ def test_config3_width_batch_identities(N, P, lmax):
     for b in range(B):
         np.testing.assert_allclose(tok[b, :lens[b]], 1.0, rtol=2e-3)
         assert np.abs(tok[b, lens[b]:]).max(initial=0.0) == 0.0
+
+
+def test_zero_probability_sentence_in_a_batch():
+    """A sentence whose token no preterminal can emit has log Z = -inf
+    (inside.py:124-129); it contributes no gradient (the reference refuses
+    its backward, inside.py:392-393) and leaves the other sentences of the
+    batch exactly as the oracle computes them without it."""
+    N, P, V, B, lmax = 16, 8, 12, 4, 7
+    root, left, right, emit, unary, lens, _ = make_case(N, P, V, B, lmax, 9, [7, 6, 7, 5])
+    unary = unary.copy()
+    unary[1, 3, :] = -np.inf  # position 3 of sentence 1: impossible token
+    grad = np.array([-0.25, -0.25, -0.25, -0.25])
+    got = run_op(root, left, right, unary, lens, grad, "fp32")
+    assert got["log_z"][1] == -np.inf
+    keep = [0, 2, 3]
+    want = O.inside_batch(left, right, root, unary[keep], lens[keep], grad[keep])
+    np.testing.assert_allclose(got["log_z"][keep], want["log_z"], rtol=1e-4)
+    for k in ("dL", "dR", "droot"):
+        assert np.isfinite(got[k]).all()
+        assert_close(k, got[k], want[k], 1e-4)
+    assert np.abs(got["dunary"][1]).max() == 0.0
+    assert_close("dunary", got["dunary"][keep], want["dunary"], 1e-4)
