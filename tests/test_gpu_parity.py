@@ -190,3 +190,21 @@ def test_zero_probability_sentence_in_a_batch():
         assert_close(k, got[k], want[k], 1e-4)
     assert np.abs(got["dunary"][1]).max() == 0.0
     assert_close("dunary", got["dunary"][keep], want["dunary"], 1e-4)
+
+
+@pytest.mark.parametrize("gemm_dtype", ["fp32", "bf16"])
+def test_long_sentences_deep_log_space(gemm_dtype):
+    """Long sentences drive log Z to hundreds of nats below zero (the
+    reference's deep log-space test, tests/test_inside.py:113-124): the
+    per-span fp64 shifts keep every stored offset small, so log Z and the
+    gradients stay within the mode's tolerance at l = 160."""
+    N, P, V, B, lmax = 16, 16, 20, 2, 160
+    root, left, right, emit, unary, lens, _ = make_case(N, P, V, B, lmax, 13, [160, 97])
+    grad = np.array([-0.5, -0.5])
+    want = O.inside_batch(left, right, root, unary, lens, grad)
+    got = run_op(root, left, right, unary, lens, grad, gemm_dtype)
+    assert want["log_z"].max() < -200.0
+    rtol = RTOL[gemm_dtype]
+    np.testing.assert_allclose(got["log_z"], want["log_z"], rtol=rtol)
+    for k in ("dL", "dR", "droot", "dunary"):
+        assert_close(k, got[k], want[k], rtol)
