@@ -208,3 +208,21 @@ def test_long_sentences_deep_log_space(gemm_dtype):
     np.testing.assert_allclose(got["log_z"], want["log_z"], rtol=rtol)
     for k in ("dL", "dR", "droot", "dunary"):
         assert_close(k, got[k], want[k], rtol)
+
+
+def test_maximum_sentence_length_identities():
+    """l = 1024, the longest sentence the engine accepts (per-span term
+    tables live in shared memory; 1025 is refused): log Z finite and the
+    inside-outside identities hold (sum droot = 1, each token's unary
+    posterior sums to 1, sum dL = l - 1 binary nodes)."""
+    N, P, V, l = 4, 4, 6, 1024
+    root, left, right, emit, unary, lens, _ = make_case(N, P, V, 1, l, 17)
+    got = run_op(root, left, right, unary, lens, np.array([1.0]), "fp32")
+    assert np.isfinite(got["log_z"]).all()
+    assert got["droot"].sum() == pytest.approx(1.0, rel=1e-4)
+    np.testing.assert_allclose(got["dunary"][0].sum(-1), np.ones(l), rtol=1e-4)
+    assert got["dL"].sum() == pytest.approx(l - 1, rel=1e-4)
+    from paper_2310_14997_b200 import _lib
+    with pytest.raises(_lib.EngineError):
+        run_op(root, left, right, np.zeros((1, l + 1, P), np.float32), np.array([l + 1]),
+               np.array([1.0]), "fp32")
