@@ -1036,6 +1036,31 @@ __global__ void k_marginals(const void* __restrict__ LQv, const float* __restric
   const int b = static_cast<int>(local / n_w), i = static_cast<int>(local % n_w);
   const bool ok = i + w <= lengths[b] && g[b] != 0.f;
   const float lg = ok ? log2f(fabsf(g[b])) : 0.f;
+  float* out = mu + (row - rowbase(2, B, lmax)) * N;
+  if ((N & 3) == 0 && (reinterpret_cast<uintptr_t>(mu) & 15) == 0) {  // 4 columns per thread
+    for (int c = 4 * threadIdx.x; c < N; c += 4 * blockDim.x) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (ok) {
+        const float4 o = __ldg(reinterpret_cast<const float4*>(O + row * Np + c));
+        if constexpr (kHalfLQ) {
+          const uint2 u = __ldg(reinterpret_cast<const uint2*>(static_cast<const __half*>(LQv) +
+                                                               row * Np + c));
+          const float2 q01 = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+          const float2 q23 = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+          const float e = LQS[row * (Np / 32) + c / 32] - lg;
+          v = make_float4(q01.x * exp2f(e + o.x), q01.y * exp2f(e + o.y), q23.x * exp2f(e + o.z),
+                          q23.y * exp2f(e + o.w));
+        } else {
+          const float4 q = __ldg(reinterpret_cast<const float4*>(
+              static_cast<const float*>(LQv) + row * Np + c));
+          v = make_float4(exp2f(q.x + o.x - lg), exp2f(q.y + o.y - lg), exp2f(q.z + o.z - lg),
+                          exp2f(q.w + o.w - lg));
+        }
+      }
+      *reinterpret_cast<float4*>(out + c) = v;
+    }
+    return;
+  }
   for (int c = threadIdx.x; c < N; c += blockDim.x) {
     float v = 0.f;
     if (ok) {
@@ -1046,7 +1071,7 @@ __global__ void k_marginals(const void* __restrict__ LQv, const float* __restric
         v = exp2f(static_cast<const float*>(LQv)[row * Np + c] + O[row * Np + c] - lg);
       }
     }
-    mu[(row - rowbase(2, B, lmax)) * N + c] = v;
+    out[c] = v;
   }
 }
 
