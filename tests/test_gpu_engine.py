@@ -193,3 +193,22 @@ def test_config3_log_z_vs_oracle(config3):
                           backward=False)["log_z"]
     np.testing.assert_allclose(lz[:2].cpu().numpy(), want, rtol=FP32)
     assert want[0] == pytest.approx(float(GOLD["cfg_n4096_l40_logz0"]), abs=1e-9)
+
+
+def test_marginals_64_symbols_against_oracle():
+    """MarginalTable of a 64-symbol grammar (the vectorised export path)
+    against the float64 oracle's go[w][:, :N] (inside.py:425-430)."""
+    from oracle import flashinside_oracle as O
+    g = random_grammar(GrammarDims(64, 64, 30), seed=5)
+    toks = np.random.default_rng(6).integers(0, 30, 12)
+    chart = engine.inside_b200(g, toks)
+    _, marg = engine.inside_backward_b200(g, toks, chart)
+    L, R = np.asarray(g.log_left), np.asarray(g.log_right)
+    unary = np.asarray(g.log_emit)[:, toks].T
+    ch = O.inside_sentence(L, R, np.asarray(g.log_root), unary)
+    *_, go = O.backward_sentence(L, R, np.asarray(g.log_root), ch)
+    want = O.marginals_sentence(ch, go)
+    for w in range(2, toks.size + 1):
+        np.testing.assert_allclose(marg.mu_sym[w], want[w], rtol=FP32, atol=1e-6,
+                                   err_msg=f"w={w}")
+        np.testing.assert_allclose(marg.mu[w], want[w].sum(axis=1), rtol=FP32, atol=1e-6)
