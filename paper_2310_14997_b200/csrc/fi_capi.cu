@@ -514,15 +514,18 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
 // persistent tiles costs k_iters x 0.55 us x t(bn) with
 //   single CTA  T = ceil(M/128) ceil(N/bn) tiles over 148 slots, t = 0.77 + 0.23 bn/256
 //   CTA pair    T = ceil(M/256) ceil(N/bn) tiles over  74 slots, t = 0.965 t_single
-// fitted to B200 measurements (scripts/gemm_bn_sweep.py, whole waves, long
-// K): a k-iteration has a large fixed part (A-tile staging, issue), so
-// narrow N tiles are nearly as expensive as wide ones, and a pair tile (two
-// SMs, 256 rows) costs 3.5% less per row than two single tiles.  The N tile
-// is free in steps of 32 (K-major B) or of one 128-B atom per CTA (MN-major
-// B) so tile counts can land on whole waves; split-K options (whole GEMM,
-// or only the partial last wave) add their partial-tile traffic and
-// fix-up launch.  FI_GEMM_PAIR / FI_GEMM_BN / FI_GEMM_KSPLIT / FI_GEMM_NOTAIL
-// force choices for A/B runs; FI_GEMM_LOG=1 prints them.
+//               (bn <= 256), 0.965 (1 + 0.476 (bn - 256) / 256) above, plus a
+//               serial epilogue per wave (the single-buffered accumulator)
+// fitted to B200 measurements (scripts/experiments/gemm_bn_sweep.py,
+// scripts/gemm_vs_cublas.py; whole waves, long K): a k-iteration has a
+// large fixed part (the per-SM shared-memory fill of A and B), so narrow N
+// tiles are nearly as expensive as wide ones, and a pair tile (two SMs, 256
+// rows) costs 3.5% less per row than two single tiles.  The N tile is free
+// in steps of 32 (K-major B) or of one 128-B atom per CTA (MN-major B) so
+// tile counts can land on whole waves; split-K options (whole GEMM, or only
+// the partial last wave) add their partial-tile traffic and reduction.
+// FI_GEMM_PAIR / FI_GEMM_BN / FI_GEMM_KSPLIT / FI_GEMM_NOTAIL force choices
+// for A/B runs; FI_GEMM_LOG=1 prints them.
 int gemm_env(const char* name, int dflt) {
   const char* e = getenv(name);
   return e ? atoi(e) : dflt;
