@@ -454,9 +454,13 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
       static_cast<size_t>(ksplit) * tsplit * Cf::BM * NCTA * bn <= g_kpart.floats) {
     sh.ksplit = ksplit;
     sh.part = g_kpart.ptr;
-    // every unit of a split tile is resident at once (units <= slots), so the
-    // tile's CTAs reduce the partials themselves (no fixup launch)
-    static const int inkernel = env_int("FI_GEMM_INKERNEL_RED", 1);
+    // FI_GEMM_INKERNEL_RED=1: every unit of a split tile is resident at once
+    // (units <= slots), so the tile's CTAs can reduce the partials themselves
+    // (no fixup launch).  Their wait needs every unit of the launch to get an
+    // SM; split launches of two streams running at once could each hold SMs
+    // the other needs, so it is opt-in (measured: no faster than the fixup
+    // kernel at config 3, 14.35-14.48 vs 14.41-14.64 ms).
+    static const int inkernel = env_int("FI_GEMM_INKERNEL_RED", 0);
     if (inkernel && g_kpart.sem && tsplit <= kKPartSems) sh.sem = g_kpart.sem;
   } else {
     tail = 0;  // no split-K available: whole tiles only
@@ -559,15 +563,14 @@ GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int bn_max_p
   GemmChoice best{0, false, 1, 0};
   double best_cost = 1e300;  // microseconds
   const double us_per_kiter = 0.55;  // one 128 x 256 bf16 k-iteration on one SM (measured)
-  // split-K reduction cost.  Whole-tile split (small M): fitted, partials at
-  // ~3 TB/s plus a fixed 8 us (12 with the separate fixup kernel,
-  // FI_GEMM_INKERNEL_RED=0).  Split tail of a multi-wave launch (the tile's
-  // CTAs reduce in-kernel): a handshake plus each CTA's own partial rows
-  // written and read at the per-SM fill rate (~60 GB/s: 2 x 128 x bn x 4 B)
-  // -- measured at config 3: 256 x 512 tails for the dgrad at M >= 2368
-  // (-10..-25 us each) and the wgrad (-0.18 ms), while 256 x 512 whole-tile
-  // splits at small M measured slower (kept to N tiles <= 256 there).
-  static const bool inkernel_red = gemm_env("FI_GEMM_INKERNEL_RED", 1) != 0;
+  // split-K reduction cost: partials at ~3 TB/s plus a fixed 12 us for the
+  // fixup kernel (8 us with FI_GEMM_INKERNEL_RED=1; its split tails: a
+  // handshake plus each CTA's own partial rows at the per-SM fill rate,
+  // ~60 GB/s: 2 x 128 x bn x 4 B).  Measured at config 3: 256 x 512 tails
+  // for the dgrad at M >= 2368 (-10..-25 us each) and the wgrad (-0.18 ms);
+  // 256 x 512 whole-tile splits at small M measured slower (kept to N tiles
+  // <= 256 there).
+  static const bool inkernel_red = gemm_env("FI_GEMM_INKERNEL_RED", 0) != 0;
   for (int pair = 0; pair < 2; ++pair) {
     if (force_pair >= 0 && pair != force_pair) continue;
     const int step = pair ? step_pair : step_single;
@@ -582,7 +585,7 @@ GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int bn_max_p
       const double t = us_per_kiter * (pair ? gemm_t_pair(bn) : gemm_t_single(bn));
       // split-K over `units` tiles of which `r` are split: feasibility and fixup cost
       auto ks_ok = [&](long long r, int ks, bool tail_split) {
-        return allow_ksplit && force_ks != 1 && (tail_split ? inkernel_red : bn <= 256) &&
+        return allow_ksplit && force_ks != 1 && (tail_split || bn <= 256) &&
                r * ks <= slots && k_iters / ks >= 4 &&
                static_cast<double>(ks) * r * tile_rows * bn <= static_cast<double>(g_kpart.floats);
       };
@@ -590,7 +593,10 @@ GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int bn_max_p
         return (inkernel_red ? 8.0 : 12.0) +
                2.0 * ks * static_cast<double>(r) * tile_rows * bn * 4.0 / 3.0e6;
       };
-      const double tail_red_us = 3.0 + 2.0 * 128 * bn * 4.0 / 60.0e3;
+      auto tail_red_us = [&](long long r, int ks) {
+        if (inkernel_red) return 3.0 + 2.0 * 128 * bn * 4.0 / 60.0e3;
+        return 12.0 + 2.0 * ks * static_cast<double>(r) * tile_rows * bn * 4.0 / 3.0e6;
+      };
       auto consider = [&](double cost, int ks, int tail) {
         if (cost < best_cost * 0.995) {
           best_cost = cost;
@@ -615,7 +621,7 @@ GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int bn_max_p
           // (+3 us: the tail is a second launch)
           const double cost = static_cast<double>(T / slots) * (k_iters * t + gemm_epi_serial(bn)) +
                               static_cast<double>((k_iters + ks - 1) / ks) * t +
-                              gemm_epi_serial(bn) + tail_red_us + 3.0;
+                              gemm_epi_serial(bn) + tail_red_us(r, ks) + 3.0;
           consider(cost, ks, static_cast<int>(r));
         }
       }

@@ -59,7 +59,8 @@ struct GemmShape {
   // apply the epilogue.
   int ksplit;
   float* part;
-  // non-null: the ksplit CTAs (x NCTA) of a split tile reduce it in-kernel --
+  // non-null (FI_GEMM_INKERNEL_RED=1; default: the k_gemm_fixup kernel): the
+  // ksplit CTAs (x NCTA) of a split tile reduce it in-kernel --
   // each publishes its partial, waits on the tile's counter sem[tile - tile_begin]
   // (zero on entry, left zero on exit) and then sums every part, in part
   // order, over its own 1/ksplit of the tile's columns and runs the epilogue.

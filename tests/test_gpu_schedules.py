@@ -38,8 +38,8 @@ print(json.dumps(out))
 @pytest.mark.parametrize("env", [
     {"FI_DUAL_ROWS": "48"},                       # narrow launches as two half-batch chains
     {"FI_DUAL": "1"},                             # every launch as two chains
-    {"FI_GEMM_INKERNEL_RED": "0", "FI_GEMM_KSPLIT": "2"},  # split-K through the fixup kernel
-    {"FI_GEMM_KSPLIT": "4"},                      # split-K reduced in-kernel
+    {"FI_GEMM_INKERNEL_RED": "1", "FI_GEMM_KSPLIT": "2"},  # split-K reduced in-kernel
+    {"FI_GEMM_KSPLIT": "4"},                      # split-K through the fixup kernel
     {"FI_SPLIT_PERS": "0"},                       # one-shot split kernel at every width
     {"FI_SPLIT_PERS": "2"},                       # persistent split kernel at every width
     {"FI_PDL": "0"},
