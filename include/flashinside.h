@@ -20,6 +20,9 @@
  *   - The workspace `ws` (fi_workspace_bytes) is caller-allocated device
  *     memory.  The forward leaves the chart in it; the backward consumes it.
  *     The library never allocates or frees caller memory.
+ *   - Calls on different streams (and threads) may run concurrently, each
+ *     with its own workspace.  (The opt-in FI_GEMM_INKERNEL_RED=1 schedule
+ *     assumes one stream at a time: its split-K units wait for each other.)
  *
  * Shapes (N = n_nt, P = n_pt, B = batch, l = max_len):
  *   L, R      : (N, N+P)   log_left / log_right  (grammar.py:99-100)
