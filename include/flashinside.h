@@ -29,7 +29,8 @@
  *   root      : (N,)       log_root
  *   unary     : (B, l, P)  unary[b, i, T] = log_emit[T, tokens[b][i]]
  *                          (the width-1 chart row, inside.py:296-298)
- *   lengths   : (B,)       2 <= lengths[b] <= l
+ *   lengths   : (B,)       2 <= lengths[b] <= l; a length outside that range
+ *                          is caught on the device (FI_FLAG_BAD_LENGTH below)
  *   log_z     : (B,)       per-sentence log partition (InsideChart.log_z)
  *   grad_log_z: (B,)       upstream gradient dLoss/dlog_z
  *   dL, dR    : (N, N+P)   sum_b grad_log_z[b] * dlog_z[b]/dL  (GrammarGrad)
@@ -63,6 +64,16 @@ extern "C" {
 #define FI_CHART_F32 1  /* fp32 base-2 log offsets a^ = log2(acc)                         */
 #define FI_CHART_F16 2  /* fp16 linear acc * 2^14 (acc = (E W^T) in [0, 1])               */
 
+/* Bits of the int32 flag word at fi_chart_layout.off_flag (cleared by every
+ * fi_inside_forward / fi_inside_backward call, then set on the stream):
+ *   FI_FLAG_ZERO_PROB  (backward) a sentence with log Z = -inf: it gets no
+ *                      gradient (inside.py:392-393 raises InsideError here)
+ *   FI_FLAG_BAD_LENGTH a lengths[b] outside [2, l] (inside.py:113-121): that
+ *                      sentence is inert -- log_z[b] = NaN, zero gradients,
+ *                      no chart write outside its own rows. */
+#define FI_FLAG_ZERO_PROB 1
+#define FI_FLAG_BAD_LENGTH 2
+
 typedef struct fi_shape {
   int32_t n_nt;        /* N */
   int32_t n_pt;        /* P */
@@ -93,7 +104,7 @@ typedef struct fi_chart_layout {
   int64_t off_o;    /* o[w]  fp32, widths 2..l (-1 if absent) */
   int64_t off_x;    /* x†    fp64 per row (log2 units)        */
   int64_t off_lq;   /* log|go|-o, widths 2..l (after backward)*/
-  int64_t off_flag; /* int32 error flags (bit0: non-finite logZ in backward) */
+  int64_t off_flag; /* int32 error flags (FI_FLAG_ZERO_PROB | FI_FLAG_BAD_LENGTH) */
   int64_t chart_fmt; /* FI_CHART_F32 or FI_CHART_F16: storage of a, b, lq */
   int64_t off_lqs;   /* FI_CHART_F16: fp32 exponent per 32 columns of lq (-1 otherwise) */
 } fi_chart_layout;

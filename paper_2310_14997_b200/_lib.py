@@ -23,6 +23,8 @@ FI_GEMM_FP32 = 2
 FI_CHART_AUTO = 0
 FI_CHART_F32 = 1
 FI_CHART_F16 = 2
+FI_FLAG_ZERO_PROB = 1
+FI_FLAG_BAD_LENGTH = 2
 
 PROF_CLASSES = ("prep", "split_fwd", "gemm_fwd", "seed", "gather_bwd", "gemm_dgrad",
                 "gemm_wgrad")

@@ -121,7 +121,7 @@ struct Plan {
   int N, P, B, l, Np, Pp, esz;
   Decomp dsplit, dgather;
   long long rows;
-  size_t wnn, wnp, e1, eall, gall, a, b, o, lq, lqs, x, top, topz, wsum, flag, kpart, total;
+  size_t wnn, wnp, e1, eall, gall, a, b, o, lq, lqs, x, top, topz, wsum, flag, lens, kpart, total;
   // element offsets of the lo planes of the GEMM operands (fp32 mode only)
   long long wnn_lo, wnp_lo, e1_lo, eall_lo, gall_lo;
   bool store_o, tf32, split, half_chart;
@@ -245,6 +245,7 @@ int make_plan(const fi_shape* s, Plan* p) {
   p->topz = take(4ull * p->B);
   p->wsum = take(16);
   p->flag = take(256);
+  p->lens = take(4ull * p->B);  // sanitized lengths (k_check_lengths)
   // split-K partial tiles + counters, one region per concurrent stream (dual sweep)
   p->kpart = take(2 * (4ull * kKPartFloats + 4ull * kKPartSems));
   p->total = off;
@@ -804,6 +805,15 @@ int forward_impl(const Plan& p, const float* L, const float* R, const float* roo
   float* TOPZ = at<float>(ws, p.topz);
 
   float* wsum = at<float>(ws, p.wsum);
+  int* flag = at<int>(ws, p.flag);
+  {  // length guard first: every later kernel reads the sanitized copy
+    ProfScope prof(FI_PROF_PREP, st);
+    FI_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    k_check_lengths<<<(p.B + 255) / 256, 256, 0, st>>>(lengths, at<int>(ws, p.lens), logZ, flag,
+                                                        p.B, p.l);
+    FI_CUDA(cudaGetLastError());
+    lengths = at<int>(ws, p.lens);
+  }
   {  // K1: exp of the child tables, once per call
     ProfScope prof(FI_PROF_PREP, st);
     FI_CUDA(cudaMemsetAsync(wsum, 0, 16, st));
@@ -978,6 +988,10 @@ int backward_impl(const Plan& p, const float* L, const float* R, const float* ro
   int* flag = at<int>(ws, p.flag);
 
   FI_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+  k_check_lengths<<<(p.B + 255) / 256, 256, 0, st>>>(lengths, at<int>(ws, p.lens), nullptr, flag,
+                                                      p.B, p.l);
+  FI_CUDA(cudaGetLastError());
+  lengths = at<int>(ws, p.lens);
   {
   ProfScope prof(FI_PROF_SEED, st);
   (void)logZ;  // the fp64-consistent log2 Z - x† (TOPZ) is used instead
@@ -1213,6 +1227,9 @@ int fi_marginals(const fi_shape* shape, const int32_t* lengths, const float* gra
   const long long nrows = p.rows - rowbase(2, p.B, p.l);
   if (nrows <= 0) return FI_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  k_check_lengths<<<(p.B + 255) / 256, 256, 0, st>>>(lengths, at<int>(ws, p.lens), nullptr,
+                                                      nullptr, p.B, p.l);
+  lengths = at<int>(ws, p.lens);
   (p.half_chart ? k_marginals<true> : k_marginals<false>)<<<static_cast<unsigned>(nrows), 256, 0, st>>>(
       at<float>(ws, p.lq), p.half_chart ? at<float>(ws, p.lqs) : nullptr, at<float>(ws, p.o),
       grad_log_z, lengths, mu, p.B, p.l, p.Np, p.N);
@@ -1229,6 +1246,9 @@ int fi_span_marginals(const fi_shape* shape, const int32_t* lengths, const float
   const long long nrows = p.rows - rowbase(2, p.B, p.l);
   if (nrows <= 0) return FI_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  k_check_lengths<<<(p.B + 255) / 256, 256, 0, st>>>(lengths, at<int>(ws, p.lens), nullptr,
+                                                      nullptr, p.B, p.l);
+  lengths = at<int>(ws, p.lens);
   (p.half_chart ? k_span_mass<true> : k_span_mass<false>)<<<static_cast<unsigned>(nrows), 256, 0,
                                                              st>>>(
       at<float>(ws, p.lq), p.half_chart ? at<float>(ws, p.lqs) : nullptr, at<float>(ws, p.o),

@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(256) k_mbr_cky(const float* __restrict__ mass,
                                                  int* __restrict__ split, int B, int lmax) {
   const int b = blockIdx.x;
   const int len = lengths[b];
+  if (len < 2 || len > lmax) return;  // invalid sentence: no tree (the host refuses it)
   const int ld = lmax + 1;
   float* sc = score + static_cast<long long>(b) * lmax * ld;
   int* sp = split + static_cast<long long>(b) * lmax * ld;
@@ -372,6 +373,11 @@ __global__ void __launch_bounds__(256) k_vit_backtrack(
     __syncthreads();
     return make_float2(rv, __int_as_float(r));
   };
+  if (len < 2 || len > lmax) {  // invalid sentence: NaN score, no nodes (the host refuses it)
+    if (threadIdx.x == 0) best_score[b] = __int_as_float(0x7fc00000);
+    for (int k = threadIdx.x; k < 2 * lmax * 3; k += blockDim.x) out[k] = -1;
+    return;
+  }
   // root symbol
   float v = kNegInf;
   int vi = 0x7fffffff;

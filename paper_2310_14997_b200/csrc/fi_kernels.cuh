@@ -209,6 +209,28 @@ __global__ void __launch_bounds__(256) k_prep_weights(
 }
 
 // ---------------------------------------------------------------------------
+// Length guard (inside.py:113-121 refuses sentences shorter than 2; the
+// batched op also needs lengths[b] <= lmax).  Writes the sanitized copy every
+// later kernel reads: a length outside [2, lmax] becomes 0, which makes the
+// sentence inert (no span is live, no log Z / seed / gradient contribution,
+// every chart write stays inside the workspace); its log Z is NaN and the
+// FI_FLAG_BAD_LENGTH bit is set for the host to raise on.
+// ---------------------------------------------------------------------------
+__global__ void k_check_lengths(const int* __restrict__ lengths, int* __restrict__ lens,
+                                float* __restrict__ logZ, int* __restrict__ flag, int B,
+                                int lmax) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int len = lengths[b];
+  const bool ok = len >= 2 && len <= lmax;
+  lens[b] = ok ? len : 0;
+  if (!ok) {
+    if (logZ) logZ[b] = __int_as_float(0x7fc00000);  // NaN
+    if (flag) atomicOr(flag, FI_FLAG_BAD_LENGTH);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Width 1: o[1] = unary (inside.py:296-298); x† = max; E1 = exp(unary - x†).
 // One CTA per (sentence, position).  Padded positions get E1 = 0, x† = 0.
 // ---------------------------------------------------------------------------
@@ -802,14 +824,16 @@ __global__ void k_seed_bwd(const float* __restrict__ root, const float* __restri
   for (int b = 0; b < B; ++b) {
     const float z = TOPZ[b];
     const float gb = g[b];
+    const int len = lengths[b];  // sanitized: 0 marks an invalid sentence (k_check_lengths)
+    if (len < 2) continue;
     const bool finite = isfinite(z);
-    if (!finite && c == 0) atomicOr(flag, 1);
+    if (!finite && c == 0) atomicOr(flag, FI_FLAG_ZERO_PROB);
     float lq = kNegInf;
     if (finite && gb != 0.f && c < N) {
       lq = fmaf(root[c], kLog2e, -z) + log2f(fabsf(gb));
       acc += gb * exp2f(TOP[static_cast<long long>(b) * Np + c] - z);
     }
-    const long long row = chart_row(lengths[b], b, 0, B, lmax);
+    const long long row = chart_row(len, b, 0, B, lmax);
     if constexpr (kHalfLQ) {  // fp16 outside weight with a per-chunk exponent
       float mx = lq;
 #pragma unroll

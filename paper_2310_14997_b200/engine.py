@@ -121,6 +121,25 @@ class DeviceGrammar:
         return self.emit.t()[tokens].contiguous()
 
 
+_DG_CACHE: list = []  # the last few (grammar, DeviceGrammar) pairs, by identity
+
+
+def device_grammar(g) -> DeviceGrammar:
+    """The device copy of ``g``, uploaded once and reused across per-sentence
+    engine calls (the reference's train loop calls the engine once per
+    sentence with the same grammar, train.py:208).  Grammars are immutable
+    (read-only arrays, grammar.py:56-59), so identity is a sound key; the
+    cache holds strong references to at most 2 grammars."""
+    dev = _device()
+    for gg, dg in _DG_CACHE:
+        if gg is g and dg.device == dev:
+            return dg
+    dg = DeviceGrammar(g, dev)
+    _DG_CACHE.insert(0, (g, dg))
+    del _DG_CACHE[2:]
+    return dg
+
+
 def _chart_from_workspace(ws: torch.Tensor, shape, n_nt: int, length: int,
                           unary_row: np.ndarray) -> InsideChart:
     """Copy one sentence's chart (batch row 0) to the reference layout.
@@ -174,7 +193,7 @@ def inside_b200(g, tokens, meter: AllocMeter | None = None,
     and keeps the device state so inside_backward_b200 can recompute."""
     toks = _prepare(g, tokens)
     l = int(toks.size)
-    dg = DeviceGrammar(g)
+    dg = device_grammar(g)
     tok_d = torch.as_tensor(toks, device=dg.device).view(1, l)
     unary = dg.unary(tok_d)
     lengths = torch.tensor([l], dtype=torch.int32, device=dg.device)
@@ -201,7 +220,16 @@ def inside_backward_b200(g, tokens, chart: InsideChart):
     if chart.length != l:
         raise InsideError(f"chart length {chart.length} != sentence length {l}")
     st = chart._device
-    if st is None or not np.array_equal(st["tokens"], toks):
+    mismatch = (st is None or not np.array_equal(st["tokens"], toks)
+                or not np.array_equal(chart.o[1][:, g.dims.n_nt:],
+                                      np.asarray(g.log_emit)[:, toks].T))   # inside.py:390
+    if not mismatch and st["dg"].g is not g:
+        # the device state holds the forward's grammar: gradients are only
+        # meaningful for that same grammar
+        og = st["dg"].g
+        mismatch = not all(np.array_equal(np.asarray(getattr(og, k)), np.asarray(getattr(g, k)))
+                           for k in ("log_root", "log_left", "log_right", "log_emit"))
+    if mismatch:
         raise InsideError("chart was not produced from this grammar and sentence")
     if not np.isfinite(chart.log_z):
         raise InsideError("zero-probability sentence; gradients undefined")
@@ -253,7 +281,7 @@ def batched_inside(g, sentences, gemm_dtype: str = DEFAULT_GEMM_DTYPE,
                    dg: DeviceGrammar | None = None) -> np.ndarray:
     """log_z of every sentence, in equal-length device batches."""
     sents = [_prepare(g, s) for s in sentences]
-    dg = dg or DeviceGrammar(g)
+    dg = dg or device_grammar(g)
     out = np.empty(len(sents))
     by_len: dict[int, list[int]] = {}
     for k, s in enumerate(sents):

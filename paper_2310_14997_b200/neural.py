@@ -48,6 +48,10 @@ class ParamError(Exception):
     """Invalid parameters or a non-finite value (neuralparam.py:24-25)."""
 
 
+class TrainError(Exception):
+    """A diverged training run: non-finite loss (train.py:33-34, :209-212)."""
+
+
 def tensor_shapes(dims: GrammarDims, d: int) -> dict[str, tuple[int, ...]]:
     """Names and shapes of the embedding parameterisation (neuralparam.py:70-83)."""
     shapes: dict[str, tuple[int, ...]] = {
@@ -181,13 +185,17 @@ class AdamState:
                          {k: torch.zeros_like(x) for k, x in tensors.items()})
 
 
+def grad_norm(grads: dict[str, torch.Tensor]) -> torch.Tensor:
+    """Joint L2 norm of all gradients (a device scalar: no host sync)."""
+    return torch.linalg.vector_norm(torch.stack([torch.linalg.vector_norm(x)
+                                                 for x in grads.values()]))
+
+
 def clip_grads_(grads: dict[str, torch.Tensor], max_norm: float) -> torch.Tensor:
     """Scale all gradients so their joint norm is at most max_norm (train.py:133-142).
     Returns the pre-clip norm (a device scalar: no host sync)."""
-    g = list(grads.values())
-    norm = torch.linalg.vector_norm(torch.stack([torch.linalg.vector_norm(x) for x in g]))
-    scale = torch.clamp(max_norm / norm, max=1.0)
-    torch._foreach_mul_(g, scale)
+    norm = grad_norm(grads)
+    torch._foreach_mul_(list(grads.values()), torch.clamp(max_norm / norm, max=1.0))
     return norm
 
 
@@ -261,17 +269,14 @@ class TrainStep:
             return grammar_tables(self.params, self.config.tied, finite_flags)
         return direct_tables(self.params, self.config.tied)
 
-    def loss_and_grads(self, tokens: torch.Tensor, lengths: torch.Tensor,
-                       global_batch: int | None = None):
-        """Loss = -sum(log Z) / global_batch and its parameter gradients
-        (the train.py:208-224 chain, batched: tables -> unary gather ->
-        inside fwd+bwd on the engine -> autograd through the tables)."""
+    def _forward_backward(self, tokens: torch.Tensor, lengths: torch.Tensor, denom: float):
+        """tables -> unary gather -> inside fwd+bwd on the engine -> autograd
+        through the tables (the train.py:208-224 chain, batched) with
+        loss = -sum(log Z) / denom.  Returns (loss, grads, log_z, checks):
+        ``checks`` are device booleans queued with the step and read once by
+        the caller (no host sync in front of the engine)."""
         cfg = self.config
         xs = list(self.params.tensors.values())
-        # activation checks are deferred: queued on the device with the whole
-        # forward + backward, read once at the end (one host sync, no bubble
-        # in front of the engine); a non-finite activation raises ParamError
-        # before any parameter is updated, as in the reference
         flags: list = []
         # the score-table GEMMs (N x d x (N+P)) run on TF32 tensor cores in the
         # fast modes; fp32 mode keeps exact fp32 products (parity mode)
@@ -280,31 +285,85 @@ class TrainStep:
         try:
             log_root, log_left, log_right, log_emit = self.tables(flags)
             unary = log_emit.T[tokens]                                 # inside.py:296-298
+            # lengths are checked with the other deferred flags (validate=False:
+            # an invalid one makes its sentence inert with log Z = NaN)
+            flags.append(("lengths", ((lengths >= 2) & (lengths <= tokens.shape[1])).all()))
             log_z = inside(log_left.contiguous(), log_right.contiguous(), log_root.contiguous(),
-                           unary.contiguous(), lengths, gemm_dtype=cfg.gemm_dtype)
-            nb = global_batch or tokens.shape[0]
-            loss = -log_z.sum() / nb                                   # train.py:218: -1/B
+                           unary.contiguous(), lengths, gemm_dtype=cfg.gemm_dtype,
+                           validate=False)
+            loss = -log_z.sum() / denom                                # train.py:218: -1/B
             grads = torch.autograd.grad(loss, xs, allow_unused=True)  # tied: f4 unused
         finally:
             torch.backends.cuda.matmul.allow_tf32 = prev
-        if flags:
-            ok = torch.stack([f for _, f in flags]).cpu()
-            if not bool(ok.all()):
-                raise ParamError(f"non-finite activation in {flags[int((~ok).nonzero()[0])][0]}")
-        return loss, [torch.zeros_like(x) if g is None else g for x, g in zip(xs, grads)]
+        grads = [torch.zeros_like(x) if g is None else g for x, g in zip(xs, grads)]
+        return loss, grads, log_z, flags
+
+    def _raise_on(self, flags, ok, log_z, lengths, loss_finite: bool, grad_finite: bool,
+                  step_no: int):
+        """The reference's error order: a non-finite activation (ParamError,
+        raised while the grammar is built), an invalid sentence length
+        (inside.py:113-121), a non-finite log Z (TrainError, train.py:209-212),
+        a non-finite gradient (ParamError, neuralparam.py:341-343) -- all
+        before any parameter is touched."""
+        for (name, _), good in zip(flags, ok):
+            if not good:
+                if name == "lengths":
+                    b = int(((lengths < 2) | (lengths > self._lmax)).nonzero()[0, 0])
+                    raise ValueError(f"sentence {b}: length {int(lengths[b])} outside "
+                                     f"[2, {self._lmax}]")
+                raise ParamError(f"non-finite activation in {name}")
+        if not loss_finite:
+            bad = (~torch.isfinite(log_z)).nonzero()
+            if bad.numel():  # this rank holds the sentence (else another rank does)
+                b = int(bad[0, 0])
+                raise TrainError(f"non-finite loss at step {step_no}: sentence {b} has log "
+                                 f"probability {float(log_z[b])}")
+            raise TrainError(f"non-finite loss at step {step_no} (on another rank)")
+        if not grad_finite:
+            raise ParamError("non-finite gradient")
+
+    def loss_and_grads(self, tokens: torch.Tensor, lengths: torch.Tensor,
+                       global_batch: int | None = None):
+        """Loss = -sum(log Z) / global_batch and its parameter gradients on this
+        rank (no collective); raises like the reference before returning."""
+        self._lmax = int(tokens.shape[1])
+        loss, grads, log_z, flags = self._forward_backward(tokens, lengths,
+                                                           float(global_batch or tokens.shape[0]))
+        ok = torch.stack([f for _, f in flags] + [torch.isfinite(loss)]).cpu().tolist()
+        self._raise_on(flags, ok[:-1], log_z, lengths, ok[-1], True, self.state.t + 1)
+        return loss, grads
 
     def step(self, tokens: torch.Tensor, lengths: torch.Tensor, global_batch: int | None = None,
              group=None) -> torch.Tensor:
+        """One optimisation step; returns the global mean NLL (device scalar).
+
+        Under torch.distributed the parameter gradients, the loss and (when
+        ``global_batch`` is not given) the sentence count travel in ONE flat
+        all-reduce, so uneven shards still average over the global batch."""
         cfg = self.config
         names = list(self.params.tensors)
         xs = [self.params.tensors[k] for k in names]
-        loss, grads = self.loss_and_grads(tokens, lengths, global_batch)
+        self._lmax = int(tokens.shape[1])
         world = dist.get_world_size(group) if dist.is_initialized() else 1
-        if world > 1:  # one collective: the flat parameter-gradient bucket (+ the loss)
-            *grads, loss = allreduce_grads(list(grads) + [loss.detach().reshape(1)], group)
-            loss = loss[0]
+        count_in_bucket = world > 1 and global_batch is None
+        denom = 1.0 if count_in_bucket else float(global_batch or tokens.shape[0])
+        loss, grads, log_z, flags = self._forward_backward(tokens, lengths, denom)
+        if world > 1:  # one collective: [parameter grads | loss | sentence count]
+            extra = [loss.detach().reshape(1)]
+            if count_in_bucket:
+                extra.append(torch.full((1,), float(tokens.shape[0]), device=loss.device))
+            out = allreduce_grads(list(grads) + extra, group)
+            grads, loss = out[:len(grads)], out[len(grads)][0]
+            if count_in_bucket:  # the global mean over however the batch was sharded
+                count = out[-1][0]
+                grads = [g / count for g in grads]
+                loss = loss / count
         gd = dict(zip(names, grads))
-        clip_grads_(gd, cfg.clip)
+        norm = grad_norm(gd)
+        ok = torch.stack([f for _, f in flags] + [torch.isfinite(loss), torch.isfinite(norm)])
+        ok = ok.cpu().tolist()  # the step's single host read
+        self._raise_on(flags, ok[:-2], log_z, lengths, ok[-2], ok[-1], self.state.t + 1)
+        torch._foreach_mul_(list(gd.values()), torch.clamp(cfg.clip / norm, max=1.0))
         with torch.no_grad():
             adam_step({k: x.data for k, x in zip(names, xs)}, gd, self.state, lr=cfg.lr,
                       beta1=cfg.beta1, beta2=cfg.beta2, eps=cfg.eps, check_finite=False)

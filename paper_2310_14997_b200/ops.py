@@ -56,6 +56,28 @@ def _check_inputs(L, R, root, unary, lengths):
     return n, p, unary.shape[0], unary.shape[1]
 
 
+def check_lengths(lengths: torch.Tensor, max_len: int) -> None:
+    """Refuse a batch with a sentence outside 2 <= lengths[b] <= max_len before
+    any launch (the reference's _prepare, inside.py:113-121, refuses length < 2).
+
+    One device->host read.  Skipped while a CUDA graph is being captured: the
+    library's own device-side guard (k_check_lengths) then makes such a
+    sentence inert with log Z = NaN and sets FI_FLAG_BAD_LENGTH."""
+    if lengths.numel() == 0 or (lengths.is_cuda and torch.cuda.is_current_stream_capturing()):
+        return
+    bad = (lengths < 2) | (lengths > max_len)
+    if bool(bad.any()):
+        b = int(bad.nonzero()[0, 0])
+        raise ValueError(f"sentence {b}: length {int(lengths[b])} outside [2, {max_len}] "
+                         f"(need a token sequence of length >= 2 that fits the padded batch)")
+
+
+def read_flags(ws: torch.Tensor, shape) -> int:
+    """The library's flag word (FI_FLAG_ZERO_PROB | FI_FLAG_BAD_LENGTH) of a workspace."""
+    off = int(_lib.chart_layout(shape).off_flag)
+    return int(ws[off:off + 4].view(torch.int32).item())
+
+
 @torch.library.custom_op("flashinside::inside_fwd", mutates_args=())
 def inside_fwd(L: torch.Tensor, R: torch.Tensor, root: torch.Tensor, unary: torch.Tensor,
                lengths: torch.Tensor, gemm_dtype: str, store_chart: bool,
@@ -130,14 +152,21 @@ inside_fwd.register_autograd(_backward, setup_context=_setup_context)
 
 
 def inside(L: torch.Tensor, R: torch.Tensor, root: torch.Tensor, unary: torch.Tensor,
-           lengths: torch.Tensor, gemm_dtype: str = "bf16", chart_dtype: str = "auto"
-           ) -> torch.Tensor:
+           lengths: torch.Tensor, gemm_dtype: str = "bf16", chart_dtype: str = "auto",
+           validate: bool = True) -> torch.Tensor:
     """Per-sentence log partition log Z (B,), differentiable in L, R, root, unary.
 
     gemm_dtype: "bf16" | "tf32" (fast modes, 2e-3 parity bound) or "fp32"
     (bf16x3 split operands, 1e-4 bound).  chart_dtype: storage of the
     projected chart vectors between GEMM and split kernels -- "auto" (fp16
-    linear in the fast modes, fp32 log in fp32 mode), "fp32" or "fp16"."""
+    linear in the fast modes, fp32 log in fp32 mode), "fp32" or "fp16".
+    validate: raise ValueError naming the first sentence whose length is
+    outside [2, l] (one host read); with validate=False such a sentence gets
+    log Z = NaN and no gradient (the device-side guard), for callers that
+    check log Z themselves without a sync (TrainStep).  A zero-probability
+    sentence returns log Z = -inf and contributes no gradient."""
+    if validate:
+        check_lengths(lengths, unary.shape[1] if unary.dim() == 3 else 0)
     log_z, _ = inside_fwd(L, R, root, unary, lengths, gemm_dtype, False, chart_dtype)
     return log_z
 
@@ -145,6 +174,7 @@ def inside(L: torch.Tensor, R: torch.Tensor, root: torch.Tensor, unary: torch.Te
 def inside_with_workspace(L, R, root, unary, lengths, gemm_dtype="bf16", store_chart=False,
                           chart_dtype="auto"):
     """Forward only, returning (log_z, workspace) for chart export / explicit backward."""
+    check_lengths(lengths, unary.shape[1] if unary.dim() == 3 else 0)
     with torch.no_grad():
         return inside_fwd(L, R, root, unary, lengths, gemm_dtype, store_chart, chart_dtype)
 

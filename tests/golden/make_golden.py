@@ -109,7 +109,9 @@ def main():
     lls, ppl = corpus_log_likelihood(g, list(toks))
     gold["cfg1_logz"] = np.array(lls)
     gold["cfg1_ppl"] = np.array(ppl)
-    for n, l in ((1024, 30), (4096, 40)):
+    # config 2, 3, 4 (|N| = 4096 at l = 10..60) and 5 (|N| = 8192): sentence 0
+    for n, l in ((1024, 30), (4096, 40), (4096, 10), (4096, 20), (4096, 30), (4096, 50),
+                 (4096, 60), (8192, 40)):
         g = random_grammar(GrammarDims(n, n, 64), seed=0)
         t = np.random.default_rng(1).integers(0, 64, (1, l))[0]
         gold[f"cfg_n{n}_l{l}_logz0"] = np.array(inside_flash(g, t).log_z)

@@ -1,0 +1,226 @@
+"""Parity at the BASELINE.json configurations themselves:
+the op on exactly the inputs bench.py times, against the float64 oracle
+(inside_batch_equal, gated against the per-sentence restatement and the
+reference's goldens in tests/test_oracle.py), element-wise.
+
+* config 3 (|N| = N = P = 4096, l = 40, B = 64): log Z of all 64 sentences
+  and every gradient table for the training loss (grad_log_z = -1/B,
+  train.py:218), in bench.py's default mode (bf16 operands, fp16 linear
+  chart), in tf32 and in the strict fp32 mode;
+* config 2 (|N| = 1024, l = 30, B = 32): the same, all modes;
+* config 5 (|N| = 8192, l = 40, B = 128, bf16): log Z of sentence 0 against
+  the reference's own value (tests/golden/make_golden.py), of sentences
+  0, 1, 127 against the oracle, and the gradients of a batch whose upstream
+  gradient lives on sentences 0 and 127;
+* peaked grammars (Dirichlet concentration 0.1 / 0.3, and a grammar after
+  200 training steps), where many rule probabilities sit far below the fp16
+  chart's 2^-28 flush point -- the fast mode's storage decision.
+
+Tolerances (north star): 1e-4 relative in fp32 mode, 2e-3 with bf16 / tf32
+operands; tables element-wise with the absolute floor rtol * max|want|
+(SURVEY D5).
+"""
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import flashinside_oracle as O
+
+pytestmark = pytest.mark.gpu
+GOLD = np.load(Path(__file__).parent / "golden" / "golden.npz")
+RTOL = {"fp32": 1e-4, "tf32": 2e-3, "bf16": 2e-3}
+V = 64
+
+
+def run_op(root, left, right, unary, lengths, grad, gemm_dtype, chart_dtype="auto"):
+    from paper_2310_14997_b200.ops import inside
+    dev = "cuda"
+    L = torch.tensor(left, dtype=torch.float32, device=dev, requires_grad=True)
+    R = torch.tensor(right, dtype=torch.float32, device=dev, requires_grad=True)
+    rt = torch.tensor(root, dtype=torch.float32, device=dev, requires_grad=True)
+    un = torch.tensor(unary, dtype=torch.float32, device=dev, requires_grad=True)
+    ln = torch.tensor(lengths, dtype=torch.int32, device=dev)
+    log_z = inside(L, R, rt, un, ln, gemm_dtype=gemm_dtype, chart_dtype=chart_dtype)
+    (log_z * torch.tensor(grad, dtype=torch.float32, device=dev)).sum().backward()
+    torch.cuda.synchronize()
+    out = {"log_z": log_z.detach().cpu().double().numpy(),
+           "dL": L.grad.cpu().double().numpy(), "dR": R.grad.cpu().double().numpy(),
+           "droot": rt.grad.cpu().double().numpy(), "dunary": un.grad.cpu().double().numpy()}
+    del L, R, rt, un, log_z
+    torch.cuda.empty_cache()
+    return out
+
+
+def worst(got, want):
+    """Worst element error in units of the D5 bound (rtol = 1)."""
+    return float((np.abs(got - want) / (np.abs(want) + np.abs(want).max() + 1e-300)).max())
+
+
+def assert_close(name, got, want, rtol):
+    floor = rtol * np.abs(want).max()
+    bad = np.abs(got - want) > rtol * np.abs(want) + floor
+    assert not bad.any(), (
+        f"{name}: {bad.sum()} / {bad.size} elements off; worst abs "
+        f"{np.abs(got - want).max():.3e} (max|want| {np.abs(want).max():.3e})")
+
+
+def check_all(got, want, rtol, tag):
+    errs = {k: worst(got[k], want[k]) for k in ("dL", "dR", "droot", "dunary")}
+    live = np.isfinite(want["log_z"])
+    errs["log_z"] = float(np.abs(got["log_z"][live] / want["log_z"][live] - 1).max())
+    print(f"{tag}: worst errors (relative to the bound's scale) {errs}")
+    np.testing.assert_allclose(got["log_z"], want["log_z"], rtol=rtol)
+    for k in ("dL", "dR", "droot", "dunary"):
+        assert_close(k, got[k], want[k], rtol)
+
+
+def bench_inputs(n, batch, length, seed=0):
+    """The grammar and tokens bench.py times (rank 0): random_grammar(N, N, 64,
+    seed=0) Dirichlet(1) rows, tokens default_rng(1).integers(0, 64, (B, l))."""
+    root, left, right, emit = O.random_grammar_arrays(n, n, V, seed=seed)
+    toks = np.random.default_rng(1).integers(0, V, (batch, length))
+    return root, left, right, emit, O.unary_from_tokens(emit, toks)
+
+
+# ------------------------------------------------------------------ config 3
+@pytest.fixture(scope="module")
+def config3():
+    root, left, right, emit, unary = bench_inputs(4096, 64, 40)
+    grad = np.full(64, -1.0 / 64)                       # the training loss, train.py:218
+    want = O.inside_batch_equal(left, right, root, unary, grad)
+    return root, left, right, unary, grad, want
+
+
+@pytest.mark.parametrize("gemm_dtype,chart_dtype", [("bf16", "auto"), ("tf32", "auto"),
+                                                    ("fp32", "auto"), ("bf16", "fp32")])
+def test_config3_full_batch_against_oracle(config3, gemm_dtype, chart_dtype):
+    root, left, right, unary, grad, want = config3
+    assert want["log_z"][0] == pytest.approx(float(GOLD["cfg_n4096_l40_logz0"]), abs=1e-9)
+    got = run_op(root, left, right, unary, np.full(64, 40), grad, gemm_dtype, chart_dtype)
+    check_all(got, want, RTOL[gemm_dtype], f"config3 {gemm_dtype}/{chart_dtype}")
+
+
+def test_config3_signed_upstream_gradients(config3):
+    """Opposite-sign upstream gradients on the same batch (fp32 mode): a
+    mis-indexed row or tile cannot hide behind the loss's uniform sign."""
+    root, left, right, unary, _, _ = config3
+    grad = np.random.default_rng(7).uniform(-1.0, 1.0, 64)
+    grad[::9] = 0.0
+    sel = [0, 5, 31, 62, 63]
+    want = O.inside_batch_equal(left, right, root, unary[sel], grad[sel])
+    g_sel = np.zeros(64)
+    g_sel[sel] = grad[sel]
+    got = run_op(root, left, right, unary, np.full(64, 40), g_sel, "fp32")
+    np.testing.assert_allclose(got["log_z"][sel], want["log_z"], rtol=1e-4)
+    dun = np.zeros_like(got["dunary"])
+    dun[sel] = want["dunary"]
+    want = dict(want, dunary=dun)
+    for k in ("dL", "dR", "droot", "dunary"):
+        assert_close(k, got[k], want[k], 1e-4)
+
+
+# ------------------------------------------------------------------ config 2
+@pytest.fixture(scope="module")
+def config2():
+    root, left, right, emit, unary = bench_inputs(1024, 32, 30)
+    grad = np.full(32, -1.0 / 32)
+    return root, left, right, unary, grad, O.inside_batch_equal(left, right, root, unary, grad)
+
+
+@pytest.mark.parametrize("gemm_dtype,chart_dtype", [("bf16", "auto"), ("tf32", "auto"),
+                                                    ("fp32", "auto"), ("bf16", "fp32"),
+                                                    ("fp32", "fp16")])
+def test_config2_full_batch_against_oracle(config2, gemm_dtype, chart_dtype):
+    root, left, right, unary, grad, want = config2
+    assert want["log_z"][0] == pytest.approx(float(GOLD["cfg_n1024_l30_logz0"]), abs=1e-9)
+    got = run_op(root, left, right, unary, np.full(32, 30), grad, gemm_dtype, chart_dtype)
+    rtol = max(RTOL[gemm_dtype], 2e-3 if chart_dtype == "fp16" else 0.0)
+    check_all(got, want, rtol, f"config2 {gemm_dtype}/{chart_dtype}")
+
+
+# ------------------------------------------------------------------ config 4
+@pytest.mark.parametrize("length", [10, 20, 30, 50, 60])
+def test_config4_lengths_log_z_against_reference(length):
+    """|N| = 4096 at the config-4 lengths (B = 64, bf16 + fp16 chart): log Z
+    of sentence 0 against the reference's own inside_flash value and of
+    sentences 0 and 63 against the oracle."""
+    root, left, right, emit, unary = bench_inputs(4096, 64, length)
+    got = run_op(root, left, right, unary, np.full(64, length), np.full(64, -1.0 / 64), "bf16")
+    assert got["log_z"][0] == pytest.approx(float(GOLD[f"cfg_n4096_l{length}_logz0"]), rel=2e-3)
+    want = O.inside_batch_equal(left, right, root, unary[[0, 63]], backward=False)["log_z"]
+    np.testing.assert_allclose(got["log_z"][[0, 63]], want, rtol=2e-3)
+    assert got["droot"].sum() == pytest.approx(1.0, rel=2e-3)
+
+
+# ------------------------------------------------------------------ config 5
+def test_config5_bf16_against_reference_and_oracle():
+    n, B, l = 8192, 128, 40
+    root, left, right, emit, unary = bench_inputs(n, B, l)
+    sel = [0, 127]
+    grad = np.zeros(B)
+    grad[sel] = -0.5
+    got = run_op(root, left, right, unary, np.full(B, l), grad, "bf16")
+    # the reference's own log Z of sentence 0 (inside_flash, tests/golden)
+    assert got["log_z"][0] == pytest.approx(float(GOLD["cfg_n8192_l40_logz0"]), rel=2e-3)
+    assert float(GOLD["cfg_n8192_l40_logz0"]) == pytest.approx(-172.456118, abs=1e-6)
+    want = O.inside_batch_equal(left, right, root, unary[[0, 1, 127]], grad[[0, 1, 127]])
+    np.testing.assert_allclose(got["log_z"][[0, 1, 127]], want["log_z"], rtol=2e-3)
+    dun = np.zeros_like(got["dunary"])
+    dun[[0, 1, 127]] = want["dunary"]
+    want = dict(want, dunary=dun)
+    errs = {k: worst(got[k], want[k]) for k in ("dL", "dR", "droot", "dunary")}
+    print("config5 bf16 worst errors:", errs)
+    for k in ("dL", "dR", "droot", "dunary"):
+        assert_close(k, got[k], want[k], 2e-3)
+
+
+# ------------------------------------------------------------ peaked grammars
+@pytest.mark.parametrize("conc", [0.1, 0.3])
+@pytest.mark.parametrize("gemm_dtype,chart_dtype", [("bf16", "auto"), ("fp32", "fp16")])
+def test_peaked_dirichlet_grammars(conc, gemm_dtype, chart_dtype):
+    """Dirichlet(0.1 / 0.3) rows (grammar.py:160-180 with a concentration):
+    most rule probabilities are far below 2^-28 (some exactly 0, -inf in log
+    space), the regime where the fp16 linear chart flushes.  |N| = 1024,
+    l = 30, B = 16."""
+    n, B, l = 1024, 16, 30
+    root, left, right, emit = O.random_grammar_arrays(n, n, V, seed=3, concentration=conc)
+    toks = np.random.default_rng(4).integers(0, V, (B, l))
+    unary = O.unary_from_tokens(emit, toks)
+    frac_tiny = float((left < np.log(2.0 ** -28)).mean())
+    grad = np.full(B, -1.0 / B)
+    want = O.inside_batch_equal(left, right, root, unary, grad)
+    got = run_op(root, left, right, unary, np.full(B, l), grad, gemm_dtype, chart_dtype)
+    print(f"conc {conc}: {frac_tiny:.0%} of the rules below 2^-28")
+    check_all(got, want, 2e-3, f"peaked conc={conc} {gemm_dtype}/{chart_dtype}")
+
+
+def test_trained_grammar_fast_mode():
+    """A grammar after 200 training steps on a skewed corpus (the neural
+    parameterisation, TrainStep in fp32 mode) is peaked the way real
+    grammars are; the bf16 + fp16-chart op must still match the oracle."""
+    from paper_2310_14997_b200 import neural
+    from paper_2310_14997_b200.grammar import GrammarDims
+    n, B, l = 512, 16, 20
+    dims = GrammarDims(n, n, V)
+    ts = neural.TrainStep(neural.init_params(dims, 64, 0, device="cuda"),
+                          neural.TrainConfig(gemm_dtype="fp32", lr=0.02))
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    base = torch.randint(0, 8, (B, l), device="cuda", generator=gen)   # a skewed corpus
+    lengths = torch.full((B,), l, dtype=torch.int32, device="cuda")
+    losses = [float(ts.step(base, lengths)) for _ in range(200)]
+    assert losses[-1] < losses[0] - 5.0
+    with torch.no_grad():
+        root, left, right, emit = (t.double().cpu().numpy() for t in ts.tables())
+    frac_tiny = float((left < np.log(2.0 ** -28)).mean())
+    toks = base.cpu().numpy()
+    unary = O.unary_from_tokens(emit, toks)
+    grad = np.full(B, -1.0 / B)
+    want = O.inside_batch_equal(left, right, root, unary, grad)
+    print(f"trained: loss {losses[0]:.2f} -> {losses[-1]:.2f}; "
+          f"{frac_tiny:.0%} of the rules below 2^-28")
+    for gemm_dtype in ("bf16", "fp32"):
+        got = run_op(root, left, right, unary, np.full(B, l), grad, gemm_dtype)
+        check_all(got, want, RTOL[gemm_dtype], f"trained {gemm_dtype}")
