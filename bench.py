@@ -5,10 +5,14 @@ kernel and the CPU oracle timed on the same host.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
+(--gpus N > 1 without torchrun relaunches itself under torch.distributed.run.)
 One step = forward + backward of the inside op over one batch of B sentences
-per GPU (weak scaling: B per rank, the batch is sharded across ranks), plus
-one NCCL all-reduce of the grammar gradients [dL | dR | droot] when N > 1.
-Rank 0 prints ONE JSON line.
+per GPU (weak scaling, the default: B per rank; --scaling strong shards a
+global B), through dp.DataParallelInside: the grammar gradients land in one
+flat [dL | dR | droot] bucket that is all-reduced over NCCL when N > 1 (dL's
+chunk overlapping dR's weight-gradient GEMM), the whole step captured as one
+CUDA graph.  At N > 1 the other scaling mode is measured too
+("scaling_other").  Rank 0 prints ONE JSON line.
 """
 
 from __future__ import annotations
@@ -183,14 +187,15 @@ def algorithmic_work(n: int, p: int, batch: int, length: int, gemm_esz: int, sto
     }
 
 
-def run_e2e(args, g, tokens, step, dev, batch, n, world, barrier):
+def run_e2e(args, g, tokens, dpi, lengths, gvec, dev, batch, n, world, barrier):
     """End-to-end through host buffers, the reference-facing call pattern:
     every step copies its inputs (grammar tables + tokens) from pinned host
-    memory to the GPU, runs fwd+bwd, and copies log_z and the GrammarGrad
-    tables (dL, dR, droot, d_emit) back to pinned host memory.  Copies run on
-    their own streams, double-buffered, so step k+1's H2D and step k's D2H
-    overlap step k's compute -- what a training loop feeding the op does.
-    The timer covers all copies of all K steps (final sync included)."""
+    memory to the GPU, runs fwd+bwd (+ the all-reduce at N > 1), and copies
+    log_z and the GrammarGrad tables (dL, dR, droot, d_emit) back to pinned
+    host memory.  Copies run on their own streams, double-buffered, so step
+    k+1's H2D and step k's D2H overlap step k's compute -- what a training
+    loop feeding the op does.  The timer covers all copies of all K steps
+    (final sync included)."""
     import torch
     import torch.distributed as dist
 
@@ -225,33 +230,33 @@ def run_e2e(args, g, tokens, step, dev, batch, n, world, barrier):
             t.record_stream(comp)
         return d, ev
 
+    out_free = [None, None]  # D2H of the output slot finished (events on s_out)
+
     def run(nsteps):
         nxt = upload(0)
-        pending = []
         for k in range(nsteps):
             d, ev = nxt
             comp.wait_event(ev)
             if k + 1 < nsteps:
                 nxt = upload(k + 1)
-            Ld = d["L"].requires_grad_(True)
-            Rd = d["R"].requires_grad_(True)
-            rd = d["root"].requires_grad_(True)
-            un = d["emit"].t()[d["tok"]].contiguous().requires_grad_(True)
-            log_z, _, dL, dR, droot, dun = step(Ld, Rd, rd, un)
+            un = d["emit"].t()[d["tok"]].contiguous()
+            if out_free[k % 2] is not None:   # step k-2's D2H of this slot is done
+                comp.wait_event(out_free[k % 2])
+            log_z, dL, dR, droot, dun = dpi.step(d["L"], d["R"], d["root"], un, lengths, gvec,
+                                                 slot=k % 2)
             d_emit = torch.zeros(VOCAB, n, device=dev).index_add_(
                 0, d["tok"].view(-1), dun.reshape(-1, n))          # inside.py:420-423
-            res = (dL, dR, droot, d_emit.t(), log_z.detach())
+            res = (dL, dR, droot, d_emit.t(), log_z)
             done = torch.cuda.Event()
             done.record(comp)
             s_out.wait_event(done)
             with torch.cuda.stream(s_out):
                 for dst, src in zip(outs[k % 2], res):
                     dst.copy_(src, non_blocking=True)
+            out_free[k % 2] = torch.cuda.Event()
+            out_free[k % 2].record(s_out)
             for t in res:
                 t.record_stream(s_out)
-            pending.append(res)
-            if len(pending) > 2:
-                pending.pop(0)
         s_out.synchronize()
         comp.synchronize()
 
@@ -267,16 +272,37 @@ def run_e2e(args, g, tokens, step, dev, batch, n, world, barrier):
         ems = float(t.item())
     return {"value": world * batch / (ems / 1e3), "unit": "sentences/s", "ms_per_step": ems,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "path": "pinned host grammar+tokens -> H2D -> op fwd+bwd -> D2H log_z + "
-                    "GrammarGrad (dL, dR, droot, d_emit); copies on side streams, "
+            "path": "pinned host grammar+tokens -> H2D -> engine fwd+bwd (dp.DataParallelInside: "
+                    "C-ABI fi_inside_forward / fi_inside_backward_ex, + all-reduce at N>1) -> "
+                    "D2H log_z + GrammarGrad (dL, dR, droot, d_emit); copies on side streams, "
                     "double-buffered across steps; wall clock over K steps"}
 
 
+def tensor_peak(gemm_dtype: str, peaks: dict) -> tuple[float, str]:
+    """The tensor-core peak that matches the GEMM operand type.  Kernels here
+    are timed over a sub-second region, so the burst (not the 4-s sustained)
+    bf16 figure applies; tf32 uses the TF32 peak measured on the box
+    (profiles/measured_tf32.json: torch.matmul tf32 8192^3, best of 10) when
+    present, else half the bf16 burst (the dense tf32:bf16 ratio); fp32 mode
+    issues three bf16 MMAs per product (hi*hi + hi*lo + lo*hi), so its
+    algorithmic flops are held to a third of the bf16 burst."""
+    if gemm_dtype == "tf32":
+        f = ROOT / "profiles" / "measured_tf32.json"
+        if f.exists():
+            d = json.loads(f.read_text())
+            return float(d["tf32_tflops"]), "measured tf32 burst (profiles/measured_tf32.json)"
+        return peaks["bf16_tflops"] / 2, peaks["source"] + " bf16 burst / 2 (tf32 dense ratio)"
+    if gemm_dtype == "fp32":
+        return peaks["bf16_tflops"] / 3, peaks["source"] + " bf16 burst / 3 (bf16x3 operands)"
+    return peaks["bf16_tflops"], peaks["source"] + " bf16 burst"
+
+
 def roofline_block(prof: dict, steps: int, n: int, batch: int, length: int, esz: int,
-                   chart_esz: int) -> dict:
+                   chart_esz: int, gemm_dtype: str = "bf16") -> dict:
     """roofline{} of the dominant kernel class from per-class CUDA-event
     times (_lib.profile_collect over `steps` steps) and the algorithmic work."""
     peaks = measured_peaks()
+    t_peak, t_src = tensor_peak(gemm_dtype, peaks)
     work = algorithmic_work(n, n, batch, length, esz, store_o=False, chart_esz=chart_esz)
     per_class = {}
     for name, (tot_ms, cnt) in prof.items():
@@ -291,15 +317,14 @@ def roofline_block(prof: dict, steps: int, n: int, batch: int, length: int, esz:
         unit = "GB/s"
     else:
         achieved = amount / (k_ms / 1e3) / 1e12
-        peak = peaks["bf16_tflops_sustained"]
+        peak = t_peak
         unit = "TFLOP/s"
     for name, d in per_class.items():
         if name in work:
             b, amt = work[name]
             d["achieved"] = amt / (d["ms_per_step"] / 1e3) / (1e9 if b == "hbm" else 1e12)
             d["unit"] = "GB/s" if b == "hbm" else "TFLOP/s"
-            d["frac"] = d["achieved"] / (peaks["hbm_gbs"] if b == "hbm"
-                                         else peaks["bf16_tflops_sustained"])
+            d["frac"] = d["achieved"] / (peaks["hbm_gbs"] if b == "hbm" else t_peak)
     # DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of one launch
     # of the dominant class from the committed ncu --set full capture, next
     # to the compulsory bytes of that same launch (scripts/summarize_profiles.py)
@@ -314,7 +339,8 @@ def roofline_block(prof: dict, steps: int, n: int, batch: int, length: int, esz:
             "traffic_launch": traffic_launch,
             "method": "algorithmic work per step / CUDA-event time of the class's launches "
                       "(same K steps re-run with per-launch events)",
-            "peak_source": peaks["source"] + (" sustained" if bound == "tensor" else ""),
+            "peak_source": t_src if bound == "tensor" else peaks["source"] + " HBM copy",
+            "tensor_peak": {"value": t_peak, "source": t_src},
             "per_class": per_class}
 
 
@@ -323,8 +349,15 @@ def init_dist(world: int, local: int):
     devices exercises the multi-rank code path on a single-GPU box)."""
     import torch
     import torch.distributed as dist
-    backend = os.environ.get("FI_DIST_BACKEND", "nccl")
-    dev_idx = local % max(torch.cuda.device_count(), 1)
+    ngpu = max(torch.cuda.device_count(), 1)
+    # more ranks than GPUs (a multi-rank dry run on a 1-GPU box): NCCL refuses
+    # two ranks on one device, so those runs use gloo (eager, no graphs)
+    backend = os.environ.get("FI_DIST_BACKEND", "nccl" if world <= ngpu else "gloo")
+    if world > 1 and backend == "nccl":
+        # NCCL's communicator init lines (one per rank) stay in the log
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    dev_idx = local % ngpu
     torch.cuda.set_device(dev_idx)
     dev = torch.device("cuda", dev_idx)
     if world > 1:
@@ -332,111 +365,128 @@ def init_dist(world: int, local: int):
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
-    return dev
+    return dev, backend
 
 
 # -------------------------------------------------------------- our arm
+def timed_steps(step, steps, warmup, use_graph, barrier, lib, dev):
+    """W eager warm-up steps, then (optionally) capture one step as a CUDA
+    graph -- NCCL all-reduce included when N > 1 -- and time K steps with
+    CUDA events between barriers.  Returns (ms per step, our kernel launches
+    in the timed region, launch mode)."""
+    import torch
+    for _ in range(warmup):
+        step()
+    barrier()
+    graph, graph_launches, mode = None, 0, "eager"
+    if use_graph:
+        try:
+            side = torch.cuda.Stream(dev)
+            side.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(side):
+                for _ in range(2):
+                    step()
+            torch.cuda.current_stream(dev).wait_stream(side)
+            barrier()
+            graph = torch.cuda.CUDAGraph()
+            c0 = lib.fi_launch_count()
+            with torch.cuda.graph(graph):
+                step()
+            graph_launches = int(lib.fi_launch_count() - c0)
+            for _ in range(2):
+                graph.replay()
+            barrier()
+            mode = "cuda-graph replay"
+        except Exception as e:  # noqa: BLE001  (reported in the JSON line)
+            graph = None
+            mode = f"eager (graph capture failed: {type(e).__name__}: {str(e)[:120]})"
+            torch.cuda.synchronize(dev)
+            barrier()
+    launch0 = lib.fi_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record()
+    for _ in range(steps):
+        if graph is not None:
+            graph.replay()
+        else:
+            step()
+    e1.record()
+    barrier()
+    ms = e0.elapsed_time(e1) / steps
+    launches = graph_launches * steps if graph is not None else int(lib.fi_launch_count() - launch0)
+    if graph is not None:
+        del graph
+        torch.cuda.synchronize(dev)
+        torch.cuda.empty_cache()
+    return ms, launches, mode
+
+
 def run_ours(args, world, rank, local):
     import torch
     import torch.distributed as dist
     from paper_2310_14997_b200 import _lib
+    from paper_2310_14997_b200.dp import DataParallelInside
     from paper_2310_14997_b200.grammar import GrammarDims, random_grammar
-    from paper_2310_14997_b200.ops import check_lengths, inside
+    from paper_2310_14997_b200.ops import check_lengths
 
-    dev = init_dist(world, local)
+    dev, backend = init_dist(world, local)
     cfg = CONFIGS[args.config]
     n, length = cfg["n"], args.length or cfg["length"]
-    batch = args.batch or cfg["batch"]
-    if args.scaling == "strong":
-        if batch % world:
-            raise SystemExit(f"strong scaling needs batch % gpus == 0 ({batch} % {world})")
-        batch //= world
+    batch_cfg = args.batch or cfg["batch"]
 
+    def per_gpu(scaling):
+        if scaling == "strong":
+            if batch_cfg % world:
+                raise SystemExit(f"strong scaling needs batch % gpus == 0 ({batch_cfg} % {world})")
+            return batch_cfg // world
+        return batch_cfg
+
+    batch = per_gpu(args.scaling)
     g = random_grammar(GrammarDims(n, n, VOCAB), seed=0)
-    rng = np.random.default_rng(1 + rank)
-    tokens = rng.integers(0, VOCAB, size=(batch, length))
     L = torch.tensor(g.log_left, dtype=torch.float32, device=dev)
     R = torch.tensor(g.log_right, dtype=torch.float32, device=dev)
     root = torch.tensor(g.log_root, dtype=torch.float32, device=dev)
     emit = torch.tensor(g.log_emit, dtype=torch.float32, device=dev)
-    tok_d = torch.as_tensor(tokens, device=dev)
-    unary = emit.t()[tok_d].contiguous()
-    lengths = torch.full((batch,), length, dtype=torch.int32, device=dev)
-    for t in (L, R, root, unary):
-        t.requires_grad_(True)
-    check_lengths(lengths, length)  # once: the timed steps skip the host read
     lib = _lib.load()
     chart_fmt = int(_lib.chart_layout(_lib.shape(n, n, batch, length, args.gemm_dtype, False,
                                                  args.chart_dtype)).chart_fmt)
-
-    def allreduce(dL, dR, droot):
-        """The step's single exchange: sum the grammar gradients over ranks,
-        in place (three back-to-back NCCL calls, no packing copies)."""
-        if world == 1:
-            return
-        works = [dist.all_reduce(t, async_op=True) for t in (dL, dR, droot)]
-        for wk in works:
-            wk.wait()
-
-    def step(Li, Ri, rooti, unaryi):
-        log_z = inside(Li, Ri, rooti, unaryi, lengths, gemm_dtype=args.gemm_dtype,
-                       chart_dtype=args.chart_dtype, validate=False)  # checked once below
-        loss = -log_z.mean()                          # train.py:218: d loss = -1/B
-        dL, dR, droot, dun = torch.autograd.grad(loss, [Li, Ri, rooti, unaryi])
-        allreduce(dL, dR, droot)
-        return log_z, loss, dL, dR, droot, dun
+    use_graph = args.graph != 0 and backend != "gloo"
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
+    def make(bsz):
+        """This rank's shard: tokens default_rng(1 + rank), lengths, the
+        data-parallel engine and the step closure (the loss is the global
+        mean NLL: grad_log_z = -1 / global batch, train.py:218)."""
+        tokens = np.random.default_rng(1 + rank).integers(0, VOCAB, size=(bsz, length))
+        tok_d = torch.as_tensor(tokens, device=dev)
+        unary = emit.t()[tok_d].contiguous()
+        lengths = torch.full((bsz,), length, dtype=torch.int32, device=dev)
+        check_lengths(lengths, length)  # once: the timed steps skip the host read
+        gvec = torch.full((bsz,), -1.0 / (bsz * world), device=dev)
+        dpi = DataParallelInside(n, n, bsz, length, args.gemm_dtype, args.chart_dtype, dev,
+                                 slots=2)
+        return tokens, unary, lengths, gvec, dpi
+
+    tokens, unary, lengths, gvec, dpi = make(batch)
+
+    def step():
+        return dpi.step(L, R, root, unary, lengths, gvec)
+
     # ---- device-resident timed region (the clock sampler runs from the
     # warm-up on; only its samples inside the timed region count)
     clocks = ClockSampler(local)
     clocks.start()
-    for _ in range(args.warmup):
-        step(L, R, root, unary)
-    barrier()
-    graph, graph_launches = None, 0
-    use_graph = args.graph == 1 or (args.graph < 0 and world == 1)
-    if use_graph and (world == 1 or os.environ.get("FI_DIST_BACKEND", "nccl") == "nccl"):
-        # one fwd+bwd(+all-reduce) step captured as a CUDA graph and replayed:
-        # the ~160 dependent launches of a step become one graph launch
-        side = torch.cuda.Stream(dev)
-        side.wait_stream(torch.cuda.current_stream(dev))
-        with torch.cuda.stream(side):
-            for _ in range(2):
-                step(L, R, root, unary)
-        torch.cuda.current_stream(dev).wait_stream(side)
-        graph = torch.cuda.CUDAGraph()
-        c0 = lib.fi_launch_count()
-        with torch.cuda.graph(graph):
-            g_out = step(L, R, root, unary)
-        graph_launches = int(lib.fi_launch_count() - c0)
-        for _ in range(2):
-            graph.replay()
-        barrier()
-    launch0 = lib.fi_launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
     clocks.mark()
-    e0.record()
-    for _ in range(args.steps):
-        if graph is not None:
-            graph.replay()
-        else:
-            _, loss, *_ = step(L, R, root, unary)
-    e1.record()
-    barrier()
+    ms, gpu_launches, launch_mode = timed_steps(step, args.steps, args.warmup, use_graph, barrier,
+                                                lib, dev)
     clk = clocks.stop()
-    ms = e0.elapsed_time(e1) / args.steps
-    if graph is not None:
-        loss = g_out[1]
-        gpu_launches = graph_launches * args.steps
-    else:
-        gpu_launches = int(lib.fi_launch_count() - launch0)
-    loss_val = float(loss.item())
+    log_z = dpi.log_z
+    loss_val = float(-(log_z.sum()) / batch)
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -447,30 +497,42 @@ def run_ours(args, world, rank, local):
     _lib.profile_enable(True)
     barrier()
     for _ in range(args.steps):
-        step(L, R, root, unary)
+        step()
     barrier()
     _lib.profile_enable(False)
     prof = _lib.profile_collect()
     value = world * batch / (ms / 1e3)
 
-    # the captured graph's private memory pool is released before the eager
-    # end-to-end loop (holding it measured 3x slower eager steps)
-    launch_mode = "cuda-graph replay" if graph is not None else "eager"
-    if graph is not None:
-        del graph, g_out
-        graph = None
-        torch.cuda.synchronize(dev)
+    # ---- the other scaling mode at N > 1 (weak: B per GPU; strong: B global)
+    other = None
+    if world > 1 and not args.no_other_scaling:
+        mode2 = "strong" if args.scaling == "weak" else "weak"
+        b2 = per_gpu(mode2)
+        del dpi
         torch.cuda.empty_cache()
+        _, unary2, lengths2, gvec2, dpi2 = make(b2)
+        ms2, _, lm2 = timed_steps(lambda: dpi2.step(L, R, root, unary2, lengths2, gvec2),
+                                  args.steps, args.warmup, use_graph, barrier, lib, dev)
+        t = torch.tensor([ms2], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms2 = float(t.item())
+        other = {"scaling": mode2, "batch_per_gpu": b2, "global_batch": b2 * world,
+                 "ms_per_step": ms2, "value": world * b2 / (ms2 / 1e3), "unit": "sentences/s",
+                 "launch": lm2}
+        del dpi2
+        torch.cuda.empty_cache()
+        tokens, unary, lengths, gvec, dpi = make(batch)
 
     # ---- end-to-end through host buffers (reference-facing call pattern)
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, g, tokens, step, dev, batch, n, world, barrier)
+        e2e = run_e2e(args, g, tokens, dpi, lengths, gvec, dev, batch, n, world, barrier)
 
     # ---- roofline of the dominant kernel class
     esz = 4 if args.gemm_dtype == "tf32" else 2
     chart_esz = 2 if chart_fmt == _lib.FI_CHART_F16 else 4
-    roofline = roofline_block(prof, args.steps, n, batch, length, esz, chart_esz)
+    roofline = roofline_block(prof, args.steps, n, batch, length, esz, chart_esz,
+                              args.gemm_dtype)
 
     # ---- CPU baseline (oracle port) on rank 0, N = 1 only
     cpu = None
@@ -494,9 +556,12 @@ def run_ours(args, world, rank, local):
                        "n_nt": n, "n_pt": n, "length": length, "batch_per_gpu": batch,
                        "global_batch": batch * world, "gemm_dtype": args.gemm_dtype,
                        "chart_dtype": "fp16" if chart_esz == 2 else "fp32",
-                       "launch": launch_mode,
+                       "launch": launch_mode, "dist_backend": backend if world > 1 else None,
                        "parallelism": f"dp{world}",
+                       "collective": ("one flat [dL|dR|droot] bucket, all-reduced in 2 chunks "
+                                      "(dL overlapping dR's wgrad GEMM)") if world > 1 else None,
                        "l2": "working set ~4 GB chart per step >> 126 MB L2 (no flush needed)"},
+            "scaling_other": other,
             "clocks": clk,
             "e2e": e2e,
             "gpu_launches": gpu_launches,
@@ -523,7 +588,7 @@ def run_train(args, world, rank, local):
     from paper_2310_14997_b200 import _lib, neural
     from paper_2310_14997_b200.grammar import GrammarDims
 
-    dev = init_dist(world, local)
+    dev, _ = init_dist(world, local)
     cfg = CONFIGS[args.config]
     n, length = cfg["n"], args.length or cfg["length"]
     batch = args.batch or cfg["batch"]
@@ -660,6 +725,22 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def relaunch(nproc: int, argv: list) -> int:
+    """Run this script under torch.distributed.run with `nproc` ranks on this
+    node (rendezvous on 127.0.0.1); rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve()), *argv]
+    rc = subprocess.call(cmd)
+    if rc:
+        sys.exit(rc)
+    return 0
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser(description=__doc__)
     ap.add_argument("--gpus", type=int, default=1)
@@ -680,12 +761,17 @@ def main(argv=None):
                     help="1: time CUDA-graph replays of the captured step; 0: eager launches; "
                          "-1 (default): graphs on one GPU, eager under torchrun")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-other-scaling", action="store_true",
+                    help="N > 1: skip the second measurement in the other scaling mode")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # not launched by torchrun: launch N ranks of this same command
+        return relaunch(args.gpus, sys.argv[1:] if argv is None else list(argv))
     world, rank, local = dist_env()
-    if world != args.gpus and not (world == 1 and args.gpus == 1):
+    if world != args.gpus:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args, world, rank)

@@ -128,6 +128,18 @@ int fi_inside_backward(const fi_shape* shape, const float* L, const float* R, co
                        const float* grad_log_z, float* dL, float* dR, float* droot,
                        float* dunary, void* ws, void* stream);
 
+/* fi_inside_backward for the data-parallel step (the sum of
+ * per-sentence GrammarGrads across ranks replaces train.py:206-218's loop):
+ * the weight-gradient GEMMs run as [width-1 block of dL and dR] -> [dL's
+ * width >= 2 block] -> record `dl_ready` (a cudaEvent_t, may be NULL) on
+ * `stream` -> [dR's width >= 2 block], so a caller can all-reduce dL on
+ * another stream while dR's GEMM still runs.  droot is final before it too.
+ * With dl_ready == NULL this is exactly fi_inside_backward. */
+int fi_inside_backward_ex(const fi_shape* shape, const float* L, const float* R,
+                          const float* root, const float* unary, const int32_t* lengths,
+                          const float* log_z, const float* grad_log_z, float* dL, float* dR,
+                          float* droot, float* dunary, void* ws, void* stream, void* dl_ready);
+
 /* Span marginals mu_sym (MarginalTable, inside.py:425-430) for widths >= 2,
  * rows ordered like the chart from rowbase(2); shape (rows - rowbase(2), N).
  * Requires store_chart = 1 and a completed backward with the same grad_log_z. */

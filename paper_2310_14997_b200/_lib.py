@@ -72,6 +72,9 @@ SIGNATURES = [
     ("fi_inside_backward", c_int32,
      [POINTER(FiShape), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
       c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("fi_inside_backward_ex", c_int32,
+     [POINTER(FiShape), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+      c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("fi_marginals", c_int32,
      [POINTER(FiShape), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("fi_span_marginals", c_int32,

@@ -972,7 +972,8 @@ int forward_impl(const Plan& p, const float* L, const float* R, const float* roo
 template <typename T, typename CT>
 int backward_impl(const Plan& p, const float* L, const float* R, const float* root,
                   const float* unary, const int* lengths, const float* logZ, const float* g,
-                  float* dL, float* dR, float* droot, float* dunary, void* ws, cudaStream_t st) {
+                  float* dL, float* dR, float* droot, float* dunary, void* ws, cudaStream_t st,
+                  cudaEvent_t dl_ready = nullptr) {
   T* wnn = at<T>(ws, p.wnn);
   T* wnp = at<T>(ws, p.wnp);
   T* eall = at<T>(ws, p.eall);
@@ -1123,27 +1124,50 @@ int backward_impl(const Plan& p, const float* L, const float* R, const float* ro
   ep.Np = p.Np;
   ep.M = 2 * p.Np;
   const long long r2 = rowbase(2, p.B, p.l), rl = rowbase(p.l, p.B, p.l);
-  if (rl > r2) {
-    const Operand opG{gall + r2 * 2 * p.Np, 2LL * p.Np, rl - r2, 2LL * p.Np, true, p.gall_lo};
-    const Operand opE{eall + r2 * p.Np, p.Np, rl - r2, p.Np, true, p.eall_lo};
-    ep.col_off = 0;
-    ep.valid_cols = p.N;
-    FI_TRY((run_gemm<T, true, true, EPI_WGRAD>(opG, opE, 2 * p.Np, p.Np,
-                                                static_cast<int>(rl - r2), 0, ep, st)));
-  } else {  // l == 2: no width >= 2 span is ever projected
-    for (int r = 0; r < p.N; ++r) {
-      FI_CUDA(cudaMemsetAsync(dL + static_cast<long long>(r) * (p.N + p.P), 0, 4ull * p.N, st));
-      FI_CUDA(cudaMemsetAsync(dR + static_cast<long long>(r) * (p.N + p.P), 0, 4ull * p.N, st));
+  // NN block (widths >= 2) over output rows [m0, m0 + m): m = 2Np both tables
+  // in one GEMM; with dl_ready, dL's rows then dR's rows as two launches
+  auto wgrad_nn = [&](int m0, int m) -> int {
+    if (rl > r2) {
+      const Operand opG{gall + r2 * 2 * p.Np + m0, static_cast<long long>(m), rl - r2,
+                        2LL * p.Np, true, p.gall_lo};
+      const Operand opE{eall + r2 * p.Np, p.Np, rl - r2, p.Np, true, p.eall_lo};
+      ep.col_off = 0;
+      ep.valid_cols = p.N;
+      ep.M = m;
+      ep.m_off = m0;
+      FI_TRY((run_gemm<T, true, true, EPI_WGRAD>(opG, opE, m, p.Np, static_cast<int>(rl - r2), 0,
+                                                  ep, st)));
+    } else {  // l == 2: no width >= 2 span is ever projected
+      for (int r = 0; r < p.N; ++r) {
+        if (m0 < p.Np)
+          FI_CUDA(cudaMemsetAsync(dL + static_cast<long long>(r) * (p.N + p.P), 0, 4ull * p.N, st));
+        if (m0 + m > p.Np)
+          FI_CUDA(cudaMemsetAsync(dR + static_cast<long long>(r) * (p.N + p.P), 0, 4ull * p.N, st));
+      }
     }
-  }
-  {
+    return FI_OK;
+  };
+  // NP block (width 1), both tables
+  auto wgrad_np = [&]() -> int {
     const Operand opG{gall, 2LL * p.Np, static_cast<long long>(p.B) * p.l, 2LL * p.Np, true,
                       p.gall_lo};
     const Operand opE{e1, p.Pp, static_cast<long long>(p.B) * p.l, p.Pp, true, p.e1_lo};
     ep.col_off = p.N;
     ep.valid_cols = p.P;
+    ep.M = 2 * p.Np;
+    ep.m_off = 0;
     FI_TRY((run_gemm<T, true, true, EPI_WGRAD>(opG, opE, 2 * p.Np, p.Pp, p.B * p.l, 0, ep, st)));
+    return FI_OK;
+  };
+  if (!dl_ready) {
+    FI_TRY(wgrad_nn(0, 2 * p.Np));
+    FI_TRY(wgrad_np());
+    return FI_OK;
   }
+  FI_TRY(wgrad_np());
+  FI_TRY(wgrad_nn(0, p.Np));
+  FI_CUDA(cudaEventRecord(dl_ready, st));  // dL (both blocks) is final from here
+  FI_TRY(wgrad_nn(p.Np, p.Np));
   return FI_OK;
 }
 
@@ -1199,6 +1223,14 @@ int fi_inside_backward(const fi_shape* shape, const float* L, const float* R, co
                        const float* unary, const int32_t* lengths, const float* log_z,
                        const float* grad_log_z, float* dL, float* dR, float* droot,
                        float* dunary, void* ws, void* stream) {
+  return fi_inside_backward_ex(shape, L, R, root, unary, lengths, log_z, grad_log_z, dL, dR,
+                               droot, dunary, ws, stream, nullptr);
+}
+
+int fi_inside_backward_ex(const fi_shape* shape, const float* L, const float* R,
+                          const float* root, const float* unary, const int32_t* lengths,
+                          const float* log_z, const float* grad_log_z, float* dL, float* dR,
+                          float* droot, float* dunary, void* ws, void* stream, void* dl_ready) {
   Plan p;
   FI_TRY(make_plan(shape, &p));
   FI_TRY(check_ptrs({L, R, root, unary, lengths, log_z, grad_log_z, dL, dR, droot, dunary, ws}));
@@ -1208,7 +1240,7 @@ int fi_inside_backward(const fi_shape* shape, const float* L, const float* R, co
   FI_TRY(kps.err);
 #define FI_BWD(T, CT)                                                                      \
   return backward_impl<T, CT>(p, L, R, root, unary, lengths, log_z, grad_log_z, dL, dR, droot, \
-                              dunary, ws, st)
+                              dunary, ws, st, static_cast<cudaEvent_t>(dl_ready))
   if (p.tf32) {
     if (p.half_chart) FI_BWD(float, __half);
     FI_BWD(float, float);

@@ -101,6 +101,8 @@ struct GemmEpi {
   int ld_lr;          // row stride of L/R/dL/dR (= N + P)
   int col_off;        // 0 for the NN block, N for the NP block
   int valid_cols;     // N or P
+  int m_off;          // output row of this launch's row 0 (0..2Np: a launch may cover
+                      // only the dR half, so dL can be all-reduced while it runs)
   // EPI_STORE
   float* C;
   int ldc;
@@ -282,8 +284,9 @@ __device__ __forceinline__ EpiRow epi_row(const GemmEpi& ep, int lrow) {
       r.aux = i < ep.lengths[b];
       r.rowptr = ep.dunary + grow * ep.P;
     } else if constexpr (EPI == EPI_WGRAD) {
-      r.aux = lrow >= ep.Np;  // 0 -> left table, 1 -> right table
-      const int arow = r.aux ? lrow - ep.Np : lrow;
+      const int mrow = lrow + ep.m_off;
+      r.aux = mrow >= ep.Np;  // 0 -> left table, 1 -> right table
+      const int arow = r.aux ? mrow - ep.Np : mrow;
       r.rowptr = (r.aux ? ep.dR : ep.dL) + static_cast<long long>(arow) * ep.ld_lr;
       if (arow >= ep.n_nt) r.rowptr = nullptr;
     } else {
@@ -298,7 +301,7 @@ __device__ __forceinline__ EpiRow epi_row(const GemmEpi& ep, int lrow) {
       if (i == 0 && ep.lengths[b] == ep.width) r.ok = false;
     }
   }
-  r.erow = (EPI == EPI_WGRAD && r.aux) ? lrow - ep.Np
+  r.erow = EPI == EPI_WGRAD ? (r.aux ? lrow + ep.m_off - ep.Np : lrow + ep.m_off)
            : EPI == EPI_DUNARY ? static_cast<int>(grow) : lrow;
   return r;
 }

@@ -43,3 +43,15 @@ def test_reference_arm_under_torchrun():
     d = _line(res.stdout)
     _check(d)
     assert d["n_gpus"] == 2
+
+
+def test_gpus_flag_without_torchrun_launches_the_ranks():
+    """`python bench.py --gpus 2` (no torchrun): bench relaunches itself under
+    torch.distributed.run; one JSON line, n_gpus 2."""
+    res = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "2",
+                          "--config", "1", "--steps", "1", "--warmup", "1"],
+                         cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stderr[-2000:]
+    d = _line(res.stdout)
+    _check(d)
+    assert d["n_gpus"] == 2

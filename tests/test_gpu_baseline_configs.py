@@ -152,7 +152,7 @@ def test_config4_lengths_log_z_against_reference(length):
     assert got["log_z"][0] == pytest.approx(float(GOLD[f"cfg_n4096_l{length}_logz0"]), rel=2e-3)
     want = O.inside_batch_equal(left, right, root, unary[[0, 63]], backward=False)["log_z"]
     np.testing.assert_allclose(got["log_z"][[0, 63]], want, rtol=2e-3)
-    assert got["droot"].sum() == pytest.approx(1.0, rel=2e-3)
+    assert got["droot"].sum() == pytest.approx(-1.0, rel=2e-3)   # sum of grad_log_z
 
 
 # ------------------------------------------------------------------ config 5
