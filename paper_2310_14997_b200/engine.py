@@ -42,15 +42,36 @@ class InsideError(Exception):
 
 
 class AllocMeter:
-    """Accounting hook kept for signature compatibility (inside.py:35-63).
+    """Arena-style allocation accounting (inside.py:35-63), same API.
 
-    The engine allocates one device workspace per call; it is reported as
-    retained bytes (the chart) with zero host transients."""
+    Host arrays go through :meth:`alloc` / :meth:`release` as in the
+    reference (the exported float64 chart is ``retained``).  The engine's
+    device memory is one caller-visible workspace per call (chart + the
+    state the backward recomputes from, fi_workspace_bytes): it is counted
+    in ``device_retained_bytes``; the engine allocates no device or host
+    transients of its own, so ``transient_bytes`` returns to 0 and
+    ``peak_transient_bytes`` stays 0 for an engine call."""
 
     def __init__(self):
         self.transient_bytes = 0
         self.peak_transient_bytes = 0
         self.retained_bytes = 0
+        self.device_retained_bytes = 0
+
+    def alloc(self, shape, dtype=np.float64, retained: bool = False) -> np.ndarray:
+        arr = np.empty(shape, dtype=dtype)
+        if retained:
+            self.retained_bytes += arr.nbytes
+        else:
+            self.transient_bytes += arr.nbytes
+            self.peak_transient_bytes = max(self.peak_transient_bytes, self.transient_bytes)
+        return arr
+
+    def release(self, arr: np.ndarray) -> None:
+        self.transient_bytes -= arr.nbytes
+
+    def device(self, nbytes: int) -> None:
+        self.device_retained_bytes += int(nbytes)
 
 
 @dataclass
@@ -141,7 +162,7 @@ def device_grammar(g) -> DeviceGrammar:
 
 
 def _chart_from_workspace(ws: torch.Tensor, shape, n_nt: int, length: int,
-                          unary_row: np.ndarray) -> InsideChart:
+                          unary_row: np.ndarray, meter: AllocMeter | None = None) -> InsideChart:
     """Copy one sentence's chart (batch row 0) to the reference layout.
 
     The engine stores base-2 offsets from an fp64 per-span shift x; the
@@ -152,6 +173,13 @@ def _chart_from_workspace(ws: torch.Tensor, shape, n_nt: int, length: int,
     n_sym = n_nt + unary_row.shape[1]
     ln2 = math.log(2.0)
     xs = ws[int(lay.off_x):int(lay.off_x) + 8 * int(lay.rows)].view(torch.float64).cpu().numpy()
+
+    meter = meter or AllocMeter()
+
+    def full(shape_):  # the exported chart arrays are retained (inside.py:52-60)
+        a = meter.alloc(shape_, retained=True)
+        a.fill(NEG_INF)
+        return a
 
     def rows(off, w, half=False):
         base = B * ((w - 1) * (l + 1) - (w - 1) * w // 2)
@@ -170,17 +198,19 @@ def _chart_from_workspace(ws: torch.Tensor, shape, n_nt: int, length: int,
     o = [None] * (length + 1)
     a = [None] * length
     b = [None] * length
-    o1 = np.full((length, n_sym), NEG_INF)
+    o1 = full((length, n_sym))
     o1[:, n_nt:] = unary_row[:length]          # exact float64 copy (inside.py:390)
     o[1] = o1
     for w in range(1, length + 1):
         if w >= 2:
-            ow = np.full((length - w + 1, n_sym), NEG_INF)
+            ow = full((length - w + 1, n_sym))
             ow[:, :n_nt] = rows(int(lay.off_o), w)
             o[w] = ow
         if w < length:
-            a[w] = rows(int(lay.off_a), w, half_ab)
-            b[w] = rows(int(lay.off_b), w, half_ab)
+            a[w] = full((length - w + 1, n_nt))
+            a[w][:] = rows(int(lay.off_a), w, half_ab)
+            b[w] = full((length - w + 1, n_nt))
+            b[w][:] = rows(int(lay.off_b), w, half_ab)
     return InsideChart(length, o, a, b, NEG_INF)
 
 
@@ -201,12 +231,12 @@ def inside_b200(g, tokens, meter: AllocMeter | None = None,
     n_nt = g.dims.n_nt
     shape = _lib.shape(n_nt, g.dims.n_pt, 1, l, gemm_dtype, True)
     unary_row = np.asarray(g.log_emit)[:, toks].T
-    chart = _chart_from_workspace(ws, shape, n_nt, l, unary_row)
+    chart = _chart_from_workspace(ws, shape, n_nt, l, unary_row, meter)
     chart.log_z = float(log_z.item())
     chart._device = dict(dg=dg, unary=unary, lengths=lengths, log_z=log_z, ws=ws,
                          shape=shape, gemm_dtype=gemm_dtype, tokens=toks)
     if meter is not None:
-        meter.retained_bytes += int(ws.numel())
+        meter.device(ws.numel())
     return chart
 
 

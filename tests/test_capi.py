@@ -114,3 +114,30 @@ def test_version_and_launch_counter():
     lib = _lib.load()
     assert lib.fi_version() >= 1
     assert lib.fi_launch_count() >= 0
+
+
+def test_workspace_grows_quadratically_in_length_and_linearly_in_batch():
+    """The GPU counterpart of the reference's allocation-shape contract
+    (tests/test_inside.py:174-187: the fused engine's memory grows ~l^2, not
+    l^3): the engine's only memory is fi_workspace_bytes."""
+    def ws(n, b, l):
+        return _lib.workspace_bytes(_lib.shape(n, n, b, l, "bf16", False))
+    for n in (64, 1024, 4096):
+        r = (ws(n, 8, 48) - ws(n, 8, 2)) / (ws(n, 8, 24) - ws(n, 8, 2))
+        assert r < 5.0, r                      # ~4 (l^2); cubic would be ~8
+        r_b = (ws(n, 32, 24) - ws(n, 1, 24)) / (ws(n, 16, 24) - ws(n, 1, 24))
+        assert 2.0 <= r_b < 2.1, r_b           # linear in the batch
+    # and far below the reference's unfused O(l^3 N) split stack at cfg3
+    l, n = 40, 4096
+    assert ws(n, 1, l) < 8 * n * (l * (l + 1) * (l + 2) // 6)
+
+
+def test_alloc_meter_api_matches_the_reference():
+    from paper_2310_14997_b200.engine import AllocMeter
+    m = AllocMeter()
+    a = m.alloc((10, 4))
+    b = m.alloc((3,), retained=True)
+    assert m.transient_bytes == 320 and m.peak_transient_bytes == 320
+    assert m.retained_bytes == b.nbytes == 24
+    m.release(a)
+    assert m.transient_bytes == 0 and m.peak_transient_bytes == 320

@@ -197,10 +197,11 @@ def test_peaked_dirichlet_grammars(conc, gemm_dtype, chart_dtype):
     check_all(got, want, 2e-3, f"peaked conc={conc} {gemm_dtype}/{chart_dtype}")
 
 
-def test_trained_grammar_fast_mode():
+@pytest.fixture(scope="module")
+def trained():
     """A grammar after 200 training steps on a skewed corpus (the neural
-    parameterisation, TrainStep in fp32 mode) is peaked the way real
-    grammars are; the bf16 + fp16-chart op must still match the oracle."""
+    parameterisation, TrainStep in fp32 mode): peaked the way real grammars
+    are (most rules far below 2^-28)."""
     from paper_2310_14997_b200 import neural
     from paper_2310_14997_b200.grammar import GrammarDims
     n, B, l = 512, 16, 20
@@ -215,12 +216,19 @@ def test_trained_grammar_fast_mode():
     with torch.no_grad():
         root, left, right, emit = (t.double().cpu().numpy() for t in ts.tables())
     frac_tiny = float((left < np.log(2.0 ** -28)).mean())
-    toks = base.cpu().numpy()
-    unary = O.unary_from_tokens(emit, toks)
+    unary = O.unary_from_tokens(emit, base.cpu().numpy())
     grad = np.full(B, -1.0 / B)
     want = O.inside_batch_equal(left, right, root, unary, grad)
     print(f"trained: loss {losses[0]:.2f} -> {losses[-1]:.2f}; "
           f"{frac_tiny:.0%} of the rules below 2^-28")
-    for gemm_dtype in ("bf16", "fp32"):
-        got = run_op(root, left, right, unary, np.full(B, l), grad, gemm_dtype)
-        check_all(got, want, RTOL[gemm_dtype], f"trained {gemm_dtype}")
+    return root, left, right, unary, grad, want, B, l
+
+
+@pytest.mark.parametrize("gemm_dtype,chart_dtype", [("bf16", "auto"), ("bf16", "fp32"),
+                                                    ("tf32", "auto"), ("fp32", "fp16"),
+                                                    ("fp32", "auto")])
+def test_trained_grammar(trained, gemm_dtype, chart_dtype):
+    root, left, right, unary, grad, want, B, l = trained
+    got = run_op(root, left, right, unary, np.full(B, l), grad, gemm_dtype, chart_dtype)
+    rtol = max(RTOL[gemm_dtype], 2e-3 if chart_dtype == "fp16" else 0.0)
+    check_all(got, want, rtol, f"trained {gemm_dtype}/{chart_dtype}")
