@@ -102,7 +102,7 @@ def test_corpus_f1_mbr_through_the_registry(ref):
         return [int(w[1:]) for w in words]
     fb = P.corpus_f1(g, bank, encode, decoder="mbr", engine="b200")
     ff = P.corpus_f1(g, bank, encode, decoder="mbr", engine="flash")
-    assert fb.mean == pytest.approx(ff.mean, abs=1e-12)
+    assert fb.mean_f1 == pytest.approx(ff.mean_f1, abs=1e-12)
     assert [r[:2] for r in fb.rows] == [r[:2] for r in ff.rows]
 
 
@@ -115,7 +115,7 @@ def test_reference_training_loop_on_the_b200_engine(ref, parameterization):
     runs = {}
     for eng in ("b200", "flash"):
         cfg = T.TrainConfig(parameterization=parameterization, n_nt=10, n_pt=8, d=16,
-                            max_epochs=2, batch_cap=4, eval_every=3, seed=0, engine=eng,
+                            max_epochs=2, batch_cap=16, eval_every=3, seed=0, engine=eng,
                             vocab_size=12, lr=0.01)
         runs[eng] = T.train(cfg, mk(train_s), mk(dev_s))
     lb = np.array([l for _, l in runs["b200"].log.steps])
