@@ -62,6 +62,32 @@ def main():
         gold[pre + "vit_logp"] = np.array(tree_log_prob(g, toks, vit))
         gold[pre + "f1_mbr_vs_vit"] = np.array(sentence_f1(mbr.spans, vit.spans, l))
         cases.append(k)
+    # realistic sizes (|N| = 256 .. 1024): the decoders at the op's scale
+    big = [(256, 256, 64, 20, 1.0), (256, 256, 64, 24, 0.3), (512, 512, 64, 16, 1.0),
+           (1024, 1024, 64, 12, 1.0), (1024, 1024, 64, 10, 0.3)]
+    for j, (n_nt, n_pt, V, l, conc) in enumerate(big):
+        k = len(cases)
+        gseed = 1000 + j
+        g = random_grammar(GrammarDims(n_nt, n_pt, V), seed=gseed, concentration=conc)
+        toks = np.random.default_rng(gseed + 1).integers(0, V, size=l)
+        chart = inside_flash(g, toks)
+        _, marg = inside_backward(g, toks, chart)
+        mbr = mbr_decode(marg)
+        vit = viterbi_decode(g, toks)
+        pre = f"c{k}_"
+        gold[pre + "meta"] = np.array([n_nt, n_pt, V, gseed, l])
+        gold[pre + "conc"] = np.array(conc)
+        gold[pre + "tokens"] = toks
+        mu = np.zeros((l + 1, l + 1))
+        for w in range(2, l + 1):
+            for i in range(l - w + 1):
+                mu[i, i + w] = marg.span(i, i + w)
+        gold[pre + "mu"] = mu
+        gold[pre + "mbr"] = spans_arr(mbr.spans)
+        gold[pre + "vit"] = spans_arr(vit.spans)
+        gold[pre + "vit_logp"] = np.array(tree_log_prob(g, toks, vit))
+        gold[pre + "f1_mbr_vs_vit"] = np.array(sentence_f1(mbr.spans, vit.spans, l))
+        cases.append(k)
     gold["n_cases"] = np.array(len(cases))
     np.savez_compressed(OUT, **gold)
     print(f"wrote {OUT} ({len(cases)} cases)")
