@@ -404,13 +404,44 @@ thread_local int g_gemm_stages = 0;
 constexpr int kGemmSmemMax = 227 * 1024;  // opt-in dynamic shared memory per CTA
 constexpr int kGemmStagesMax = 12;        // barrier block (256 B) holds 2 x 12 + 4 mbarriers
 
-template <typename T, int BN, bool AMN, bool BMN, int EPI, bool SPLIT, int CHUNK, bool PAIR>
+// Co-resident clusters of `cl` CTAs of `kern` (one per SM-group), cached per
+// kernel and device: the persistent grid of a multicast-cluster GEMM.
+template <typename K>
+int max_clusters(K kern, int cl, int threads, size_t smem) {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (cache[dev & 63]) return cache[dev & 63];
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cl * 64);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = cl;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    n = num_sms() / cl;
+  }
+  cache[dev & 63] = n;
+  return n;
+}
+
+template <typename T, int BN, bool AMN, bool BMN, int EPI, bool SPLIT, int CHUNK, bool PAIR,
+          bool MC = false>
 int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_row0,
                 const GemmEpi& ep, cudaStream_t st, int bn, int ksplit, int tail) {
   using Cf = GemmCfg<T, BN>;
   constexpr int NCTA = PAIR ? 2 : 1;
+  constexpr int CL = MC ? 4 : NCTA;
   CUtensorMap ta, tb, ta2, tb2;
-  const int abi = AMN ? Cf::ATOM : Cf::BK, abo = AMN ? Cf::BK : Cf::BM;
+  // MC: each CTA loads (and multicasts) half of its 128 A rows
+  const int abi = AMN ? Cf::ATOM : Cf::BK, abo = AMN ? Cf::BK : (MC ? Cf::BM / 2 : Cf::BM);
   const int bbi = BMN ? Cf::ATOM : Cf::BK, bbo = BMN ? Cf::BK : bn / NCTA;
   FI_TRY(encode<T>(&ta, A, abi, abo));
   FI_TRY(encode<T>(&tb, B, bbi, bbo));
@@ -444,7 +475,8 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
   sh.num_m = (M + Cf::BM * NCTA - 1) / (Cf::BM * NCTA);
   sh.num_n = (N + bn - 1) / bn;
   sh.num_k = (K + Cf::BK - 1) / Cf::BK;
-  const int tiles = sh.num_m * sh.num_n;
+  const int tiles = sh.num_m * (MC ? (sh.num_n + 1) / 2 : sh.num_n);  // MC: cluster tiles
+  if (MC) ksplit = 1;  // split-K partials are indexed per pair tile
   sh.ksplit = 1;
   sh.part = nullptr;
   sh.sem = nullptr;
@@ -466,7 +498,7 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
   } else {
     tail = 0;  // no split-K available: whole tiles only
   }
-  auto kern = k_gemm<T, BN, AMN, BMN, EPI, SPLIT, CHUNK, PAIR>;
+  auto kern = k_gemm<T, BN, AMN, BMN, EPI, SPLIT, CHUNK, PAIR, MC>;
   static bool attr_done[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -475,16 +507,18 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
                                  kGemmSmemMax));
     attr_done[dev & 63] = true;
   }
-  const int slots = num_sms() / NCTA;  // persistent: one CTA (pair) per SM (pair)
+  // persistent: one CTA (pair, cluster) per SM (pair, group of 4 SMs)
+  const int slots = MC ? max_clusters(kern, CL, gemm_threads<CHUNK>(), smem_bytes)
+                       : num_sms() / NCTA;
   ProfScope prof(EPI == EPI_FWD || EPI == EPI_FWD_H ? FI_PROF_GEMM_FWD
                  : EPI == EPI_WGRAD ? FI_PROF_GEMM_WGRAD
                  : EPI == EPI_STORE ? FI_PROF_PREP : FI_PROF_GEMM_DGRAD, st);  // DGRAD(_H), DUNARY
   auto go = [&](const GemmShape& g) -> int {
     const int units = ((g.tile_end > 0 ? g.tile_end : tiles) - g.tile_begin) * g.ksplit;
-    const int grid = (units < slots ? units : slots) * NCTA;
+    const int grid = (units < slots ? units : slots) * CL;
     if (grid <= 0) return FI_OK;
     if constexpr (PAIR) {
-      FI_TRY(launch_cluster(kern, 2, dim3(grid), dim3(gemm_threads<CHUNK>()), smem_bytes, st, ta,
+      FI_TRY(launch_cluster(kern, CL, dim3(grid), dim3(gemm_threads<CHUNK>()), smem_bytes, st, ta,
                             tb, ta2, tb2, g, ep));
     } else {
       FI_TRY(launch_ex(kern, 1, dim3(grid), dim3(gemm_threads<CHUNK>()), smem_bytes, st, ta, tb,
@@ -656,6 +690,14 @@ int run_gemm_s(const Operand& A, const Operand& B, int M, int N, int K, int a_ro
     fprintf(stderr, "[fi gemm] EPI=%d M=%d N=%d K=%d -> bn=%d pair=%d ksplit=%d tail=%d\n", EPI, M,
             N, K, c.bn, static_cast<int>(c.pair), c.ksplit, c.tail);
   if (c.bn == 0) return set_err(FI_ERR_ARG, "no GEMM tile for N=%d (FI_GEMM_BN?)", N);
+  // FI_GEMM_MC=1: pair tiles of N <= 256 run as multicast clusters of two
+  // pairs (A rows shared, adjacent N tiles; see k_gemm) when eligible
+  static const int use_mc = env_int("FI_GEMM_MC", 0);
+  if constexpr (!AMN && !SPLIT && kChunk == 0) {
+    if (use_mc && c.pair && c.bn <= kBnSingle && c.ksplit == 1 && c.tail == 0)
+      return launch_gemm<T, kBnSingle, AMN, BMN, EPI, SPLIT, kChunk, true, true>(
+          A, B, M, N, K, a_row0, ep, st, c.bn, 1, 0);
+  }
   if (c.pair) {
     if (c.bn > kBnSingle)  // 256 x 512-class pair tiles: two MMAs per K step
       return launch_gemm<T, kBnMax, AMN, BMN, EPI, SPLIT, kChunk, true>(A, B, M, N, K, a_row0, ep,

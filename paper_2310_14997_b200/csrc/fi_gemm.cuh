@@ -345,13 +345,25 @@ constexpr int gemm_epi_warps() { return 4; }
 template <int CHUNK>
 constexpr int gemm_threads() { return 128 + 32 * gemm_epi_warps<CHUNK>(); }
 
-template <typename T, int BN, bool A_MN, bool B_MN, int EPI, bool SPLIT, int CHUNK, bool PAIR>
+// MC (multicast clusters): a cluster of FOUR CTAs = two CTA pairs that work
+// on the same 256 A rows and adjacent N tiles (a 256 x 2bn cluster tile).
+// Each CTA loads only half of its 128 A rows and multicasts them to the CTA
+// at the same pair position in the other pair, so a CTA fetches 8 KB of A +
+// bn/2 rows of B per K step (24 KB at bn = 256) -- the bytes per MMA of a
+// 256 x 512 pair tile -- while keeping the double-buffered 2 x 256 TMEM
+// accumulator (epilogue overlapped with the next tile) and 256-column N
+// granularity.  A stage is released only when both pairs' MMAs consumed it.
+template <typename T, int BN, bool A_MN, bool B_MN, int EPI, bool SPLIT, int CHUNK, bool PAIR,
+          bool MC = false>
 __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
            GemmShape sh, GemmEpi ep) {
   using C = GemmCfg<T, BN>;
   constexpr int NCTA = PAIR ? 2 : 1;
+  constexpr int CL = MC ? 4 : NCTA;  // CTAs per cluster
+  static_assert(!MC || (PAIR && !A_MN && !SPLIT && CHUNK == 0 && BN <= 256),
+                "multicast clusters: bf16/tf32 K-major A, double-buffered pair tiles");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -371,7 +383,8 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int num_tiles = sh.num_m * sh.num_n;
+  // MC: a unit's tile index counts cluster tiles (M block, pair of N tiles)
+  const int num_tiles = sh.num_m * (MC ? (sh.num_n + 1) / 2 : sh.num_n);
   const int k_iters = sh.num_k;
   const int ks = sh.ksplit > 1 ? sh.ksplit : 1;
   const int tb = sh.tile_begin;
@@ -380,9 +393,16 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
   const int bn = sh.bn;                       // runtime N tile <= BN
   const int bn_cta = bn / NCTA;               // B rows staged by this CTA
   const int nbuf = SPLIT || bn <= C::TMEM_HALF ? 2 : 1;  // accumulator buffers in TMEM
-  const uint32_t rank = PAIR ? cluster_rank() : 0;
-  const int tile0 = PAIR ? blockIdx.x / 2 : blockIdx.x;
-  const int tstep = PAIR ? gridDim.x / 2 : gridDim.x;
+  const uint32_t crank = PAIR ? cluster_rank() : 0;
+  const uint32_t rank = crank & 1u;               // position in the CTA pair
+  const uint32_t pidx = MC ? (crank >> 1) : 0u;   // which pair of the cluster
+  const uint32_t lead = crank & ~1u;              // cluster rank of this pair's leader
+  const int tile0 = blockIdx.x / CL;
+  const int tstep = gridDim.x / CL;
+  auto tile_mn = [&](int tile, int& m_blk, int& n_blk) {
+    m_blk = tile % sh.num_m;
+    n_blk = MC ? 2 * (tile / sh.num_m) + static_cast<int>(pidx) : tile / sh.num_m;
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -393,7 +413,7 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
     }
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC ? 2 : 1);  // MC: both pairs' MMAs read this stage's A
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -423,8 +443,8 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
         const int tu = u / ks, kpart = u - tu * ks;
         const int tile = tb + tu;
         const int k0 = k_iters * kpart / ks, k1 = k_iters * (kpart + 1) / ks;
-        const int m_blk = tile % sh.num_m;
-        const int n_blk = tile / sh.num_m;
+        int m_blk, n_blk;
+        tile_mn(tile, m_blk, n_blk);
         const int m0 = m_blk * (C::BM * NCTA) + rank * C::BM;  // this CTA's A rows
         const int n0 = n_blk * bn + rank * bn_cta;              // this CTA's B rows
         for (int it = k0; it < k1; ++it) {
@@ -435,7 +455,7 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
           // completion is counted on the leader's full barrier (both CTAs' bytes)
           uint32_t fb = smem_u32(&full[stage]);
           if constexpr (PAIR) {
-            fb = mapa_rank(&full[stage], 0);
+            fb = mapa_rank(&full[stage], lead);
             if (rank == 0) mbar_expect_tx(&full[stage], stage_tx);
           } else {
             mbar_expect_tx(&full[stage], stage_tx);
@@ -461,7 +481,15 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
                 load(dst + j * C::BK * 128, mb, n0 + j * C::ATOM, kb * C::BK);
             }
           };
-          load_a(a_dst, &tmA);
+          if constexpr (MC) {  // this CTA's half of the A rows, to both pairs
+            constexpr int kHalfRows = C::BM / 2;
+            const uint16_t mask = static_cast<uint16_t>((1u << rank) | (1u << (2 + rank)));
+            tma_load_2d_pair_mc(a_dst + pidx * kHalfRows * 128, &tmA,
+                                pair_leader_addr(&full[stage]), mask, kb * C::BK,
+                                sh.a_row0 + m0 + static_cast<int>(pidx) * kHalfRows);
+          } else {
+            load_a(a_dst, &tmA);
+          }
           load_b(b_dst, &tmB);
           if constexpr (SPLIT) {  // the lo planes behind the hi tiles
             load_a(a_dst + C::A_BYTES, &tmA2);
@@ -543,14 +571,16 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
                   make_sdesc(b_base + sub_b_off + k * b_kstep, b_lbo, b_sbo, b_lay), idesc1, accum);
             }
           }
-          if constexpr (PAIR) umma_commit2(&empty[stage]);
+          if constexpr (MC) umma_commit2_mask(&empty[stage], 0xF);  // both pairs' stages
+          else if constexpr (PAIR) umma_commit2(&empty[stage]);
           else umma_commit(&empty[stage]);
           if (++stage == NS) {
             stage = 0;
             phase ^= 1;
           }
           if (kc == cl - 1 || kb == k1 - 1) {
-            if constexpr (PAIR) umma_commit2(&tfull[acc]);
+            if constexpr (MC) umma_commit2_mask(&tfull[acc], static_cast<uint16_t>(3u << lead));
+            else if constexpr (PAIR) umma_commit2(&tfull[acc]);
             else umma_commit(&tfull[acc]);
             if (++acc == nbuf) {
               acc = 0;
@@ -569,8 +599,8 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
     uint32_t acc_phase = 0;
     // TMEM-empty arrivals go to the leader (its MMA issuer reuses the buffer)
     uint32_t te[2];
-    te[0] = PAIR ? mapa_rank(&tempty[0], 0) : smem_u32(&tempty[0]);
-    te[1] = PAIR ? mapa_rank(&tempty[1], 0) : smem_u32(&tempty[1]);
+    te[0] = PAIR ? mapa_rank(&tempty[0], lead) : smem_u32(&tempty[0]);
+    te[1] = PAIR ? mapa_rank(&tempty[1], lead) : smem_u32(&tempty[1]);
     auto release = [&](int a) {
       tc_fence_before();
       __syncwarp();
@@ -583,8 +613,8 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
       const int tu = u / ks, kpart = u - tu * ks;
       const int tile = tb + tu;
       const int k0 = k_iters * kpart / ks, k1 = k_iters * (kpart + 1) / ks;
-      const int m_blk = tile % sh.num_m;
-      const int n_blk = tile / sh.num_m;
+      int m_blk, n_blk;
+      tile_mn(tile, m_blk, n_blk);
       const int lrow = m_blk * (C::BM * NCTA) + rank * C::BM + r;  // row within this GEMM
       const EpiRow er = epi_row<EPI>(ep, lrow);
       const int col_base = n_blk * bn;

@@ -213,6 +213,23 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
       "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1)
       : "memory");
 }
+// The same load multicast to the CTAs of `mask` (same shared offset in each).
+// `bar` is this CTA's local barrier address with the pair bit cleared
+// (Sm100 convention): in every destination CTA the transaction bytes are
+// counted on the barrier at that offset in the destination's pair leader.
+__device__ __forceinline__ void tma_load_2d_pair_mc(void* dst, const CUtensorMap* m,
+                                                    uint32_t bar, uint16_t mask, int32_t c0,
+                                                    int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%4, %5}], [%2], %3;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "h"(mask), "r"(c0), "r"(c1)
+      : "memory");
+}
+// Local shared address of `p` with the CTA-pair bit (bit 24) cleared.
+__device__ __forceinline__ uint32_t pair_leader_addr(const void* p) {
+  return smem_u32(p) & 0xFEFFFFFFu;
+}
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc2(uint32_t* slot_smem) {  // one warp in each CTA
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -242,6 +259,15 @@ __device__ __forceinline__ void umma2(uint32_t d_tmem, uint64_t a_desc, uint64_t
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
   }
+}
+// Arrive on the mbarrier at local offset `bar` in every CTA of `mask` once
+// all previously issued cta_group::2 MMAs of this thread complete.
+__device__ __forceinline__ void umma_commit2_mask(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
 }
 // Arrive on the mbarrier at local offset `bar` in BOTH CTAs of the pair once
 // all previously issued cta_group::2 MMAs of this thread complete.

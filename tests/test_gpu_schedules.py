@@ -43,6 +43,11 @@ print(json.dumps(out))
     {"FI_SPLIT_PERS": "0"},                       # one-shot split kernel at every width
     {"FI_SPLIT_PERS": "2"},                       # persistent split kernel at every width
     {"FI_PDL": "0"},
+    # multicast clusters (two CTA pairs sharing the A rows) for every eligible GEMM
+    {"FI_GEMM_MC": "1", "FI_GEMM_PAIR": "1", "FI_GEMM_BN": "256", "FI_GEMM_KSPLIT": "1",
+     "FI_GEMM_NOTAIL": "1"},
+    {"FI_GEMM_MC": "1", "FI_GEMM_PAIR": "1", "FI_GEMM_BN": "128", "FI_GEMM_KSPLIT": "1",
+     "FI_GEMM_NOTAIL": "1"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_schedule_matches_oracle(env):
     res = subprocess.run([sys.executable, "-c", CHILD], cwd=ROOT, capture_output=True, text=True,
