@@ -539,11 +539,11 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
   FI_TRY(go(sh));
   if (sh.ksplit > 1 && !sh.sem) {  // sum the partials in order and run the epilogue
     const int tile_rows = Cf::BM * NCTA;
-    const long long chunks =
-        static_cast<long long>(tiles - sh.tile_begin) * tile_rows * (bn / 32);
-    FI_TRY(launch_ex(k_gemm_fixup<EPI>, 1, dim3(static_cast<unsigned>((chunks + 255) / 256)),
-                     dim3(256), 0, st, static_cast<const float*>(sh.part), sh.ksplit, M, N,
-                     sh.num_m, tile_rows, bn, sh.tile_begin, tiles, ep));
+    const long long blocks = static_cast<long long>(tiles - sh.tile_begin) * (tile_rows / kFixRows);
+    const size_t fsm = sizeof(float) * kFixRows * (bn / 32) * 36;  // <= 18 KB
+    FI_TRY(launch_ex(k_gemm_fixup<EPI>, 1, dim3(static_cast<unsigned>(blocks)), dim3(256), fsm,
+                     st, static_cast<const float*>(sh.part), sh.ksplit, M, N, sh.num_m,
+                     tile_rows, bn, sh.tile_begin, tiles, ep));
     FI_CUDA(cudaGetLastError());
   }
   return FI_OK;

@@ -754,42 +754,63 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
 }
 
 // Split-K fixup (FI_GEMM_INKERNEL_RED=0, or more split tiles than counters):
-// sum the ksplit raw partials of every (row, 32-column chunk)
-// of the tiles [tile_begin, T) in part order and run the launch's epilogue.
-// One thread per chunk; a tile is tile_rows x bn (bn a multiple of 32).
+// sum the ksplit raw partials of the tiles [tile_begin, T) in part order and
+// run the launch's epilogue.  One CTA per (tile, block of kFixRows rows):
+// the partial rows are read as coalesced float4 runs (each warp streams 512
+// contiguous bytes per load), summed in registers in part order
+// (deterministic), staged in shared memory, and the epilogue then runs one
+// thread per (row, 32-column chunk) from there.
+constexpr int kFixRows = 8;
 template <int EPI>
 __global__ void __launch_bounds__(256) k_gemm_fixup(const float* __restrict__ part, int ksplit,
                                                     int M, int N, int num_m, int tile_rows,
                                                     int bn, int tile_begin, int num_tiles,
                                                     GemmEpi ep) {
   pdl_wait();
-  const int per_tile = tile_rows * (bn / 32);
-  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= static_cast<long long>(num_tiles - tile_begin) * per_tile) return;
-  const int tile = tile_begin + static_cast<int>(t / per_tile);
-  const int within = static_cast<int>(t % per_tile);
-  const int lrow = (tile % num_m) * tile_rows + within / (bn / 32);
-  const int col = (tile / num_m) * bn + (within % (bn / 32)) * 32;
-  if (lrow >= M || col >= N) return;
+  extern __shared__ __align__(16) float fix_sm[];  // kFixRows x bn
+  const int blocks_per_tile = tile_rows / kFixRows;
+  const int tile = tile_begin + static_cast<int>(blockIdx.x) / blocks_per_tile;
+  const int r0 = (static_cast<int>(blockIdx.x) % blocks_per_tile) * kFixRows;
   const long long tsplit = num_tiles - tile_begin;
-  float v[32];
-#pragma unroll
-  for (int q = 0; q < 32; ++q) v[q] = 0.f;
-  for (int k = 0; k < ksplit; ++k) {
-    const float4* src = reinterpret_cast<const float4*>(
-        part + ((k * tsplit + tile - tile_begin) * tile_rows) * bn +
-        static_cast<long long>(within / (bn / 32)) * bn + (within % (bn / 32)) * 32);
+  const int row_base = (tile % num_m) * tile_rows + r0;   // GEMM row of smem row 0
+  const int col_base = (tile / num_m) * bn;
+  const long long pstride = tsplit * tile_rows * static_cast<long long>(bn);
+  const float4* src = reinterpret_cast<const float4*>(
+      part + ((tile - tile_begin) * static_cast<long long>(tile_rows) + r0) * bn);
+  // shared layout [row][chunk][36 floats]: 32 values + 4 pad, so the
+  // epilogue threads' 16-B reads of consecutive chunks hit distinct banks
+  const int chunks = bn / 32;
+  const int n4 = kFixRows * bn / 4;
+  for (int i = threadIdx.x; i < n4; i += blockDim.x) {
+    float4 acc = __ldcg(src + i);
+    for (int k = 1; k < ksplit; ++k) {
+      const float4 w = __ldcg(src + k * (pstride / 4) + i);
+      acc.x += w.x;
+      acc.y += w.y;
+      acc.z += w.z;
+      acc.w += w.w;
+    }
+    const int c4 = i % (bn / 4), rr = i / (bn / 4);
+    *reinterpret_cast<float4*>(fix_sm + (rr * chunks + c4 / 8) * 36 + (c4 % 8) * 4) = acc;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < kFixRows * chunks; t += blockDim.x) {
+    const int rr = t / chunks, ch = t % chunks;
+    const int lrow = row_base + rr, col = col_base + ch * 32;
+    if (lrow >= M || col >= N) continue;
+    float v[32];
+    const float4* p4 = reinterpret_cast<const float4*>(fix_sm + t * 36);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const float4 w = __ldcg(src + q);
-      v[4 * q] += w.x;
-      v[4 * q + 1] += w.y;
-      v[4 * q + 2] += w.z;
-      v[4 * q + 3] += w.w;
+      const float4 x = p4[q];
+      v[4 * q] = x.x;
+      v[4 * q + 1] = x.y;
+      v[4 * q + 2] = x.z;
+      v[4 * q + 3] = x.w;
     }
+    const EpiRow er = epi_row<EPI>(ep, lrow);
+    epi_emit<EPI>(ep, er, col, N, v);
   }
-  const EpiRow er = epi_row<EPI>(ep, lrow);
-  epi_emit<EPI>(ep, er, col, N, v);
 }
 
 }  // namespace fi
