@@ -172,6 +172,24 @@ int fi_viterbi(const fi_shape* shape, const float* L, const float* R, const floa
                const float* unary, const int32_t* lengths, float* va, float* vb, float* vo,
                int32_t* nodes, float* best, void* stream);
 
+/* Score tables of the grammar parameterisations (
+ * replaces the float64 products + row log-softmax of neuralparam.py:185-189
+ * and the matching softmax backward of backward_params, :242-320):
+ *   logp = log_softmax(A B^T, rows)     A (rows, d), B (cols, d), logp (rows, cols)
+ * e.g. log_left = log_softmax(f3 f2^T) with rows = N, cols = N + P.  The
+ * product runs on the engine's tcgen05 GEMM: tf32 operands for
+ * FI_GEMM_BF16 / FI_GEMM_TF32, bf16x3 split operands for FI_GEMM_FP32 (the
+ * 1e-4 parity mode).  ws: fi_param_workspace_bytes device bytes (scratch;
+ * the backward does not need the forward's). */
+size_t fi_param_workspace_bytes(int32_t gemm_dtype, int32_t rows, int32_t cols, int32_t d);
+int fi_param_scores(int32_t gemm_dtype, int32_t rows, int32_t cols, int32_t d, const float* A,
+                    const float* B, float* logp, void* ws, void* stream);
+/* Backward of fi_param_scores given dlogp = dLoss/dlogp:
+ *   g = dlogp - exp(logp) * rowsum(dlogp);  dA = g B;  dB = g^T A. */
+int fi_param_scores_backward(int32_t gemm_dtype, int32_t rows, int32_t cols, int32_t d,
+                             const float* A, const float* B, const float* logp,
+                             const float* dlogp, float* dA, float* dB, void* ws, void* stream);
+
 /* Test hook: C[M,N] = A * B^T in the engine's tcgen05 GEMM (fp32 out).
  * a_mn / b_mn select MN-major operands: A is (M,K) K-major or (K,M) MN-major,
  * B is (N,K) K-major or (K,N) MN-major; elements bf16 (dtype 0) or fp32/tf32. */

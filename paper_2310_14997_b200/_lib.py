@@ -84,6 +84,12 @@ SIGNATURES = [
     ("fi_viterbi", c_int32,
      [POINTER(FiShape), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
       c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("fi_param_workspace_bytes", c_size_t, [c_int32, c_int32, c_int32, c_int32]),
+    ("fi_param_scores", c_int32,
+     [c_int32, c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("fi_param_scores_backward", c_int32,
+     [c_int32, c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+      c_void_p, c_void_p, c_void_p]),
     ("fi_test_gemm", c_int32,
      [c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p,
       c_void_p]),

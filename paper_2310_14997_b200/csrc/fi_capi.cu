@@ -32,6 +32,7 @@
 #include "fi_gemm.cuh"
 #include "fi_kernels.cuh"
 #include "fi_decode.cuh"
+#include "fi_param.cuh"
 
 using namespace fi;
 
@@ -606,6 +607,9 @@ GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int bn_max_p
   // 256 x 512 whole-tile splits at small M measured slower (kept to N tiles
   // <= 256 there).
   static const bool inkernel_red = gemm_env("FI_GEMM_INKERNEL_RED", 0) != 0;
+  // k_gemm_fixup: fixed cost (launch + ramp, us) and partial-read rate (GB/s)
+  static const double fix_us = gemm_env("FI_GEMM_FIXUP_US", 12);
+  static const double fix_gbs = gemm_env("FI_GEMM_FIXUP_GBS", 3000);
   for (int pair = 0; pair < 2; ++pair) {
     if (force_pair >= 0 && pair != force_pair) continue;
     const int step = pair ? step_pair : step_single;
@@ -625,12 +629,12 @@ GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int bn_max_p
                static_cast<double>(ks) * r * tile_rows * bn <= static_cast<double>(g_kpart.floats);
       };
       auto fixup_us = [&](long long r, int ks) {  // whole-tile split
-        return (inkernel_red ? 8.0 : 12.0) +
-               2.0 * ks * static_cast<double>(r) * tile_rows * bn * 4.0 / 3.0e6;
+        return (inkernel_red ? 8.0 : fix_us) +
+               2.0 * ks * static_cast<double>(r) * tile_rows * bn * 4.0 / (fix_gbs * 1e3);
       };
       auto tail_red_us = [&](long long r, int ks) {
         if (inkernel_red) return 3.0 + 2.0 * 128 * bn * 4.0 / 60.0e3;
-        return 12.0 + 2.0 * ks * static_cast<double>(r) * tile_rows * bn * 4.0 / 3.0e6;
+        return fix_us + 2.0 * ks * static_cast<double>(r) * tile_rows * bn * 4.0 / (fix_gbs * 1e3);
       };
       auto consider = [&](double cost, int ks, int tail) {
         if (cost < best_cost * 0.995) {
@@ -1213,6 +1217,117 @@ int backward_impl(const Plan& p, const float* L, const float* R, const float* ro
   return FI_OK;
 }
 
+// ------------------------------------------------ parameterisation tables
+// Workspace of fi_param_scores / fi_param_scores_backward (fi_param.cuh):
+// packed operands (padded to 64 columns; bf16 hi + lo planes in fp32 mode,
+// fp32 for tf32), the fp32 product / softmax-gradient operand, the padded
+// gradient outputs and one split-K region.
+struct ParamPlan {
+  bool split;  // fp32 mode: bf16x3 split products
+  int esz, planes, dp, cp;
+  size_t a, b, c, g, da, db, kpart, total;
+};
+
+int param_plan(int mode, int rows, int cols, int d, ParamPlan* q) {
+  if (rows < 1 || cols < 1 || d < 1)
+    return set_err(FI_ERR_ARG, "score table needs rows, cols, d >= 1 (got %d, %d, %d)", rows, cols,
+                   d);
+  if (mode != FI_GEMM_BF16 && mode != FI_GEMM_TF32 && mode != FI_GEMM_FP32)
+    return set_err(FI_ERR_ARG, "unknown gemm_dtype %d", mode);
+  q->split = mode == FI_GEMM_FP32;
+  q->esz = q->split ? 2 : 4;
+  q->planes = q->split ? 2 : 1;
+  q->dp = static_cast<int>(align_up(d, 64));
+  q->cp = static_cast<int>(align_up(cols, 64));
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + bytes, 1024);
+    return o;
+  };
+  const size_t e = static_cast<size_t>(q->esz) * q->planes;
+  q->a = take(e * rows * q->dp);
+  q->b = take(e * q->cp * q->dp);
+  q->c = take(4ull * rows * q->cp);
+  q->g = take(e * rows * q->cp);
+  q->da = take(4ull * rows * q->dp);
+  q->db = take(4ull * q->cp * q->dp);
+  q->kpart = take(4ull * kKPartRegion);
+  q->total = off;
+  return FI_OK;
+}
+
+unsigned grid_for(long long n) {
+  const long long b = (n + 255) / 256;
+  return static_cast<unsigned>(b < 4LL * num_sms() ? (b < 1 ? 1 : b) : 4LL * num_sms());
+}
+
+template <typename T>
+int param_forward(const ParamPlan& q, int rows, int cols, int d, const float* A, const float* B,
+                  float* logp, void* ws, cudaStream_t st) {
+  T* ap = at<T>(ws, q.a);
+  T* bp = at<T>(ws, q.b);
+  float* c = at<float>(ws, q.c);
+  const long long alo = q.split ? static_cast<long long>(rows) * q.dp : 0;
+  const long long blo = q.split ? static_cast<long long>(cols) * q.dp : 0;
+  ProfScope prof(FI_PROF_PREP, st);
+  k_pack_rows<T><<<grid_for(1LL * rows * q.dp), 256, 0, st>>>(A, rows, d, ap, q.dp, alo);
+  k_pack_rows<T><<<grid_for(1LL * cols * q.dp), 256, 0, st>>>(B, cols, d, bp, q.dp, blo);
+  g_launches += 2;
+  FI_CUDA(cudaGetLastError());
+  GemmEpi ep = {};
+  ep.M = rows;
+  ep.C = c;
+  ep.ldc = q.cp;
+  const Operand opA{ap, q.dp, rows, q.dp, false, alo};
+  const Operand opB{bp, q.dp, cols, q.dp, false, blo};
+  FI_TRY((run_gemm<T, false, false, EPI_STORE>(opA, opB, rows, q.cp, q.dp, 0, ep, st)));
+  k_row_log_softmax<<<rows, 256, 0, st>>>(c, q.cp, logp, cols);
+  ++g_launches;
+  FI_CUDA(cudaGetLastError());
+  return FI_OK;
+}
+
+template <typename T>
+int param_backward(const ParamPlan& q, int rows, int cols, int d, const float* A, const float* B,
+                   const float* logp, const float* dlogp, float* dA, float* dB, void* ws,
+                   cudaStream_t st) {
+  T* ap = at<T>(ws, q.a);
+  T* bp = at<T>(ws, q.b);
+  T* g = at<T>(ws, q.g);
+  float* da = at<float>(ws, q.da);
+  float* db = at<float>(ws, q.db);
+  const long long alo = q.split ? static_cast<long long>(rows) * q.dp : 0;
+  const long long blo = q.split ? static_cast<long long>(cols) * q.dp : 0;
+  const long long glo = q.split ? static_cast<long long>(rows) * q.cp : 0;
+  ProfScope prof(FI_PROF_PREP, st);
+  k_pack_rows<T><<<grid_for(1LL * rows * q.dp), 256, 0, st>>>(A, rows, d, ap, q.dp, alo);
+  k_pack_rows<T><<<grid_for(1LL * cols * q.dp), 256, 0, st>>>(B, cols, d, bp, q.dp, blo);
+  k_row_softmax_bwd<T><<<rows, 256, 0, st>>>(logp, dlogp, cols, g, q.cp, glo);
+  g_launches += 3;
+  FI_CUDA(cudaGetLastError());
+  GemmEpi ep = {};
+  // dA = g B: (rows x cp) K-major times B as MN-major (K = cols rows, N = dp)
+  ep.M = rows;
+  ep.C = da;
+  ep.ldc = q.dp;
+  FI_TRY((run_gemm<T, false, true, EPI_STORE>(Operand{g, q.cp, rows, q.cp, false, glo},
+                                              Operand{bp, q.dp, cols, q.dp, true, blo}, rows, q.dp,
+                                              q.cp, 0, ep, st)));
+  // dB = g^T A: g as MN-major A (M = cp, K = rows), A as MN-major B (K = rows, N = dp)
+  ep.M = q.cp;
+  ep.C = db;
+  ep.ldc = q.dp;
+  FI_TRY((run_gemm<T, true, true, EPI_STORE>(Operand{g, q.cp, rows, q.cp, true, glo},
+                                             Operand{ap, q.dp, rows, q.dp, true, alo}, q.cp, q.dp,
+                                             rows, 0, ep, st)));
+  k_copy_cols<<<grid_for(1LL * rows * d), 256, 0, st>>>(da, q.dp, dA, rows, d);
+  k_copy_cols<<<grid_for(1LL * cols * d), 256, 0, st>>>(db, q.dp, dB, cols, d);
+  g_launches += 2;
+  FI_CUDA(cudaGetLastError());
+  return FI_OK;
+}
+
 }  // namespace
 
 // ====================================================================== ABI
@@ -1399,6 +1514,40 @@ int fi_viterbi(const fi_shape* shape, const float* L, const float* R, const floa
   ++g_launches;
   FI_CUDA(cudaGetLastError());
   return FI_OK;
+}
+
+size_t fi_param_workspace_bytes(int32_t gemm_dtype, int32_t rows, int32_t cols, int32_t d) {
+  ParamPlan q;
+  if (param_plan(gemm_dtype, rows, cols, d, &q) != FI_OK) return 0;
+  return q.total;
+}
+
+int fi_param_scores(int32_t gemm_dtype, int32_t rows, int32_t cols, int32_t d, const float* A,
+                    const float* B, float* logp, void* ws, void* stream) {
+  ParamPlan q;
+  FI_TRY(param_plan(gemm_dtype, rows, cols, d, &q));
+  FI_TRY(check_ptrs({A, B, logp, ws}));
+  FI_TRY(load_encode());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  KPartScope kps(at<float>(ws, q.kpart), st, 1);
+  FI_TRY(kps.err);
+  if (q.split) return param_forward<__nv_bfloat16>(q, rows, cols, d, A, B, logp, ws, st);
+  return param_forward<float>(q, rows, cols, d, A, B, logp, ws, st);
+}
+
+int fi_param_scores_backward(int32_t gemm_dtype, int32_t rows, int32_t cols, int32_t d,
+                             const float* A, const float* B, const float* logp,
+                             const float* dlogp, float* dA, float* dB, void* ws, void* stream) {
+  ParamPlan q;
+  FI_TRY(param_plan(gemm_dtype, rows, cols, d, &q));
+  FI_TRY(check_ptrs({A, B, logp, dlogp, dA, dB, ws}));
+  FI_TRY(load_encode());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  KPartScope kps(at<float>(ws, q.kpart), st, 1);
+  FI_TRY(kps.err);
+  if (q.split)
+    return param_backward<__nv_bfloat16>(q, rows, cols, d, A, B, logp, dlogp, dA, dB, ws, st);
+  return param_backward<float>(q, rows, cols, d, A, B, logp, dlogp, dA, dB, ws, st);
 }
 
 int fi_test_gemm(int32_t dtype, int32_t a_mn, int32_t b_mn, int32_t M, int32_t N, int32_t K,

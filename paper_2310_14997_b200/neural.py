@@ -22,9 +22,11 @@ step of train.py, with the same names and semantics:
                          -> backward -> (data-parallel all-reduce of the
                          PARAMETER gradients) -> clip -> Adam
 
-The parameterisation's dense products (N x d by d x (N+P) score tables) are
-plain library GEMMs (cuBLAS through torch.matmul); the inside algorithm runs
-on this repo's engine.  With data parallelism the single collective is an
+The four score tables (N x d by d x (N+P) products + row log-softmax, and
+their backward) run on this repo's engine (``score_table``:
+fi_param_scores / fi_param_scores_backward, the tcgen05 GEMM); the residual
+MLP layers (d x d) are plain library GEMMs; the inside algorithm runs on the
+engine.  With data parallelism the single collective is an
 all-reduce of the parameter gradients (~9.2 M + 512 V floats at N = 4096,
 d = 512), not of dL and dR (67 M floats).
 """
@@ -39,9 +41,10 @@ import torch
 import torch.distributed as dist
 import torch.nn.functional as F
 
+from . import _lib
 from .dp import allreduce_grads
 from .grammar import GrammarDims
-from .ops import inside
+from .ops import _p, _stream, inside
 
 
 class ParamError(Exception):
@@ -106,12 +109,78 @@ def _two_layer(x, w1, b1, w2, b2):
     return x + torch.relu(x @ w1.T + b1) @ w2.T + b2
 
 
-def grammar_tables(p: EmbeddingParams, tied: bool = False, finite_flags: list | None = None):
-    """(log_root (N,), log_left (N, N+P), log_right, log_emit (P, V)), differentiable.
+class _ScoreTable(torch.autograd.Function):
+    """log_softmax(A B^T, rows) on the engine (fi_param_scores /
+    fi_param_scores_backward: the tcgen05 GEMM + row log-softmax passes)."""
+
+    @staticmethod
+    def forward(ctx, A, B, gemm_dtype):
+        A = A.contiguous()
+        B = B.contiguous()
+        rows, d = A.shape
+        cols = B.shape[0]
+        mode = _lib.GEMM_DTYPES[gemm_dtype]
+        lib = _lib.load()
+        ws = torch.empty(lib.fi_param_workspace_bytes(mode, rows, cols, d), dtype=torch.uint8,
+                         device=A.device)
+        logp = torch.empty(rows, cols, dtype=torch.float32, device=A.device)
+        with torch.cuda.device(A.device):
+            _lib.check(lib.fi_param_scores(mode, rows, cols, d, _p(A), _p(B), _p(logp), _p(ws),
+                                           _stream(A.device)))
+        ctx.save_for_backward(A, B, logp)
+        ctx.mode = mode
+        return logp
+
+    @staticmethod
+    def backward(ctx, dlogp):
+        A, B, logp = ctx.saved_tensors
+        rows, d = A.shape
+        cols = B.shape[0]
+        lib = _lib.load()
+        dlogp = dlogp.contiguous().to(torch.float32)
+        ws = torch.empty(lib.fi_param_workspace_bytes(ctx.mode, rows, cols, d),
+                         dtype=torch.uint8, device=A.device)
+        dA = torch.empty_like(A)
+        dB = torch.empty_like(B)
+        with torch.cuda.device(A.device):
+            _lib.check(lib.fi_param_scores_backward(ctx.mode, rows, cols, d, _p(A), _p(B),
+                                                    _p(logp), _p(dlogp), _p(dA), _p(dB), _p(ws),
+                                                    _stream(A.device)))
+        return dA, dB, None
+
+
+def score_table(A: torch.Tensor, B: torch.Tensor, gemm_dtype: str = "fp32") -> torch.Tensor:
+    """log_softmax(A @ B.T, dim=-1) of fp32 CUDA tensors on the engine's kernels
+    (neuralparam.py:185-189); differentiable in A and B.  tf32 products for
+    gemm_dtype "bf16" / "tf32", bf16x3 split products for "fp32" (parity)."""
+    if not (A.is_cuda and B.is_cuda) or A.dtype != torch.float32 or B.dtype != torch.float32:
+        raise ValueError("score_table needs fp32 CUDA tensors (the engine has no CPU path)")
+    return _ScoreTable.apply(A, B, gemm_dtype)
+
+
+def grammar_tables(p: EmbeddingParams, tied: bool = False, finite_flags: list | None = None,
+                   gemm_dtype: str = "fp32"):
+    """(log_root (N,), log_left (N, N+P), log_right, log_emit (P, V)), differentiable,
+    on the GPU: the residual MLPs (d x d layers, library GEMMs) and the four
+    score tables on the engine (``score_table``).  Same graph as
+    ``grammar_tables_torch``, the plain-torch restatement the CPU tests pin
+    against the reference (neuralparam.py:149-208)."""
+    return _tables(p, tied, finite_flags, lambda a, b: score_table(a, b, gemm_dtype))
+
+
+def grammar_tables_torch(p: EmbeddingParams, tied: bool = False,
+                         finite_flags: list | None = None):
+    """The parameterisation in plain torch (any device / dtype, float64 on the
+    CPU in tests): the restatement of neuralparam.py:149-208 that
+    ``grammar_tables`` runs on the engine.
 
     Non-finite activations raise ParamError (neuralparam.py); with
     ``finite_flags`` the per-activation checks are appended there as device
     booleans instead (no host sync: the caller checks them once)."""
+    return _tables(p, tied, finite_flags, lambda a, b: F.log_softmax(a @ b.T, dim=-1))
+
+
+def _tables(p: EmbeddingParams, tied: bool, finite_flags: list | None, scores):
 
     def check(name, a):
         if finite_flags is not None:
@@ -133,15 +202,15 @@ def grammar_tables(p: EmbeddingParams, tied: bool = False, finite_flags: list | 
                     t["f5.w3"], t["f5.b3"], t["f5.w4"], t["f5.b4"])
     for name, a in (("f1", f1), ("f2", f2), ("f3", f3), ("f5", f5)):
         check(name, a)
-    log_root = F.log_softmax((f1 @ t["u_nt"].T)[0], dim=-1)
-    log_left = F.log_softmax(f3 @ f2.T, dim=-1)
+    log_root = scores(f1, t["u_nt"])[0]
+    log_left = scores(f3, f2)
     if tied:
         log_right = log_left
     else:
         f4 = _residual_relu(x_child, t["f4.w"], t["f4.b"])
         check("f4", f4)
-        log_right = F.log_softmax(f3 @ f4.T, dim=-1)
-    log_emit = F.log_softmax(f5 @ t["u_voc"].T, dim=-1)
+        log_right = scores(f3, f4)
+    log_emit = scores(f5, t["u_voc"])
     return log_root, log_left, log_right, log_emit
 
 
@@ -163,6 +232,8 @@ def init_direct(dims: GrammarDims, seed: int = 0, scale: float = 0.5, device=Non
 
 
 def direct_tables(p: DirectLogits, tied: bool = False):
+    """Row log-softmax of the raw tables (neuralparam.py:359-375); elementwise
+    library ops (no product to put on the engine)."""
     t = p.tensors
     log_left = F.log_softmax(t["left"], dim=-1)
     log_right = log_left if tied else F.log_softmax(t["right"], dim=-1)
@@ -266,7 +337,8 @@ class TrainStep:
 
     def tables(self, finite_flags: list | None = None):
         if isinstance(self.params, EmbeddingParams):
-            return grammar_tables(self.params, self.config.tied, finite_flags)
+            return grammar_tables(self.params, self.config.tied, finite_flags,
+                                  self.config.gemm_dtype)
         return direct_tables(self.params, self.config.tied)
 
     def _forward_backward(self, tokens: torch.Tensor, lengths: torch.Tensor, denom: float):

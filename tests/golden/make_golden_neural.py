@@ -78,6 +78,22 @@ def main():
     bd = backward_direct(dl, total)
     for k, v in bd.tensors.items():
         gold["direct.grad." + k] = v.copy()
+    # realistic size: |N| = P = 256, V = 64, d = 64 (the GPU step's parity at scale)
+    bdims = GrammarDims(256, 256, 64)
+    bp = init_params(bdims, 64, SEED)
+    btoks = np.random.default_rng(SEED + 2).integers(0, 64, size=(4, 10))
+    gold["big.tokens"] = btoks
+    g = forward_grammar(bp)
+    for name in ("log_root", "log_left", "log_right", "log_emit"):
+        gold[f"big.{name}"] = getattr(g, name).copy()
+    total = GrammarGrad.zeros(bdims)
+    for row in btoks:
+        gr, _ = inside_backward(g, row, inside_flash(g, row))
+        total.add_(gr)
+    total.scale_(-1.0 / len(btoks))
+    pg = backward_params(bp, total)
+    for k, v in pg.tensors.items():
+        gold[f"big.grad.{k}"] = v.copy()
     np.savez_compressed(OUT, **gold)
     print(f"wrote {OUT} ({len(gold)} arrays)")
 

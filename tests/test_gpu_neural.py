@@ -66,3 +66,50 @@ def test_training_reduces_the_loss_bf16():
     losses = [float(ts.step(tok, lengths)) for _ in range(15)]
     assert all(np.isfinite(losses))
     assert losses[-1] < losses[0] - 1.0
+
+
+@pytest.mark.parametrize("rows,cols,d", [(6, 11, 16), (1, 6, 16), (256, 512, 64), (300, 700, 96),
+                                         (1024, 2048, 512)])
+@pytest.mark.parametrize("gemm_dtype,tol", [("fp32", 1e-5), ("tf32", 2e-3)])
+def test_score_table_on_the_engine(rows, cols, d, gemm_dtype, tol):
+    """log_softmax(A B^T) and its backward through fi_param_scores(_backward)
+    (tcgen05 GEMM + row passes) against float64 torch."""
+    g = torch.Generator(device="cuda").manual_seed(rows + cols + d)
+    A = torch.randn(rows, d, device="cuda", generator=g) / d ** 0.25
+    B = torch.randn(cols, d, device="cuda", generator=g) / d ** 0.25
+    up = torch.randn(rows, cols, device="cuda", generator=g)
+    A.requires_grad_(True)
+    B.requires_grad_(True)
+    lp = neural.score_table(A, B, gemm_dtype)
+    (lp * up).sum().backward()
+    A64 = A.detach().double().requires_grad_(True)
+    B64 = B.detach().double().requires_grad_(True)
+    lp64 = torch.log_softmax(A64 @ B64.T, dim=-1)
+    (lp64 * up.double()).sum().backward()
+    for name, got, want in (("logp", lp.detach(), lp64.detach()), ("dA", A.grad, A64.grad),
+                            ("dB", B.grad, B64.grad)):
+        err = ((got.double() - want).abs().max() / want.abs().max()).item()
+        assert err < tol, f"{name}: {err:.2e}"
+
+
+def test_realistic_size_gradients_match_reference():
+    """|N| = P = 256, V = 64, d = 64 (tests/golden/neural.npz "big.*", the
+    reference's forward_grammar + inside_backward + backward_params): the
+    GPU step's tables and parameter gradients in fp32 mode."""
+    dims = GrammarDims(256, 256, 64)
+    ts = neural.TrainStep(neural.init_params(dims, 64, SEED, device="cuda"),
+                          neural.TrainConfig(gemm_dtype="fp32"))
+    with torch.no_grad():
+        tabs = ts.tables()
+    for name, t in zip(("log_root", "log_left", "log_right", "log_emit"), tabs):
+        want = GOLD[f"big.{name}"]
+        np.testing.assert_allclose(t.double().cpu().numpy(), want, rtol=FP32,
+                                   atol=FP32 * np.abs(want).max(), err_msg=name)
+    tok = torch.as_tensor(GOLD["big.tokens"], device="cuda")
+    lengths = torch.full((tok.shape[0],), tok.shape[1], dtype=torch.int32, device="cuda")
+    loss, grads = ts.loss_and_grads(tok, lengths)
+    for k, gr in zip(ts.params.tensors, grads):
+        want = GOLD[f"big.grad.{k}"]
+        got = gr.double().cpu().numpy()
+        np.testing.assert_allclose(got, want, rtol=FP32, atol=FP32 * np.abs(want).max() + 1e-12,
+                                   err_msg=k)

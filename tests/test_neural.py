@@ -29,7 +29,7 @@ def test_init_params_draws_match_reference():
 @pytest.mark.parametrize("tied", [False, True])
 def test_grammar_tables_match_forward_grammar(tied):
     tag = "tied" if tied else "untied"
-    tabs = neural.grammar_tables(params64(), tied)
+    tabs = neural.grammar_tables_torch(params64(), tied)
     for name, t in zip(("log_root", "log_left", "log_right", "log_emit"), tabs):
         np.testing.assert_allclose(t.numpy(), GOLD[f"{tag}.{name}"], rtol=1e-12, atol=1e-12,
                                    err_msg=name)
@@ -43,7 +43,7 @@ def test_autograd_matches_backward_params(tied):
     xs = list(p.tensors.values())
     for x in xs:
         x.requires_grad_(True)
-    tabs = neural.grammar_tables(p, tied)
+    tabs = neural.grammar_tables_torch(p, tied)
     gg = [torch.tensor(GOLD[f"{tag}.gg.{n}"]) for n in ("d_root", "d_left", "d_right", "d_emit")]
     if tied:  # the reference adds d_left + d_right onto the single left head
         obj = (gg[0] * tabs[0]).sum() + ((gg[1] + gg[2]) * tabs[1]).sum() + (gg[3] * tabs[3]).sum()
