@@ -1262,27 +1262,54 @@ unsigned grid_for(long long n) {
   return static_cast<unsigned>(b < 4LL * num_sms() ? (b < 1 ? 1 : b) : 4LL * num_sms());
 }
 
+// Row passes: threads per CTA and whether the register-resident float4 form applies.
+struct RowLaunch {
+  int threads;
+  bool vec;
+};
+RowLaunch row_launch(int cols, int ld_a, int ld_b) {
+  const int threads = cols > 4 * kRowVec * 256 ? 512 : 256;
+  const bool vec = cols % 4 == 0 && ld_a % 4 == 0 && ld_b % 4 == 0 &&
+                   cols <= 4 * kRowVec * threads;
+  return {threads, vec};
+}
+
+// Operands already in the GEMM's format need no packing: fp32 (tf32) rows of
+// a multiple of 64 elements are TMA-ready as they are.
+bool param_direct(const ParamPlan& q, int d) { return !q.split && d % 64 == 0; }
+
 template <typename T>
 int param_forward(const ParamPlan& q, int rows, int cols, int d, const float* A, const float* B,
                   float* logp, void* ws, cudaStream_t st) {
-  T* ap = at<T>(ws, q.a);
-  T* bp = at<T>(ws, q.b);
-  float* c = at<float>(ws, q.c);
+  const bool direct = param_direct(q, d);
+  const T* ap = direct ? reinterpret_cast<const T*>(A) : at<T>(ws, q.a);
+  const T* bp = direct ? reinterpret_cast<const T*>(B) : at<T>(ws, q.b);
   const long long alo = q.split ? static_cast<long long>(rows) * q.dp : 0;
   const long long blo = q.split ? static_cast<long long>(cols) * q.dp : 0;
   ProfScope prof(FI_PROF_PREP, st);
-  k_pack_rows<T><<<grid_for(1LL * rows * q.dp), 256, 0, st>>>(A, rows, d, ap, q.dp, alo);
-  k_pack_rows<T><<<grid_for(1LL * cols * q.dp), 256, 0, st>>>(B, cols, d, bp, q.dp, blo);
-  g_launches += 2;
-  FI_CUDA(cudaGetLastError());
+  if (!direct) {
+    k_pack_rows<T><<<grid_for(1LL * rows * q.dp), 256, 0, st>>>(A, rows, d, at<T>(ws, q.a), q.dp,
+                                                                alo);
+    k_pack_rows<T><<<grid_for(1LL * cols * q.dp), 256, 0, st>>>(B, cols, d, at<T>(ws, q.b), q.dp,
+                                                                blo);
+    g_launches += 2;
+    FI_CUDA(cudaGetLastError());
+  }
+  // the product lands in logp itself when its rows are 64-aligned (the row
+  // pass then runs in place), else in the padded scratch
+  const bool inplace = cols % 64 == 0;
+  float* c = inplace ? logp : at<float>(ws, q.c);
+  const int ldc = inplace ? cols : q.cp;
   GemmEpi ep = {};
   ep.M = rows;
   ep.C = c;
-  ep.ldc = q.cp;
+  ep.ldc = ldc;
   const Operand opA{ap, q.dp, rows, q.dp, false, alo};
   const Operand opB{bp, q.dp, cols, q.dp, false, blo};
   FI_TRY((run_gemm<T, false, false, EPI_STORE>(opA, opB, rows, q.cp, q.dp, 0, ep, st)));
-  k_row_log_softmax<<<rows, 256, 0, st>>>(c, q.cp, logp, cols);
+  const RowLaunch rl = row_launch(cols, ldc, cols);
+  if (rl.vec) k_row_log_softmax<true><<<rows, rl.threads, 0, st>>>(c, ldc, logp, cols);
+  else k_row_log_softmax<false><<<rows, rl.threads, 0, st>>>(c, ldc, logp, cols);
   ++g_launches;
   FI_CUDA(cudaGetLastError());
   return FI_OK;
@@ -1292,19 +1319,29 @@ template <typename T>
 int param_backward(const ParamPlan& q, int rows, int cols, int d, const float* A, const float* B,
                    const float* logp, const float* dlogp, float* dA, float* dB, void* ws,
                    cudaStream_t st) {
-  T* ap = at<T>(ws, q.a);
-  T* bp = at<T>(ws, q.b);
+  const bool direct = param_direct(q, d);
+  const T* ap = direct ? reinterpret_cast<const T*>(A) : at<T>(ws, q.a);
+  const T* bp = direct ? reinterpret_cast<const T*>(B) : at<T>(ws, q.b);
   T* g = at<T>(ws, q.g);
-  float* da = at<float>(ws, q.da);
-  float* db = at<float>(ws, q.db);
+  float* da = direct ? dA : at<float>(ws, q.da);
+  float* db = direct && cols % 64 == 0 ? dB : at<float>(ws, q.db);
   const long long alo = q.split ? static_cast<long long>(rows) * q.dp : 0;
   const long long blo = q.split ? static_cast<long long>(cols) * q.dp : 0;
   const long long glo = q.split ? static_cast<long long>(rows) * q.cp : 0;
   ProfScope prof(FI_PROF_PREP, st);
-  k_pack_rows<T><<<grid_for(1LL * rows * q.dp), 256, 0, st>>>(A, rows, d, ap, q.dp, alo);
-  k_pack_rows<T><<<grid_for(1LL * cols * q.dp), 256, 0, st>>>(B, cols, d, bp, q.dp, blo);
-  k_row_softmax_bwd<T><<<rows, 256, 0, st>>>(logp, dlogp, cols, g, q.cp, glo);
-  g_launches += 3;
+  if (!direct) {
+    k_pack_rows<T><<<grid_for(1LL * rows * q.dp), 256, 0, st>>>(A, rows, d, at<T>(ws, q.a), q.dp,
+                                                                alo);
+    k_pack_rows<T><<<grid_for(1LL * cols * q.dp), 256, 0, st>>>(B, cols, d, at<T>(ws, q.b), q.dp,
+                                                                blo);
+    g_launches += 2;
+  }
+  const RowLaunch rl = row_launch(cols, cols, q.cp);
+  if (rl.vec)
+    k_row_softmax_bwd<T, true><<<rows, rl.threads, 0, st>>>(logp, dlogp, cols, g, q.cp, glo);
+  else
+    k_row_softmax_bwd<T, false><<<rows, rl.threads, 0, st>>>(logp, dlogp, cols, g, q.cp, glo);
+  ++g_launches;
   FI_CUDA(cudaGetLastError());
   GemmEpi ep = {};
   // dA = g B: (rows x cp) K-major times B as MN-major (K = cols rows, N = dp)
@@ -1315,15 +1352,20 @@ int param_backward(const ParamPlan& q, int rows, int cols, int d, const float* A
                                               Operand{bp, q.dp, cols, q.dp, true, blo}, rows, q.dp,
                                               q.cp, 0, ep, st)));
   // dB = g^T A: g as MN-major A (M = cp, K = rows), A as MN-major B (K = rows, N = dp)
-  ep.M = q.cp;
+  ep.M = db == dB ? cols : q.cp;
   ep.C = db;
   ep.ldc = q.dp;
   FI_TRY((run_gemm<T, true, true, EPI_STORE>(Operand{g, q.cp, rows, q.cp, true, glo},
-                                             Operand{ap, q.dp, rows, q.dp, true, alo}, q.cp, q.dp,
+                                             Operand{ap, q.dp, rows, q.dp, true, alo}, ep.M, q.dp,
                                              rows, 0, ep, st)));
-  k_copy_cols<<<grid_for(1LL * rows * d), 256, 0, st>>>(da, q.dp, dA, rows, d);
-  k_copy_cols<<<grid_for(1LL * cols * d), 256, 0, st>>>(db, q.dp, dB, cols, d);
-  g_launches += 2;
+  if (da != dA) {
+    k_copy_cols<<<grid_for(1LL * rows * d), 256, 0, st>>>(da, q.dp, dA, rows, d);
+    ++g_launches;
+  }
+  if (db != dB) {
+    k_copy_cols<<<grid_for(1LL * cols * d), 256, 0, st>>>(db, q.dp, dB, cols, d);
+    ++g_launches;
+  }
   FI_CUDA(cudaGetLastError());
   return FI_OK;
 }
