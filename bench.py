@@ -635,7 +635,8 @@ def run_train(args, world, rank, local):
     roofline = roofline_block(prof, args.steps, n, batch, length,
                               4 if args.gemm_dtype == "tf32" else 2,
                               2 if chart_fmt == _lib.FI_CHART_F16 else 4)
-    inside_ms = sum(d["ms_per_step"] for d in roofline["per_class"].values())
+    inside_ms = sum(d["ms_per_step"] for k, d in roofline["per_class"].items() if k != "param")
+    param_ms = roofline["per_class"].get("param", {}).get("ms_per_step", 0.0)
     if rank == 0:
         print(json.dumps({
             "metric": TRAIN_METRIC, "value": world * batch / (ms / 1e3), "unit": "sentences/s",
@@ -648,7 +649,8 @@ def run_train(args, world, rank, local):
                        "parallelism": f"dp{world}", "global_batch": batch * world},
             "clocks": clk, "gpu_launches": gpu_launches, "loss": float(loss),
             "inside_engine_ms_per_step": inside_ms,
-            "parameterisation_and_optimizer_ms_per_step": ms - inside_ms,
+            "score_tables_ms_per_step": param_ms,
+            "mlp_and_optimizer_ms_per_step": ms - inside_ms - param_ms,
             "roofline": roofline}), flush=True)
     if world > 1:
         dist.destroy_process_group()

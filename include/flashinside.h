@@ -211,7 +211,8 @@ int64_t fi_launch_count(void);
 #define FI_PROF_GATHER 4     /* k_gather_bwd: split backward                  */
 #define FI_PROF_GEMM_DGRAD 5 /* dgrad GEMMs (EPI_DGRAD, EPI_DUNARY)           */
 #define FI_PROF_GEMM_WGRAD 6 /* wgrad GEMMs (EPI_WGRAD)                       */
-#define FI_PROF_NCLASS 7
+#define FI_PROF_PARAM 7      /* fi_param_scores(_backward): GEMMs + row passes */
+#define FI_PROF_NCLASS 8
 void fi_profile_enable(int32_t on);
 int fi_profile_collect(float* ms, int32_t* counts, int32_t n);
 /* Same record, per launch in issue order: ms[k] and class cls[k] for the

@@ -27,7 +27,7 @@ FI_FLAG_ZERO_PROB = 1
 FI_FLAG_BAD_LENGTH = 2
 
 PROF_CLASSES = ("prep", "split_fwd", "gemm_fwd", "seed", "gather_bwd", "gemm_dgrad",
-                "gemm_wgrad")
+                "gemm_wgrad", "param")
 
 GEMM_DTYPES = {"bf16": FI_GEMM_BF16, "tf32": FI_GEMM_TF32, "fp32": FI_GEMM_FP32}
 CHART_DTYPES = {"auto": FI_CHART_AUTO, "fp32": FI_CHART_F32, "fp16": FI_CHART_F16}

@@ -66,6 +66,12 @@ cudaEvent_t prof_event() {  // caller holds g_prof_mu
   return e;
 }
 
+thread_local int g_prof_class = -1;  // >= 0: class of this thread's GEMM launches
+struct ProfClassScope {  // the parameterisation's GEMMs count as FI_PROF_PARAM
+  int saved;
+  explicit ProfClassScope(int c) : saved(g_prof_class) { g_prof_class = c; }
+  ~ProfClassScope() { g_prof_class = saved; }
+};
 struct ProfScope {
   cudaStream_t st;
   ProfRec rec;
@@ -511,7 +517,8 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
   // persistent: one CTA (pair, cluster) per SM (pair, group of 4 SMs)
   const int slots = MC ? max_clusters(kern, CL, gemm_threads<CHUNK>(), smem_bytes)
                        : num_sms() / NCTA;
-  ProfScope prof(EPI == EPI_FWD || EPI == EPI_FWD_H ? FI_PROF_GEMM_FWD
+  ProfScope prof(g_prof_class >= 0 ? g_prof_class
+                 : EPI == EPI_FWD || EPI == EPI_FWD_H ? FI_PROF_GEMM_FWD
                  : EPI == EPI_WGRAD ? FI_PROF_GEMM_WGRAD
                  : EPI == EPI_STORE ? FI_PROF_PREP : FI_PROF_GEMM_DGRAD, st);  // DGRAD(_H), DUNARY
   auto go = [&](const GemmShape& g) -> int {
@@ -1286,8 +1293,9 @@ int param_forward(const ParamPlan& q, int rows, int cols, int d, const float* A,
   const T* bp = direct ? reinterpret_cast<const T*>(B) : at<T>(ws, q.b);
   const long long alo = q.split ? static_cast<long long>(rows) * q.dp : 0;
   const long long blo = q.split ? static_cast<long long>(cols) * q.dp : 0;
-  ProfScope prof(FI_PROF_PREP, st);
+  ProfClassScope pc(FI_PROF_PARAM);
   if (!direct) {
+    ProfScope prof(FI_PROF_PARAM, st);
     k_pack_rows<T><<<grid_for(1LL * rows * q.dp), 256, 0, st>>>(A, rows, d, at<T>(ws, q.a), q.dp,
                                                                 alo);
     k_pack_rows<T><<<grid_for(1LL * cols * q.dp), 256, 0, st>>>(B, cols, d, at<T>(ws, q.b), q.dp,
@@ -1308,6 +1316,7 @@ int param_forward(const ParamPlan& q, int rows, int cols, int d, const float* A,
   const Operand opB{bp, q.dp, cols, q.dp, false, blo};
   FI_TRY((run_gemm<T, false, false, EPI_STORE>(opA, opB, rows, q.cp, q.dp, 0, ep, st)));
   const RowLaunch rl = row_launch(cols, ldc, cols);
+  ProfScope prof(FI_PROF_PARAM, st);
   if (rl.vec) k_row_log_softmax<true><<<rows, rl.threads, 0, st>>>(c, ldc, logp, cols);
   else k_row_log_softmax<false><<<rows, rl.threads, 0, st>>>(c, ldc, logp, cols);
   ++g_launches;
@@ -1328,8 +1337,9 @@ int param_backward(const ParamPlan& q, int rows, int cols, int d, const float* A
   const long long alo = q.split ? static_cast<long long>(rows) * q.dp : 0;
   const long long blo = q.split ? static_cast<long long>(cols) * q.dp : 0;
   const long long glo = q.split ? static_cast<long long>(rows) * q.cp : 0;
-  ProfScope prof(FI_PROF_PREP, st);
+  ProfClassScope pc(FI_PROF_PARAM);
   if (!direct) {
+    ProfScope prof(FI_PROF_PARAM, st);
     k_pack_rows<T><<<grid_for(1LL * rows * q.dp), 256, 0, st>>>(A, rows, d, at<T>(ws, q.a), q.dp,
                                                                 alo);
     k_pack_rows<T><<<grid_for(1LL * cols * q.dp), 256, 0, st>>>(B, cols, d, at<T>(ws, q.b), q.dp,
@@ -1337,10 +1347,13 @@ int param_backward(const ParamPlan& q, int rows, int cols, int d, const float* A
     g_launches += 2;
   }
   const RowLaunch rl = row_launch(cols, cols, q.cp);
+  {
+  ProfScope prof(FI_PROF_PARAM, st);
   if (rl.vec)
     k_row_softmax_bwd<T, true><<<rows, rl.threads, 0, st>>>(logp, dlogp, cols, g, q.cp, glo);
   else
     k_row_softmax_bwd<T, false><<<rows, rl.threads, 0, st>>>(logp, dlogp, cols, g, q.cp, glo);
+  }
   ++g_launches;
   FI_CUDA(cudaGetLastError());
   GemmEpi ep = {};
@@ -1358,6 +1371,7 @@ int param_backward(const ParamPlan& q, int rows, int cols, int d, const float* A
   FI_TRY((run_gemm<T, true, true, EPI_STORE>(Operand{g, q.cp, rows, q.cp, true, glo},
                                              Operand{ap, q.dp, rows, q.dp, true, alo}, ep.M, q.dp,
                                              rows, 0, ep, st)));
+  ProfScope prof(FI_PROF_PARAM, st);
   if (da != dA) {
     k_copy_cols<<<grid_for(1LL * rows * d), 256, 0, st>>>(da, q.dp, dA, rows, d);
     ++g_launches;
