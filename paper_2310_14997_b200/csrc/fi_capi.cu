@@ -517,6 +517,8 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
   // persistent: one CTA (pair, cluster) per SM (pair, group of 4 SMs)
   const int slots = MC ? max_clusters(kern, CL, gemm_threads<CHUNK>(), smem_bytes)
                        : num_sms() / NCTA;
+  static const int log_slots = env_int("FI_GEMM_LOG", 0);
+  if (log_slots && MC) fprintf(stderr, "[fi gemm] multicast clusters: %d co-resident\n", slots);
   ProfScope prof(g_prof_class >= 0 ? g_prof_class
                  : EPI == EPI_FWD || EPI == EPI_FWD_H ? FI_PROF_GEMM_FWD
                  : EPI == EPI_WGRAD ? FI_PROF_GEMM_WGRAD
