@@ -92,3 +92,37 @@ def test_grad_bucket_roundtrip():
     for a, b in zip(bk.views(), ts):
         assert torch.equal(a, b)
     assert bk.flat.numel() == 27
+
+
+def _bucket_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ts = [torch.full((3, 4), float(rank + 1)), torch.arange(5.0) * (rank + 1)]
+        a = dp.allreduce_grads(ts)
+        first = [t.clone() for t in a]
+        b = dp.allreduce_grads([t * 2 for t in ts])   # same shapes: the bucket is reused
+        q.put((rank, [t.numpy() for t in first], [t.numpy() for t in b],
+               a[0].data_ptr() == b[0].data_ptr()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_allreduce_grads_sums_and_reuses_one_bucket():
+    """dp.allreduce_grads: one collective over a persistent flat bucket per
+    shape set (no per-step allocation), sums over ranks."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bucket_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, first, second, same in res:
+        np.testing.assert_allclose(first[0], np.full((3, 4), 3.0))
+        np.testing.assert_allclose(first[1], np.arange(5.0) * 3)
+        np.testing.assert_allclose(second[1], np.arange(5.0) * 6)
+        assert same

@@ -87,3 +87,14 @@ def test_engine_registers_into_the_reference_registry():
     reg = dict(ref_inside.ENGINES)
     engine.register(reg)
     assert set(reg) == set(ref_inside.ENGINES) | {"b200"}
+
+
+def test_check_lengths_names_the_first_bad_sentence():
+    """ops.check_lengths (the op's host-side refusal, inside.py:113-121) on
+    CPU tensors: no GPU involved."""
+    import torch
+    from paper_2310_14997_b200.ops import check_lengths
+    check_lengths(torch.tensor([2, 5, 5], dtype=torch.int32), 5)
+    for lens, b in (([5, 1, 0], 1), ([6, 2, 3], 0), ([2, 3, -1], 2)):
+        with pytest.raises(ValueError, match=f"sentence {b}: length"):
+            check_lengths(torch.tensor(lens, dtype=torch.int32), 5)
