@@ -439,8 +439,10 @@ int max_clusters(K kern, int cl, int threads, size_t smem) {
   return n;
 }
 
+// TR: A and B are the kernel's operands (A = the weight table, B = the chart
+// rows), M / N the kernel's dims; `a_row0` is then the chart rows' offset.
 template <typename T, int BN, bool AMN, bool BMN, int EPI, bool SPLIT, int CHUNK, bool PAIR,
-          bool MC = false>
+          bool MC = false, bool TR = false>
 int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_row0,
                 const GemmEpi& ep, cudaStream_t st, int bn, int ksplit, int tail) {
   using Cf = GemmCfg<T, BN>;
@@ -466,18 +468,20 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
   sh.M = M;
   sh.N = N;
   sh.K = K;
-  sh.a_row0 = a_row0;
+  sh.a_row0 = TR ? 0 : a_row0;
+  sh.b_row0 = TR ? a_row0 : 0;
   sh.bn = bn;
   // ring depth: as many (A + this CTA's share of B) stages as fit in 227 KB
   // (a pair CTA stages half the N tile, so pairs run deeper rings)
   sh.b_stage = bn / NCTA * 128 * (SPLIT ? 2 : 1);  // SPLIT: hi and lo tiles per stage
   const int stage_bytes = Cf::A_BYTES * (SPLIT ? 2 : 1) + sh.b_stage;
-  int max_stages = (kGemmSmemMax - 1024 - 256) / stage_bytes;
+  constexpr int kTransBytes = TR ? 4 * 32 * 33 * 4 : 0;  // epilogue transpose tiles
+  int max_stages = (kGemmSmemMax - 1024 - 256 - kTransBytes) / stage_bytes;
   max_stages = max_stages > kGemmStagesMax ? kGemmStagesMax : max_stages;
   static const int env_stages = env_int("FI_GEMM_STAGES", 0);  // A/B experiments
   const int cap = g_gemm_stages > 1 ? g_gemm_stages : env_stages;
   sh.stages = (cap > 1 && cap < max_stages) ? cap : max_stages;
-  const size_t smem_bytes = static_cast<size_t>(sh.stages) * stage_bytes + 1024 + 256;
+  const size_t smem_bytes = static_cast<size_t>(sh.stages) * stage_bytes + 1024 + 256 + kTransBytes;
 
   sh.num_m = (M + Cf::BM * NCTA - 1) / (Cf::BM * NCTA);
   sh.num_n = (N + bn - 1) / bn;
@@ -501,11 +505,11 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
     // the other needs, so it is opt-in (measured: no faster than the fixup
     // kernel at config 3, 14.35-14.48 vs 14.41-14.64 ms).
     static const int inkernel = env_int("FI_GEMM_INKERNEL_RED", 0);
-    if (inkernel && g_kpart.sem && tsplit <= kKPartSems) sh.sem = g_kpart.sem;
+    if (inkernel && !TR && g_kpart.sem && tsplit <= kKPartSems) sh.sem = g_kpart.sem;
   } else {
     tail = 0;  // no split-K available: whole tiles only
   }
-  auto kern = k_gemm<T, BN, AMN, BMN, EPI, SPLIT, CHUNK, PAIR, MC>;
+  auto kern = k_gemm<T, BN, AMN, BMN, EPI, SPLIT, CHUNK, PAIR, MC, TR>;
   static bool attr_done[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -547,7 +551,15 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
     sh.tile_begin = tiles - tail;
   }
   FI_TRY(go(sh));
-  if (sh.ksplit > 1 && !sh.sem) {  // sum the partials in order and run the epilogue
+  if (TR && sh.ksplit > 1) {  // transposed partial tiles: sum, transpose, epilogue
+    const int tile_rows = Cf::BM * NCTA;
+    const long long blocks = static_cast<long long>(tiles - sh.tile_begin) * (tile_rows / 32);
+    const size_t fsm = sizeof(float) * 32 * (bn + 1);
+    FI_TRY(launch_ex(k_gemm_fixup_tr<EPI>, 1, dim3(static_cast<unsigned>(blocks)), dim3(256), fsm,
+                     st, static_cast<const float*>(sh.part), sh.ksplit, M, N, sh.num_m,
+                     tile_rows, bn, sh.tile_begin, tiles, ep));
+    FI_CUDA(cudaGetLastError());
+  } else if (sh.ksplit > 1 && !sh.sem) {  // sum the partials in order and run the epilogue
     const int tile_rows = Cf::BM * NCTA;
     const long long blocks = static_cast<long long>(tiles - sh.tile_begin) * (tile_rows / kFixRows);
     const size_t fsm = sizeof(float) * kFixRows * (bn / 32) * 36;  // <= 18 KB
@@ -697,8 +709,26 @@ int run_gemm_s(const Operand& A, const Operand& B, int M, int N, int K, int a_ro
   // MN-major B is staged in whole 128-B atoms per CTA
   const int step1 = BMN ? (ATOM > 32 ? ATOM : 32) : 32;
   const int step2 = BMN ? 2 * ATOM : 32;
-  const GemmChoice c = choose_gemm(M, N, k_iters, kBnSingle, kBnMax, step1, step2, kChunk == 0);
   static const int log_choice = env_int("FI_GEMM_LOG", 0);
+  // Transposed output (TR, see k_gemm): the weight table on the MMA's M side
+  // and the chart rows as the N tile.  FI_GEMM_TRANS=1 forces it where it
+  // applies (bf16 operands, K-major chart rows, not the weight gradients).
+  static const int use_tr = env_int("FI_GEMM_TRANS", 0);
+  if constexpr (!AMN && !SPLIT && kChunk == 0 && sizeof(T) == 2 && EPI != EPI_WGRAD) {
+    if (use_tr) {
+      const GemmChoice t = choose_gemm(N, M, k_iters, kBnSingle, kBnSingle, 32, 32, true);
+      if (log_choice)
+        fprintf(stderr, "[fi gemm] EPI=%d M=%d N=%d K=%d -> TR bn=%d pair=%d ksplit=%d tail=%d\n",
+                EPI, M, N, K, t.bn, static_cast<int>(t.pair), t.ksplit, t.tail);
+      if (t.bn == 0) return set_err(FI_ERR_ARG, "no transposed GEMM tile for M=%d", M);
+      if (t.pair)
+        return launch_gemm<T, kBnSingle, BMN, false, EPI, SPLIT, kChunk, true, false, true>(
+            B, A, N, M, K, a_row0, ep, st, t.bn, t.ksplit, t.tail);
+      return launch_gemm<T, kBnSingle, BMN, false, EPI, SPLIT, kChunk, false, false, true>(
+          B, A, N, M, K, a_row0, ep, st, t.bn, t.ksplit, t.tail);
+    }
+  }
+  const GemmChoice c = choose_gemm(M, N, k_iters, kBnSingle, kBnMax, step1, step2, kChunk == 0);
   if (log_choice)
     fprintf(stderr, "[fi gemm] EPI=%d M=%d N=%d K=%d -> bn=%d pair=%d ksplit=%d tail=%d\n", EPI, M,
             N, K, c.bn, static_cast<int>(c.pair), c.ksplit, c.tail);

@@ -47,6 +47,7 @@ enum EpiMode : int {
 struct GemmShape {
   int M, N, K;    // logical problem; rows >= M are masked in the epilogue
   int a_row0;     // K-major A: first row coordinate inside the tensor map
+  int b_row0;     // K-major B: first row coordinate (TR: the chart rows are the B operand)
   int num_m, num_n, num_k;  // tiles of (128 or 256 for pairs) x bn x BK
   int bn;         // N tile (runtime, <= the kernel's BN bound, multiple of 32)
   int stages;     // smem ring depth (runtime: as many as fit in shared memory)
@@ -353,8 +354,18 @@ constexpr int gemm_threads() { return 128 + 32 * gemm_epi_warps<CHUNK>(); }
 // 256 x 512 pair tile -- while keeping the double-buffered 2 x 256 TMEM
 // accumulator (epilogue overlapped with the next tile) and 256-column N
 // granularity.  A stage is released only when both pairs' MMAs consumed it.
+//
+// TR (transposed output): the launch computes C^T = B A^T -- the kernel's A
+// operand is the weight table (the MMA's M side: 128 / 256 W rows per
+// tile, output columns) and its B operand the chart rows (the MMA's N side,
+// N tile = any multiple of 32 up to 256, output rows).  Few chart rows then
+// need no re-read of the 64 MB weight table per row tile, and the N tile can
+// divide the row count exactly (the wave-quantisation fix of the library
+// GEMMs on these shapes).  The epilogue transposes each warp's 32 x 32
+// accumulator chunk through shared memory and runs the ordinary row
+// epilogue on the output rows.
 template <typename T, int BN, bool A_MN, bool B_MN, int EPI, bool SPLIT, int CHUNK, bool PAIR,
-          bool MC = false>
+          bool MC = false, bool TR = false>
 __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
@@ -364,6 +375,8 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
   constexpr int CL = MC ? 4 : NCTA;  // CTAs per cluster
   static_assert(!MC || (PAIR && !A_MN && !SPLIT && CHUNK == 0 && BN <= 256),
                 "multicast clusters: bf16/tf32 K-major A, double-buffered pair tiles");
+  static_assert(!TR || (!B_MN && !SPLIT && CHUNK == 0 && BN <= 256 && !MC),
+                "transposed output: K-major chart rows as B, double-buffered tiles");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -380,6 +393,8 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
   uint64_t* tfull = empty + NS;
   uint64_t* tempty = tfull + 2;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  // TR: one 32 x 33 transpose tile per epilogue warp, behind the 256-B barrier block
+  float* tbuf = reinterpret_cast<float*>(smB + NS * sh.b_stage + 256);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -475,7 +490,7 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
           };
           auto load_b = [&](uint8_t* dst, const CUtensorMap* mb) {
             if constexpr (!B_MN) {
-              load(dst, mb, kb * C::BK, n0);
+              load(dst, mb, kb * C::BK, sh.b_row0 + n0);
             } else {
               for (int j = 0; j < bn_cta / C::ATOM; ++j)
                 load(dst + j * C::BK * 128, mb, n0 + j * C::ATOM, kb * C::BK);
@@ -616,7 +631,8 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
       int m_blk, n_blk;
       tile_mn(tile, m_blk, n_blk);
       const int lrow = m_blk * (C::BM * NCTA) + rank * C::BM + r;  // row within this GEMM
-      const EpiRow er = epi_row<EPI>(ep, lrow);
+      // (TR: rows are output columns; the row epilogue runs after the transpose)
+      const EpiRow er = TR ? EpiRow{} : epi_row<EPI>(ep, lrow);
       const int col_base = n_blk * bn;
       // tile column of TMEM column chunk j: with two sub-tiles in a pair, each
       // CTA stages B rows [0, 128) of sub-tile 0 then the rest of its half,
@@ -640,7 +656,22 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
             dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
           return;
         }
-        epi_emit<EPI>(ep, er, col_base + tc, sh.N, v);
+        if constexpr (TR) {  // v = 32 output rows of output column lrow: transpose
+          float* tw = tbuf + (warp - 4) * (32 * 33);
+#pragma unroll
+          for (int q = 0; q < 32; ++q) tw[lane * 33 + q] = v[q];
+          __syncwarp();
+          float w[32];
+#pragma unroll
+          for (int q = 0; q < 32; ++q) w[q] = tw[q * 33 + lane];
+          __syncwarp();
+          const int orow = col_base + tc + lane;                         // output row
+          const int ocol = m_blk * (C::BM * NCTA) + rank * C::BM + quad * 32;  // first column
+          const EpiRow ert = epi_row<EPI>(ep, orow);
+          epi_emit<EPI>(ep, ert, ocol, sh.M, w);
+        } else {
+          epi_emit<EPI>(ep, er, col_base + tc, sh.N, v);
+        }
       };
       const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
       if constexpr (CHUNK == 0) {
@@ -810,6 +841,42 @@ __global__ void __launch_bounds__(256) k_gemm_fixup(const float* __restrict__ pa
     }
     const EpiRow er = epi_row<EPI>(ep, lrow);
     epi_emit<EPI>(ep, er, col, N, v);
+  }
+}
+
+// Split-K fixup of a TR launch: the partial tiles are in kernel layout
+// (W rows x chart rows); one CTA per (tile, 32 kernel rows) sums them in
+// part order into shared memory and each thread then emits one output row
+// (a kernel column) for those 32 output columns.
+template <int EPI>
+__global__ void __launch_bounds__(256) k_gemm_fixup_tr(const float* __restrict__ part, int ksplit,
+                                                       int M, int N, int num_m, int tile_rows,
+                                                       int bn, int tile_begin, int num_tiles,
+                                                       GemmEpi ep) {
+  pdl_wait();
+  extern __shared__ __align__(16) float fix_sm[];  // 32 x (bn + 1)
+  const int blocks_per_tile = tile_rows / 32;
+  const int tile = tile_begin + static_cast<int>(blockIdx.x) / blocks_per_tile;
+  const int r0 = (static_cast<int>(blockIdx.x) % blocks_per_tile) * 32;
+  const long long tsplit = num_tiles - tile_begin;
+  const int krow0 = (tile % num_m) * tile_rows + r0;   // kernel row = output column
+  const int kcol0 = (tile / num_m) * bn;               // kernel column = output row
+  const long long pstride = tsplit * tile_rows * static_cast<long long>(bn);
+  const float* src = part + ((tile - tile_begin) * static_cast<long long>(tile_rows) + r0) * bn;
+  for (int i = threadIdx.x; i < 32 * bn; i += blockDim.x) {
+    float acc = __ldcg(src + i);
+    for (int k = 1; k < ksplit; ++k) acc += __ldcg(src + k * pstride + i);
+    fix_sm[(i / bn) * (bn + 1) + i % bn] = acc;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < bn; t += blockDim.x) {
+    const int orow = kcol0 + t;
+    if (orow >= ep.M || krow0 >= M) continue;
+    float v[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) v[q] = fix_sm[q * (bn + 1) + t];
+    const EpiRow er = epi_row<EPI>(ep, orow);
+    epi_emit<EPI>(ep, er, krow0, M, v);
   }
 }
 

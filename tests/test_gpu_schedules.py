@@ -48,6 +48,10 @@ print(json.dumps(out))
      "FI_GEMM_NOTAIL": "1"},
     {"FI_GEMM_MC": "1", "FI_GEMM_PAIR": "1", "FI_GEMM_BN": "128", "FI_GEMM_KSPLIT": "1",
      "FI_GEMM_NOTAIL": "1"},
+    # transposed-output GEMMs (weight table on the MMA's M side) for fwd / dgrad / dunary
+    {"FI_GEMM_TRANS": "1"},
+    {"FI_GEMM_TRANS": "1", "FI_GEMM_KSPLIT": "3", "FI_GEMM_PAIR": "0"},
+    {"FI_GEMM_TRANS": "1", "FI_GEMM_KSPLIT": "2", "FI_GEMM_PAIR": "1", "FI_GEMM_BN": "128"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_schedule_matches_oracle(env):
     res = subprocess.run([sys.executable, "-c", CHILD], cwd=ROOT, capture_output=True, text=True,
