@@ -17,7 +17,9 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 python scripts/pick_launches.py ${O}_launches.csv 20 40 > ${O}_pick20.txt
 python scripts/pick_launches.py ${O}_launches.csv 10 40 > ${O}_pick10.txt
 cat ${O}_pick20.txt ${O}_pick10.txt
-cap() { timeout 900 ncu --set full --clock-control none --import-source on -s $2 -c 1 -o ${O}_prof_$1 $P > /dev/null 2>&1; echo "ncu $1 rc=$?"; }
+mkdir -p /tmp/ncu
+cap() { timeout 900 ncu --set full --clock-control none --import-source on -s $2 -c 1 -o /tmp/ncu/prof_$1 $P > /dev/null 2>&1; echo "ncu $1 rc=$?";
+        ncu -i /tmp/ncu/prof_$1.ncu-rep --page details --csv > ${O}_prof_$1_details.csv 2>/dev/null; }
 cap split $(awk '$1=="split"{print $2}' ${O}_pick20.txt)
 cap gather $(awk '$1=="gather"{print $2}' ${O}_pick20.txt)
 cap gemm_fwd $(awk '$1=="gemm_fwd"{print $2}' ${O}_pick10.txt)
@@ -36,4 +38,7 @@ print(next(k[0] for k in seq if k[0] >= half and "k_gemm<" in k[1] and ", 1, 1, 
 PY
 )
 cap gemm_wgrad $W
+python scripts/summarize_profiles.py --tag r02 --launches ${O}_launches.csv --reps /tmp/ncu/prof_*.ncu-rep \
+  --split-width 20 --gather-width 20 --gemm-width 10 > ${O}_summary.log 2>&1; tail -3 ${O}_summary.log
+cp profiles/r02_launches_summary.md profiles/r02_ncu_kernels.json profiles/ncu_traffic.json gpurun_out/ 2>/dev/null
 du -sh gpurun_out
