@@ -194,7 +194,8 @@ def run_e2e(args, g, tokens, dpi, lengths, gvec, dev, batch, n, world, barrier):
     log_z and the GrammarGrad tables (dL, dR, droot, d_emit) back to pinned
     host memory.  Copies run on their own streams, double-buffered, so step
     k+1's H2D and step k's D2H overlap step k's compute -- what a training
-    loop feeding the op does.  The timer covers all copies of all K steps
+    loop feeding the op does (dp.HostStreamedStep: the device part of a step
+    is one CUDA-graph replay).  The timer covers all copies of all K steps
     (final sync included)."""
     import torch
     import torch.distributed as dist
@@ -216,49 +217,13 @@ def run_e2e(args, g, tokens, dpi, lengths, gvec, dev, batch, n, world, barrier):
             for _ in range(2)]
     h2d = sum(t.numel() * t.element_size() for t in hosts[0].values())
     d2h = sum(t.numel() * t.element_size() for t in outs[0])
-    comp = torch.cuda.current_stream(dev)
-    s_in = torch.cuda.Stream(dev)
-    s_out = torch.cuda.Stream(dev)
-
-    def upload(k):
-        h = hosts[k % 2]
-        ev = torch.cuda.Event()
-        with torch.cuda.stream(s_in):
-            d = {key: t.to(dev, non_blocking=True) for key, t in h.items()}
-            ev.record(s_in)
-        for t in d.values():
-            t.record_stream(comp)
-        return d, ev
-
-    out_free = [None, None]  # D2H of the output slot finished (events on s_out)
+    from paper_2310_14997_b200.dp import HostStreamedStep
+    hs = HostStreamedStep(dpi, VOCAB, lengths, gvec)   # one CUDA graph per buffer slot
 
     def run(nsteps):
-        nxt = upload(0)
         for k in range(nsteps):
-            d, ev = nxt
-            comp.wait_event(ev)
-            if k + 1 < nsteps:
-                nxt = upload(k + 1)
-            un = d["emit"].t()[d["tok"]].contiguous()
-            if out_free[k % 2] is not None:   # step k-2's D2H of this slot is done
-                comp.wait_event(out_free[k % 2])
-            log_z, dL, dR, droot, dun = dpi.step(d["L"], d["R"], d["root"], un, lengths, gvec,
-                                                 slot=k % 2)
-            d_emit = torch.zeros(VOCAB, n, device=dev).index_add_(
-                0, d["tok"].view(-1), dun.reshape(-1, n))          # inside.py:420-423
-            res = (dL, dR, droot, d_emit.t(), log_z)
-            done = torch.cuda.Event()
-            done.record(comp)
-            s_out.wait_event(done)
-            with torch.cuda.stream(s_out):
-                for dst, src in zip(outs[k % 2], res):
-                    dst.copy_(src, non_blocking=True)
-            out_free[k % 2] = torch.cuda.Event()
-            out_free[k % 2].record(s_out)
-            for t in res:
-                t.record_stream(s_out)
-        s_out.synchronize()
-        comp.synchronize()
+            hs.step(k, hosts[k % 2], outs[k % 2])
+        hs.synchronize()
 
     run(max(2, args.warmup))
     barrier()
@@ -272,10 +237,11 @@ def run_e2e(args, g, tokens, dpi, lengths, gvec, dev, batch, n, world, barrier):
         ems = float(t.item())
     return {"value": world * batch / (ems / 1e3), "unit": "sentences/s", "ms_per_step": ems,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "path": "pinned host grammar+tokens -> H2D -> engine fwd+bwd (dp.DataParallelInside: "
-                    "C-ABI fi_inside_forward / fi_inside_backward_ex, + all-reduce at N>1) -> "
-                    "D2H log_z + GrammarGrad (dL, dR, droot, d_emit); copies on side streams, "
-                    "double-buffered across steps; wall clock over K steps"}
+            "path": "pinned host grammar+tokens -> H2D -> dp.HostStreamedStep: one CUDA-graph "
+                    "replay of unary gather + engine fwd+bwd (C-ABI fi_inside_forward / "
+                    "fi_inside_backward_ex, + all-reduce at N>1) + d_emit scatter -> D2H log_z + "
+                    "GrammarGrad (dL, dR, droot, d_emit); copies on side streams, double-buffered "
+                    "across steps; wall clock over K steps"}
 
 
 def tensor_peak(gemm_dtype: str, peaks: dict) -> tuple[float, str]:

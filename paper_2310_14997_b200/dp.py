@@ -146,3 +146,94 @@ class DataParallelInside:
                 dist.all_reduce(o["tail"], group=self.group)    # [dR | droot]
             cur.wait_stream(self.comm)
         return o["log_z"], o["dL"], o["dR"], o["droot"], o["dunary"]
+
+
+class HostStreamedStep:
+    """The op's step fed from host memory, the way a training loop calls it:
+    every step brings new grammar tables and tokens from pinned host buffers
+    and takes log Z and the GrammarGrad tables (dL, dR, droot, d_emit) back.
+
+    The device part -- unary gather, ``DataParallelInside.step`` (engine
+    fwd + bwd, all-reduce at N > 1) and the d_emit scatter
+    (inside.py:420-423) -- is captured once per buffer slot as a CUDA graph
+    over static device inputs; a step is then H2D (side stream) -> one
+    graph replay -> D2H (side stream).  Two slots alternate, so step k+1's
+    copies in and step k's copies out overlap the compute.  ``step`` only
+    enqueues; ``synchronize`` waits for every copy."""
+
+    def __init__(self, dpi: DataParallelInside, vocab: int, lengths, grad_log_z):
+        self.dpi = dpi
+        dev = dpi.device
+        s = dpi.shape
+        n, p, b, l = s.n_nt, s.n_pt, s.batch, s.max_len
+        self.n_pt = p
+        self.lengths, self.gvec = lengths, grad_log_z
+        self.comp = torch.cuda.current_stream(dev)
+        self.s_in = torch.cuda.Stream(dev)
+        self.s_out = torch.cuda.Stream(dev)
+        nslot = len(dpi.slots)
+        self.inputs = [dict(L=torch.empty(n, n + p, device=dev), R=torch.empty(n, n + p, device=dev),
+                            root=torch.empty(n, device=dev), emit=torch.empty(p, vocab, device=dev),
+                            tok=torch.zeros(b, l, dtype=torch.int64, device=dev))
+                       for _ in range(nslot)]
+        self.in_ready = [torch.cuda.Event() for _ in range(nslot)]
+        self.in_free = [None] * nslot
+        self.out_ready = [torch.cuda.Event() for _ in range(nslot)]
+        self.out_free = [None] * nslot
+        self.outputs = [None] * nslot
+        self.graphs = [self._capture(k) for k in range(nslot)]
+
+    def _device_step(self, k):
+        d = self.inputs[k]
+        un = d["emit"].t()[d["tok"]].contiguous()                   # inside.py:296-298
+        log_z, dL, dR, droot, dun = self.dpi.step(d["L"], d["R"], d["root"], un, self.lengths,
+                                                  self.gvec, slot=k)
+        d_emit = torch.zeros(d["emit"].shape[1], self.n_pt, device=un.device).index_add_(
+            0, d["tok"].view(-1), dun.reshape(-1, self.n_pt))        # inside.py:420-423
+        return dL, dR, droot, d_emit.t(), log_z
+
+    def _capture(self, k):
+        side = torch.cuda.Stream(self.dpi.device)
+        side.wait_stream(self.comp)
+        with torch.cuda.stream(side):
+            for _ in range(2):
+                self._device_step(k)
+        self.comp.wait_stream(side)
+        if self.dpi.world > 1 and dist.get_backend(self.dpi.group) != "nccl":
+            return None  # gloo collectives cannot be captured: eager replays
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            self.outputs[k] = self._device_step(k)
+        return graph
+
+    def step(self, k: int, host_in: dict, host_out: list):
+        """Enqueue step k: host_in (pinned L, R, root, emit, tok) -> slot k % 2 ->
+        host_out (pinned dL, dR, droot, d_emit, log_z)."""
+        j = k % len(self.graphs)
+        d = self.inputs[j]
+        with torch.cuda.stream(self.s_in):
+            if self.in_free[j] is not None:       # step k-2 has consumed these buffers
+                self.s_in.wait_event(self.in_free[j])
+            for key, t in host_in.items():
+                d[key].copy_(t, non_blocking=True)
+            self.in_ready[j].record(self.s_in)
+        self.comp.wait_event(self.in_ready[j])
+        if self.out_free[j] is not None:          # step k-2's results are on the host
+            self.comp.wait_event(self.out_free[j])
+        if self.graphs[j] is not None:
+            self.graphs[j].replay()
+        else:
+            self.outputs[j] = self._device_step(j)
+        self.in_free[j] = torch.cuda.Event()
+        self.in_free[j].record(self.comp)
+        self.out_ready[j].record(self.comp)
+        with torch.cuda.stream(self.s_out):
+            self.s_out.wait_event(self.out_ready[j])
+            for dst, src in zip(host_out, self.outputs[j]):
+                dst.copy_(src, non_blocking=True)
+            self.out_free[j] = torch.cuda.Event()
+            self.out_free[j].record(self.s_out)
+
+    def synchronize(self):
+        self.s_out.synchronize()
+        self.comp.synchronize()

@@ -109,3 +109,40 @@ def test_two_ranks_sum_to_the_full_batch():
         for got, want in ((dL, full[1]), (dR, full[2]), (droot, full[3])):
             np.testing.assert_allclose(got, want, rtol=1e-5, atol=1e-7 * np.abs(want).max())
         np.testing.assert_allclose(dunary, full[4][idx], rtol=1e-6, atol=1e-9)
+
+
+def test_host_streamed_step_matches_eager_steps():
+    """dp.HostStreamedStep (H2D -> one graph replay -> D2H, two alternating
+    slots) returns, for each step's own host inputs, what eager
+    DataParallelInside steps return for them."""
+    from paper_2310_14997_b200.dp import HostStreamedStep
+    root, left, right, emit = O.random_grammar_arrays(N, P, V, seed=2)
+    lengths = torch.tensor([12, 11, 12, 7, 12, 2, 9, 12], dtype=torch.int32, device="cuda")
+    g = torch.full((B,), -1.0 / B, device="cuda")
+    rng = np.random.default_rng(9)
+    hosts = []
+    for k in range(3):
+        j = np.float32(0.01 * k)
+        hosts.append(dict(L=torch.tensor(left + j, dtype=torch.float32).pin_memory(),
+                          R=torch.tensor(right - j, dtype=torch.float32).pin_memory(),
+                          root=torch.tensor(root, dtype=torch.float32).pin_memory(),
+                          emit=torch.tensor(emit, dtype=torch.float32).pin_memory(),
+                          tok=torch.as_tensor(rng.integers(0, V, (B, L_))).pin_memory()))
+    outs = [[torch.empty(N, N + P).pin_memory(), torch.empty(N, N + P).pin_memory(),
+             torch.empty(N).pin_memory(), torch.empty(P, V).pin_memory(),
+             torch.empty(B).pin_memory()] for _ in range(3)]
+    dpi = DataParallelInside(N, P, B, L_, "fp32", device="cuda", slots=2)
+    hs = HostStreamedStep(dpi, V, lengths, g)
+    for k in range(3):
+        hs.step(k, hosts[k], outs[k])
+    hs.synchronize()
+    ref = DataParallelInside(N, P, B, L_, "fp32", device="cuda")
+    for k in range(3):
+        h = {key: t.cuda() for key, t in hosts[k].items()}
+        un = h["emit"].t()[h["tok"]].contiguous()
+        log_z, dL, dR, droot, dun = ref.step(h["L"], h["R"], h["root"], un, lengths, g)
+        d_emit = torch.zeros(V, P, device="cuda").index_add_(0, h["tok"].view(-1),
+                                                             dun.reshape(-1, P)).t()
+        for got, want, name in zip(outs[k], (dL, dR, droot, d_emit, log_z),
+                                   ("dL", "dR", "droot", "d_emit", "log_z")):
+            assert torch.equal(got, want.cpu()), f"step {k} {name}"
