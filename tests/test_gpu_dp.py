@@ -145,4 +145,7 @@ def test_host_streamed_step_matches_eager_steps():
                                                              dun.reshape(-1, P)).t()
         for got, want, name in zip(outs[k], (dL, dR, droot, d_emit, log_z),
                                    ("dL", "dR", "droot", "d_emit", "log_z")):
-            assert torch.equal(got, want.cpu()), f"step {k} {name}"
+            if name == "d_emit":   # index_add_ accumulates with atomics: order-dependent
+                torch.testing.assert_close(got, want.cpu(), rtol=1e-5, atol=1e-7)
+            else:
+                assert torch.equal(got, want.cpu()), f"step {k} {name}"
