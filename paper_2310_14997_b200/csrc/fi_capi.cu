@@ -1119,6 +1119,41 @@ int backward_impl(const Plan& p, const float* L, const float* R, const float* ro
                                        : dc.cols_per_cta * 4;
     const size_t smem = align128(sizeof(GatherTerm) * p.l) +
                         static_cast<size_t>(stages) * (dc.cols_per_cta * sizeof(CT) + qb + 16);
+    // FI_GATHER_PERS=1: the persistent form when the launch has more (span,
+    // chunk) items than co-resident CTAs (2: always).  Off by default:
+    // measured 10-25% slower per launch at config 3 (4.52 vs 3.68 ms per
+    // step) -- each CTA stalls on its item's G-row epilogue loads while its
+    // ring sits full, where one-shot CTAs overlap each other.
+    static const int gpers = env_int("FI_GATHER_PERS", 0);
+    bool launched = false;
+    if (gpers) {
+      const size_t stage_bytes = dc.cols_per_cta * sizeof(CT) + qb;
+      const size_t psmem = static_cast<size_t>(stages) * (stage_bytes + 16) +
+                           align128(sizeof(float) * stages) + sizeof(GatherTerm) * p.l + 64;
+      const long long items = static_cast<long long>(nb) * n_m * dc.clusters;
+      FI_TRY(dispatch_v(dc.v, [&](auto vc) {
+        constexpr int V = decltype(vc)::value;
+        if constexpr (V > 4) {
+          return FI_OK;
+        } else {
+          auto kern = k_gather_bwd_pers<T, CT, V>;
+          FI_TRY(set_smem(kern, psmem));
+          int occ = 0;
+          FI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 + dc.threads, psmem));
+          const long long slots = static_cast<long long>(occ < 1 ? 1 : occ) * num_sms();
+          if (gpers < 2 && items <= slots) return FI_OK;  // one round: the one-shot kernel
+          static const int nprod = env_int("FI_GNPROD", 4);
+          FI_TRY(launch_ex(kern, 1, dim3(static_cast<unsigned>(items < slots ? items : slots)),
+                           dim3(32 + dc.threads), psmem, s, ga, stages, nprod, dc.clusters));
+          launched = true;
+          return FI_OK;
+        }
+      }));
+    }
+    if (launched) {
+      FI_CUDA(cudaGetLastError());
+      return FI_OK;
+    }
     FI_TRY(dispatch_v(dc.v, [&](auto vc) {
       constexpr int V = decltype(vc)::value;
       if constexpr (V > 4) {

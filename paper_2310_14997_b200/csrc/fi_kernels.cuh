@@ -1046,6 +1046,204 @@ __global__ void __launch_bounds__(288) k_gather_bwd_bulk(GatherArgs a, int stage
   }
 }
 
+// Persistent gather (the k_gather_bwd_bulk work, one CTA looping over
+// work items (span row, column chunk) blockIdx.x, blockIdx.x + gridDim.x,
+// ...).  As in k_split_fwd_pers: the producer warp builds an item's term
+// table (all 32 lanes), `nprod` lanes issue its sibling / parent copies into
+// the ring, each stage carrying the term's weight d, and goes straight on to
+// the next item while the consumers still accumulate -- so the ring does
+// not drain between items, and the per-CTA prologue (barrier init, term
+// table) is paid once per CTA instead of once per item.  Items outside a
+// sentence take no stage (both sides know it from the lengths).
+// ---------------------------------------------------------------------------
+template <typename T, typename CT, int V>
+__global__ void __launch_bounds__(288, 3) k_gather_bwd_pers(GatherArgs a, int stages, int nprod,
+                                                            int chunks) {
+  constexpr bool kHalf = sizeof(CT) == 2;
+  nprod = nprod < 1 ? 1 : (nprod > stages ? stages : (nprod > 32 ? 32 : nprod));
+  extern __shared__ __align__(128) uint8_t dsm[];
+  const int m = a.m;
+  const int n_m = a.lmax - m + 1;
+  const int items = a.nb * n_m * chunks;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ncons = blockDim.x - 32;
+  const int cpc = a.cols_per_cta;
+  const CT* Ach = static_cast<const CT*>(a.A);
+  const CT* Bch = static_cast<const CT*>(a.Bc);
+  const int sbytes = cpc * static_cast<int>(sizeof(CT));
+  const int qbytes = kHalf ? cpc * 2 : cpc * 4;
+  const int sxbytes = kHalf ? cpc / 8 : 0;
+  const int stage_bytes = sbytes + qbytes + sxbytes;
+  uint8_t* ring = dsm;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + static_cast<size_t>(stages) * stage_bytes);
+  uint64_t* empty = full + stages;
+  float* hdr = reinterpret_cast<float*>(empty + stages);            // term weight per stage
+  GatherTerm* ptab = reinterpret_cast<GatherTerm*>(
+      reinterpret_cast<uint8_t*>(hdr) + align128(sizeof(float) * stages));  // producer-private
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < stages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], ncons >> 5);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_wait();     // LQ / chart rows of the previous kernels visible from here
+  pdl_trigger();  // persistent: the next kernel may queue behind this one
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    long long g0 = 0;
+    for (int kk = blockIdx.x; kk < items; kk += gridDim.x) {
+      const int local = a.b0 * n_m + kk / chunks;
+      const int chunk0 = (kk % chunks) * cpc;
+      const int b = local / n_m, i = local % n_m;
+      const int len = a.lengths[b];
+      if (i + m > len) continue;  // dead span: no stages
+      const long long row = rowbase(m, a.B, a.lmax) + local;
+      const int n_left = len - i - m;
+      const int n_all = n_left + i;
+      const double xm = a.X[row] - (kHalf ? kChartScale : 0);
+      for (int t = lane; t < n_all; t += 32) {
+        long long rs, rp;
+        if (t < n_left) {  // left child (i, i+m) of parent (i, i+w): sibling b[w-m][i+m]
+          const int w = m + 1 + t;
+          rs = chart_row(w - m, b, i + m, a.B, a.lmax);
+          rp = chart_row(w, b, i, a.B, a.lmax);
+        } else {           // right child of parent (s, i+m): sibling a[i-s][s]
+          const int sidx = t - n_left;
+          rs = chart_row(i - sidx, b, sidx, a.B, a.lmax);
+          rp = chart_row(i + m - sidx, b, sidx, a.B, a.lmax);
+        }
+        ptab[t].rs = rs;
+        ptab[t].rp = rp;
+        ptab[t].d = static_cast<float>(xm + a.X[rs] - a.X[rp]);
+      }
+      __syncwarp();
+      // lanes issue in lockstep batches of nprod consecutive terms (nprod <=
+      // stages: a parity wait is never more than one phase behind)
+      for (int t0 = 0; t0 < n_all; t0 += nprod) {
+        const int t = t0 + lane;
+        if (lane < nprod && t < n_all) {
+          const long long gg = g0 + t;
+          const int st = static_cast<int>(gg % stages);
+          mbar_wait(&empty[st], static_cast<uint32_t>((gg / stages) & 1) ^ 1);
+          hdr[st] = ptab[t].d;
+          mbar_expect_tx(&full[st], static_cast<uint32_t>(stage_bytes));
+          uint8_t* dst = ring + static_cast<size_t>(st) * stage_bytes;
+          const CT* sib = t < n_left ? Bch : Ach;
+          bulk_g2s(dst, sib + ptab[t].rs * a.Np + chunk0, sbytes, &full[st]);
+          if constexpr (kHalf) {
+            bulk_g2s(dst + sbytes, static_cast<const __half*>(a.LQ) + ptab[t].rp * a.Np + chunk0,
+                     qbytes, &full[st]);
+            bulk_g2s(dst + sbytes + qbytes, a.LQS + ptab[t].rp * (a.Np / 32) + chunk0 / 32,
+                     sxbytes, &full[st]);
+          } else {
+            bulk_g2s(dst + sbytes, static_cast<const float*>(a.LQ) + ptab[t].rp * a.Np + chunk0,
+                     qbytes, &full[st]);
+          }
+        }
+        __syncwarp();
+      }
+      g0 += n_all;
+      __syncwarp();  // the term table is rewritten for the next item
+    }
+    return;
+  }
+  // -------------------------------------------------------------- consumers
+  const int ci = threadIdx.x - 32;
+  long long g0 = 0;
+  for (int kk = blockIdx.x; kk < items; kk += gridDim.x) {
+    const int local = a.b0 * n_m + kk / chunks;
+    const int chunk0 = (kk % chunks) * cpc;
+    const int b = local / n_m, i = local % n_m;
+    const int len = a.lengths[b];
+    const long long row = rowbase(m, a.B, a.lmax) + local;
+    const int col0 = chunk0 + ci * 4;
+    T* G = reinterpret_cast<T*>(a.G) + row * (2LL * a.Np);
+    if (i + m > len) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const int c = col0 + v * ncons * 4;
+        store4s<T>(G + c, a.g_lo, 0.f, 0.f, 0.f, 0.f);
+        store4s<T>(G + a.Np + c, a.g_lo, 0.f, 0.f, 0.f, 0.f);
+      }
+      continue;
+    }
+    const int n_left = len - i - m;
+    const int n_all = n_left + i;
+    float gl[4 * V], gr[4 * V];
+#pragma unroll
+    for (int k = 0; k < 4 * V; ++k) gl[k] = gr[k] = 0.f;
+    for (int t = 0; t < n_all; ++t) {
+      const long long gg = g0 + t;
+      const int st = static_cast<int>(gg % stages);
+      mbar_wait(&full[st], static_cast<uint32_t>((gg / stages) & 1));
+      const float d = hdr[st];
+      const uint8_t* stg = ring + static_cast<size_t>(st) * stage_bytes;
+      const CT* src = reinterpret_cast<const CT*>(stg) + ci * 4;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const float4 x = chart4<CT>(src + v * ncons * 4);
+        if constexpr (kHalf) {
+          // term = sib * q * 2^(d + s_chunk): one EX2 per 4 columns
+          const __half* qh = reinterpret_cast<const __half*>(stg + sbytes);
+          const float* sx = reinterpret_cast<const float*>(stg + sbytes + qbytes);
+          const int cl = ci * 4 + v * ncons * 4;  // column within the item's chunk
+          const float4 q = chart4<__half>(qh + cl);
+          const float f = ex2(d + sx[cl >> 5]);
+          // (explicit branches keep gl / gr in registers)
+          if (t < n_left) {
+            gl[4 * v + 0] = fmaf(x.x * q.x, f, gl[4 * v + 0]);
+            gl[4 * v + 1] = fmaf(x.y * q.y, f, gl[4 * v + 1]);
+            gl[4 * v + 2] = fmaf(x.z * q.z, f, gl[4 * v + 2]);
+            gl[4 * v + 3] = fmaf(x.w * q.w, f, gl[4 * v + 3]);
+          } else {
+            gr[4 * v + 0] = fmaf(x.x * q.x, f, gr[4 * v + 0]);
+            gr[4 * v + 1] = fmaf(x.y * q.y, f, gr[4 * v + 1]);
+            gr[4 * v + 2] = fmaf(x.z * q.z, f, gr[4 * v + 2]);
+            gr[4 * v + 3] = fmaf(x.w * q.w, f, gr[4 * v + 3]);
+          }
+        } else {
+          const float* srq = reinterpret_cast<const float*>(stg + sbytes) + ci * 4;
+          const float4 q = *reinterpret_cast<const float4*>(srq + v * ncons * 4);
+          if (t < n_left) {
+            gl[4 * v + 0] += ex2(x.x + q.x + d);
+            gl[4 * v + 1] += ex2(x.y + q.y + d);
+            gl[4 * v + 2] += ex2(x.z + q.z + d);
+            gl[4 * v + 3] += ex2(x.w + q.w + d);
+          } else {
+            gr[4 * v + 0] += ex2(x.x + q.x + d);
+            gr[4 * v + 1] += ex2(x.y + q.y + d);
+            gr[4 * v + 2] += ex2(x.z + q.z + d);
+            gr[4 * v + 3] += ex2(x.w + q.w + d);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    g0 += n_all;
+    // zero-mass projections carry no gradient (inside.py:441-443 NaN guard)
+    const float sg = a.g[b] < 0.f ? -1.f : 1.f;
+    const CT* pam = Ach + row * a.Np;
+    const CT* pbm = Bch + row * a.Np;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int c = col0 + v * ncons * 4;
+      const float4 am = chart4_ldg<CT>(pam + c), bm = chart4_ldg<CT>(pbm + c);
+      store4s<T>(G + c, a.g_lo, is_dead<CT>(am.x) ? 0.f : sg * gl[4 * v + 0],
+                 is_dead<CT>(am.y) ? 0.f : sg * gl[4 * v + 1],
+                 is_dead<CT>(am.z) ? 0.f : sg * gl[4 * v + 2],
+                 is_dead<CT>(am.w) ? 0.f : sg * gl[4 * v + 3]);
+      store4s<T>(G + a.Np + c, a.g_lo, is_dead<CT>(bm.x) ? 0.f : sg * gr[4 * v + 0],
+                 is_dead<CT>(bm.y) ? 0.f : sg * gr[4 * v + 1],
+                 is_dead<CT>(bm.z) ? 0.f : sg * gr[4 * v + 2],
+                 is_dead<CT>(bm.w) ? 0.f : sg * gr[4 * v + 3]);
+    }
+  }
+}
+
 // Span marginals mu_sym[w][i, A] = go / |g| = 2^(LQ^ + O^ - log2|g|)  (inside.py:425-430)
 template <bool kHalfLQ>
 __global__ void k_marginals(const void* __restrict__ LQv, const float* __restrict__ LQS,

@@ -43,6 +43,8 @@ print(json.dumps(out))
     {"FI_SPLIT_PERS": "0"},                       # one-shot split kernel at every width
     {"FI_SPLIT_PERS": "2"},                       # persistent split kernel at every width
     {"FI_PDL": "0"},
+    {"FI_GATHER_PERS": "0"},                      # one-shot gather at every width
+    {"FI_GATHER_PERS": "2"},                      # persistent gather at every width
     # multicast clusters (two CTA pairs sharing the A rows) for every eligible GEMM
     {"FI_GEMM_MC": "1", "FI_GEMM_PAIR": "1", "FI_GEMM_BN": "256", "FI_GEMM_KSPLIT": "1",
      "FI_GEMM_NOTAIL": "1"},
