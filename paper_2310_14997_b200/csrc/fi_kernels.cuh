@@ -462,9 +462,9 @@ __global__ void __launch_bounds__(288) k_split_fwd_bulk(SplitArgs a, int stages)
   for (int k = 0; k < 4 * V; ++k) S[k] = 0.f;
   if (warp == 0) {
     if (lane == 0) {  // producer: a[m][i] and b[w-m][i+m] chunks of every split
-      for (int t = 0; t < nsplit; ++t) {
-        const int s = t % stages;
-        const uint32_t ph = (t / stages) & 1;
+      int s = 0;
+      uint32_t ph = 0;  // ring position, advanced without integer division
+      for (int t = 0; t < nsplit; ++t, s = (s + 1 == stages) ? (ph ^= 1u, 0) : s + 1) {
         mbar_wait(&ring.empty[s], ph ^ 1);
         mbar_expect_tx(&ring.full[s], 2u * cbytes);
         uint8_t* dst = ring.buf + static_cast<size_t>(s) * ring.stage_bytes;
@@ -473,9 +473,9 @@ __global__ void __launch_bounds__(288) k_split_fwd_bulk(SplitArgs a, int stages)
       }
     }
   } else {
-    for (int t = 0; t < nsplit; ++t) {
-      const int s = t % stages;
-      const uint32_t ph = (t / stages) & 1;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int t = 0; t < nsplit; ++t, s = (s + 1 == stages) ? (ph ^= 1u, 0) : s + 1) {
       mbar_wait(&ring.full[s], ph);
       const float dl = kHalf ? terms[t].c : terms[t].d;
       const CT* src = reinterpret_cast<const CT*>(ring.buf + static_cast<size_t>(s) * ring.stage_bytes) + ci * 4;
@@ -637,7 +637,18 @@ __global__ void __launch_bounds__(288, 3) k_split_fwd_pers(SplitArgs a, int stag
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
-    long long g0 = 0;  // stages used before this row (identical count in the consumers)
+    // ring position of this row's first stage (the consumers walk the same
+    // sequence); lanes derive theirs with at most one wrap (nprod <= stages)
+    int rs = 0;
+    uint32_t rph = 0;
+    auto advance = [&](int by) {  // by >= 0; once per row / batch, not per term
+      rph ^= static_cast<uint32_t>((by / stages) & 1);
+      rs += by % stages;
+      if (rs >= stages) {
+        rs -= stages;
+        rph ^= 1u;
+      }
+    };
     for (int kk = blockIdx.x; kk < nrows; kk += gridDim.x) {
       const int local = a.b0 * n_w + kk;
       const int b = local / n_w, i = local % n_w;
@@ -658,13 +669,12 @@ __global__ void __launch_bounds__(288, 3) k_split_fwd_pers(SplitArgs a, int stag
       const double D = ub;
       if (dead) {
         if (lane == 0) {
-          const int s = static_cast<int>(g0 % stages);
-          mbar_wait(&empty[s], static_cast<uint32_t>((g0 / stages) & 1) ^ 1);
-          hdr[s].dead = 1;
-          hdr[s].D = D;
-          mbar_arrive(&full[s]);
+          mbar_wait(&empty[rs], rph ^ 1);
+          hdr[rs].dead = 1;
+          hdr[rs].D = D;
+          mbar_arrive(&full[rs]);
         }
-        g0 += 1;
+        advance(1);
       } else {
         // lanes issue in lockstep batches of nprod consecutive terms (nprod <=
         // stages): a parity wait on empty[] is then never more than one phase
@@ -672,9 +682,13 @@ __global__ void __launch_bounds__(288, 3) k_split_fwd_pers(SplitArgs a, int stag
         for (int t0 = 0; t0 < nsplit; t0 += nprod) {
           const int t = t0 + lane;
           if (lane < nprod && t < nsplit) {
-            const long long g = g0 + t;
-            const int s = static_cast<int>(g % stages);
-            mbar_wait(&empty[s], static_cast<uint32_t>((g / stages) & 1) ^ 1);
+            int s = rs + lane;
+            uint32_t ph = rph;
+            if (s >= stages) {
+              s -= stages;
+              ph ^= 1u;
+            }
+            mbar_wait(&empty[s], ph ^ 1);
             const int m = t + 1;
             const float d = static_cast<float>(ptab[t] - D);
             hdr[s].scal = kHalf ? exp2f(d - 2.f * kChartScale) : d;
@@ -687,8 +701,8 @@ __global__ void __launch_bounds__(288, 3) k_split_fwd_pers(SplitArgs a, int stag
                      &full[s]);
           }
           __syncwarp();
+          advance(nsplit - t0 < nprod ? nsplit - t0 : nprod);
         }
-        g0 += nsplit;
       }
       __syncwarp();  // the term table is rewritten for the next row
     }
@@ -697,15 +711,21 @@ __global__ void __launch_bounds__(288, 3) k_split_fwd_pers(SplitArgs a, int stag
   // -------------------------------------------------------------- consumers
   const int ci = threadIdx.x - 32;
   const int col0 = ci * 4;
-  long long g0 = 0;
+  int s = 0;
+  uint32_t ph = 0;  // ring position (same sequence as the producer's), no integer division
+  auto advance = [&]() {
+    if (++s == stages) {
+      s = 0;
+      ph ^= 1u;
+    }
+  };
   for (int kk = blockIdx.x; kk < nrows; kk += gridDim.x) {
-      const int local = a.b0 * n_w + kk;
+    const int local = a.b0 * n_w + kk;
     const int b = local / n_w, i = local % n_w;
     const int len = a.lengths[b];
     const long long row = rowbase(w, a.B, a.lmax) + local;
     // first stage: D, or the dead marker
-    int s = static_cast<int>(g0 % stages);
-    mbar_wait(&full[s], static_cast<uint32_t>((g0 / stages) & 1));
+    mbar_wait(&full[s], ph);
     const double D = hdr[s].D;
     if (hdr[s].dead) {
       __syncwarp();
@@ -718,16 +738,14 @@ __global__ void __launch_bounds__(288, 3) k_split_fwd_pers(SplitArgs a, int stag
         if (E) store4s<T>(E + row * a.Np + c, a.e_lo, 0.f, 0.f, 0.f, 0.f);
       }
       if (ci == 0) a.X[row] = D;
-      g0 += 1;
+      advance();
       continue;
     }
     float S[4 * V];
 #pragma unroll
     for (int k = 0; k < 4 * V; ++k) S[k] = 0.f;
     for (int t = 0; t < nsplit; ++t) {
-      const long long g = g0 + t;
-      s = static_cast<int>(g % stages);
-      if (t) mbar_wait(&full[s], static_cast<uint32_t>((g / stages) & 1));
+      if (t) mbar_wait(&full[s], ph);
       const float dl = hdr[s].scal;
       const CT* src = reinterpret_cast<const CT*>(ring + static_cast<size_t>(s) * stage_bytes) + col0;
 #pragma unroll
@@ -748,8 +766,8 @@ __global__ void __launch_bounds__(288, 3) k_split_fwd_pers(SplitArgs a, int stag
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      advance();
     }
-    g0 += nsplit;
     float o[4 * V];  // o - D
     float mx = kNegInf;
 #pragma unroll
@@ -953,11 +971,17 @@ __global__ void __launch_bounds__(288) k_gather_bwd_bulk(GatherArgs a, int stage
     // stages, so a parity wait is never more than one phase behind): a CTA
     // keeps more bulk copies in flight than one issuing thread can
     const unsigned imask = (1u << nprod) - 1u;
+    int bs = 0;
+    uint32_t bph = 0;  // ring position of the batch's first term (no per-term division)
     for (int t0 = 0; t0 < n_all && lane < nprod; t0 += nprod) {
       const int t = t0 + lane;
       if (t < n_all) {
-        const int s = t % stages;
-        const uint32_t ph = (t / stages) & 1;
+        int s = bs + lane;
+        uint32_t ph = bph;
+        if (s >= stages) {  // at most one wrap: nprod <= stages
+          s -= stages;
+          ph ^= 1u;
+        }
         mbar_wait(&ring.empty[s], ph ^ 1);
         mbar_expect_tx(&ring.full[s], static_cast<uint32_t>(ring.stage_bytes));
         uint8_t* dst = ring.buf + static_cast<size_t>(s) * ring.stage_bytes;
@@ -975,11 +999,16 @@ __global__ void __launch_bounds__(288) k_gather_bwd_bulk(GatherArgs a, int stage
         }
       }
       __syncwarp(imask);
+      bs += nprod;
+      if (bs >= stages) {
+        bs -= stages;
+        bph ^= 1u;
+      }
     }
   } else {
-    for (int t = 0; t < n_all; ++t) {
-      const int s = t % stages;
-      const uint32_t ph = (t / stages) & 1;
+    int s = 0;
+    uint32_t ph = 0;  // ring position, advanced without integer division
+    for (int t = 0; t < n_all; ++t, s = (s + 1 == stages) ? (ph ^= 1u, 0) : s + 1) {
       mbar_wait(&ring.full[s], ph);
       const float d = gterms[t].d;
       const uint8_t* stg = ring.buf + static_cast<size_t>(s) * ring.stage_bytes;
