@@ -542,8 +542,8 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
         const int k0 = k_iters * kpart / ks, k1 = k_iters * (kpart + 1) / ks;
         const int cl = CHUNK > 0 ? CHUNK : k1 - k0;
         uint32_t d_tmem = tmem_base;
-        for (int kb = k0; kb < k1; ++kb) {
-          const int kc = (kb - k0) % cl;
+        int kc = 0;  // K iteration within the accumulator chunk (no per-iteration division)
+        for (int kb = k0; kb < k1; ++kb, kc = (kc + 1 == cl) ? 0 : kc + 1) {
           if (kc == 0) {  // start a chunk in a drained accumulator
             mbar_wait(&tempty[acc], acc_phase ^ 1);
             tc_fence_after();
