@@ -518,8 +518,11 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {
       // ------------------------------------------------ MMA issuer (leader)
+      // The whole warp runs the loop (waits, bookkeeping, descriptor math:
+      // warp-uniform values the compiler keeps in uniform registers); one
+      // elected lane issues the MMAs and commits.
       // N tiles above 256 are two MMAs per K step (sub-tiles of 256 + the rest)
       const uint32_t idesc0 = make_idesc<C::TF32>(bn > 256 ? 256 : bn, A_MN, B_MN, C::BM * NCTA);
       const uint32_t idesc1 = make_idesc<C::TF32>(bn > 256 ? bn - 256 : 64, A_MN, B_MN, C::BM * NCTA);
@@ -557,7 +560,14 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
             if constexpr (PAIR) umma2<C::TF32>(dt, ad, bd, id, accum);
             else umma<C::TF32>(dt, ad, bd, id, accum);
           };
-          if constexpr (SPLIT) {  // small (lo*hi + hi*lo) at +0, big (hi*hi) at +BN
+          // K step k of a stage: the start-address field (bits 0-13, 16-B units)
+          // advances by kstep / 16 -- no carry within a stage
+          const uint64_t ad0 = make_sdesc(a_base, a_lbo, a_sbo, a_lay);
+          const uint64_t bd0 = make_sdesc(b_base, b_lbo, b_sbo, b_lay);
+          const bool issuer = elect_one();
+          if (!issuer) {
+            // the other lanes only keep the bookkeeping in step
+          } else if constexpr (SPLIT) {  // small (lo*hi + hi*lo) at +0, big (hi*hi) at +BN
             const uint32_t b_lo = static_cast<uint32_t>(sh.b_stage / 2);
 #pragma unroll
             for (int k = 0; k < C::BK / C::UK; ++k) {
@@ -573,30 +583,37 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
           } else if constexpr (BN <= 256) {  // BN > 256 kernels run only N tiles above 256
 #pragma unroll
             for (int k = 0; k < C::BK / C::UK; ++k)
-              mma(d_tmem, make_sdesc(a_base + k * a_kstep, a_lbo, a_sbo, a_lay),
-                  make_sdesc(b_base + k * b_kstep, b_lbo, b_sbo, b_lay), idesc0,
+              mma(d_tmem, ad0 + static_cast<uint64_t>(k * (a_kstep >> 4)),
+                  bd0 + static_cast<uint64_t>(k * (b_kstep >> 4)), idesc0,
                   (kc | k) != 0 ? 1u : 0u);
           } else {
+            constexpr uint64_t kSubB = sub_b_off >> 4;
 #pragma unroll
             for (int k = 0; k < C::BK / C::UK; ++k) {
-              const uint64_t ad = make_sdesc(a_base + k * a_kstep, a_lbo, a_sbo, a_lay);
+              const uint64_t ad = ad0 + static_cast<uint64_t>(k * (a_kstep >> 4));
+              const uint64_t bd = bd0 + static_cast<uint64_t>(k * (b_kstep >> 4));
               const uint32_t accum = (kc | k) != 0 ? 1u : 0u;
-              mma(d_tmem, ad, make_sdesc(b_base + k * b_kstep, b_lbo, b_sbo, b_lay), idesc0, accum);
-              mma(d_tmem + 256u, ad,
-                  make_sdesc(b_base + sub_b_off + k * b_kstep, b_lbo, b_sbo, b_lay), idesc1, accum);
+              mma(d_tmem, ad, bd, idesc0, accum);
+              mma(d_tmem + 256u, ad, bd + kSubB, idesc1, accum);
             }
           }
-          if constexpr (MC) umma_commit2_mask(&empty[stage], 0xF);  // both pairs' stages
-          else if constexpr (PAIR) umma_commit2(&empty[stage]);
-          else umma_commit(&empty[stage]);
+          const bool chunk_end = kc == cl - 1 || kb == k1 - 1;
+          if (issuer) {
+            if constexpr (MC) umma_commit2_mask(&empty[stage], 0xF);  // both pairs' stages
+            else if constexpr (PAIR) umma_commit2(&empty[stage]);
+            else umma_commit(&empty[stage]);
+            if (chunk_end) {
+              if constexpr (MC) umma_commit2_mask(&tfull[acc], static_cast<uint16_t>(3u << lead));
+              else if constexpr (PAIR) umma_commit2(&tfull[acc]);
+              else umma_commit(&tfull[acc]);
+            }
+          }
+          __syncwarp();
           if (++stage == NS) {
             stage = 0;
             phase ^= 1;
           }
-          if (kc == cl - 1 || kb == k1 - 1) {
-            if constexpr (MC) umma_commit2_mask(&tfull[acc], static_cast<uint16_t>(3u << lead));
-            else if constexpr (PAIR) umma_commit2(&tfull[acc]);
-            else umma_commit(&tfull[acc]);
+          if (chunk_end) {
             if (++acc == nbuf) {
               acc = 0;
               acc_phase ^= 1;

@@ -279,6 +279,15 @@ __device__ __forceinline__ void umma_commit2(uint64_t* bar) {
       : "memory");
 }
 
+// One lane of a converged warp (elect.sync): the issuing lane of warp-wide loops.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // ------------------------------------------------------- UMMA descriptors
 // Shared-memory matrix descriptor (sm_100 "version 1").
 //   K-major  SWIZZLE_128B : rows of 128 B, 8-row groups SBO (1024 B) apart.
