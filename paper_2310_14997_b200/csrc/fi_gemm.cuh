@@ -659,7 +659,8 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
         if (!PAIR || BN <= 256) return c;
         const int sb = c >> 8, w = c & 255;
         const int hs = (sb ? bn - 256 : 256) / 2;
-        return (w / hs) * bn_cta + sb * 128 + w % hs;
+        const int q = w >= hs ? 1 : 0;  // w < 2 hs: the CTA half, without a division
+        return q * bn_cta + sb * 128 + (w - q * hs);
       };
       auto emit = [&](int j, const float (&v)[32]) {
         const int tc = tile_col(j);
