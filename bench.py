@@ -237,6 +237,7 @@ def run_e2e(args, g, tokens, dpi, lengths, gvec, dev, batch, n, world, barrier):
         ems = float(t.item())
     return {"value": world * batch / (ems / 1e3), "unit": "sentences/s", "ms_per_step": ems,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "graphs": all(gr is not None for gr in hs.graphs),
             "path": "pinned host grammar+tokens -> H2D -> dp.HostStreamedStep: one CUDA-graph "
                     "replay of unary gather + engine fwd+bwd (C-ABI fi_inside_forward / "
                     "fi_inside_backward_ex, + all-reduce at N>1) + d_emit scatter -> D2H log_z + "

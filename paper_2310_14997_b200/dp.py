@@ -181,6 +181,7 @@ class HostStreamedStep:
         self.out_ready = [torch.cuda.Event() for _ in range(nslot)]
         self.out_free = [None] * nslot
         self.outputs = [None] * nslot
+        self.capture_error = False
         self.graphs = [self._capture(k) for k in range(nslot)]
 
     def _device_step(self, k):
@@ -202,8 +203,13 @@ class HostStreamedStep:
         if self.dpi.world > 1 and dist.get_backend(self.dpi.group) != "nccl":
             return None  # gloo collectives cannot be captured: eager replays
         graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            self.outputs[k] = self._device_step(k)
+        try:
+            with torch.cuda.graph(graph):
+                self.outputs[k] = self._device_step(k)
+        except Exception:  # noqa: BLE001  (a collective that refuses capture: run eagerly)
+            torch.cuda.synchronize(self.dpi.device)
+            self.capture_error = True
+            return None
         return graph
 
     def step(self, k: int, host_in: dict, host_out: list):
