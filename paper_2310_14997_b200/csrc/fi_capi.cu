@@ -19,7 +19,10 @@
 #include <cstring>
 #include <atomic>
 #include <type_traits>
+#include <algorithm>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <vector>
 #include <cudaTypedefs.h>
 
@@ -42,6 +45,9 @@ thread_local char g_err[512] = "";
 // Process-wide count of kernels this library enqueued (autograd runs the
 // backward on its own thread, so nothing here is thread-local).
 std::atomic<long long> g_launches{0};
+// > 0 while this thread times GEMM tile candidates (see tuned_choice): those
+// launches are neither counted nor recorded by the profiler.
+thread_local int g_tuning = 0;
 
 // ---------------------------------------------------------------- profiler
 // Optional per-kernel-class CUDA-event timing (bench.py roofline): when
@@ -76,7 +82,7 @@ struct ProfScope {
   cudaStream_t st;
   ProfRec rec;
   bool on;
-  ProfScope(int cls, cudaStream_t s) : st(s), on(g_prof_on.load()) {
+  ProfScope(int cls, cudaStream_t s) : st(s), on(g_prof_on.load() && g_tuning == 0) {
     if (!on) return;
     std::lock_guard<std::mutex> lk(g_prof_mu);
     rec.cls = cls;
@@ -354,7 +360,7 @@ int launch_ex(K kern, int cluster, dim3 grid, dim3 block, size_t smem, cudaStrea
   cfg.attrs = attr;
   cfg.numAttrs = n;
   FI_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
-  ++g_launches;
+  if (g_tuning == 0) ++g_launches;
   return FI_OK;
 }
 
@@ -611,8 +617,14 @@ double gemm_t_pair(int bn) {
 // overlapped with the next tile's main loop: its cost per wave (model units).
 double gemm_epi_serial(int bn) { return bn > 256 ? 6.0 * bn / 512.0 : 0.0; }
 
+struct GemmCand {
+  double cost;
+  GemmChoice c;
+};
+
 GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int bn_max_pair,
-                       int step_single, int step_pair, bool allow_ksplit) {
+                       int step_single, int step_pair, bool allow_ksplit,
+                       std::vector<GemmCand>* all = nullptr) {
   static const int force_pair = gemm_env("FI_GEMM_PAIR", -1);
   static const int force_bn = gemm_env("FI_GEMM_BN", 0);
   static const int force_ks = gemm_env("FI_GEMM_KSPLIT", 0);  // 1: never split K
@@ -658,6 +670,7 @@ GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int bn_max_p
         return fix_us + 2.0 * ks * static_cast<double>(r) * tile_rows * bn * 4.0 / (fix_gbs * 1e3);
       };
       auto consider = [&](double cost, int ks, int tail) {
+        if (all) all->push_back({cost, {bn, pair != 0, ks, tail}});
         if (cost < best_cost * 0.995) {
           best_cost = cost;
           best = {bn, pair != 0, ks, tail};
@@ -688,6 +701,108 @@ GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int bn_max_p
     }
   }
   return best;
+}
+
+// ------------------------------------------------------ measured tile choice
+// The cost model above ranks tile shapes from whole-wave fits; per shape its
+// pick is within ~10% of the best, but which alternative wins (pair 256 x 512
+// with a split tail, 256 x 256 double-buffered, a narrower N tile on whole
+// waves ...) depends on the epilogue and on the box.  FI_GEMM_TUNE=1 (the
+// default) times the model's cheapest candidates (cost within 1.6x of the
+// best, at most 10) on the caller's stream the first time a (kernel, M, N, K)
+// is launched eagerly, and keeps the fastest for the life of the process.
+// Launches inside a CUDA-graph capture use the stored pick (or the model's
+// when the shape was never run eagerly).  Every GEMM epilogue is a pure
+// function of its operands, so re-running a launch while timing it is
+// harmless.  A forced tile (FI_GEMM_PAIR / BN / KSPLIT) disables tuning.
+bool same_choice(const GemmChoice& a, const GemmChoice& b) {
+  return a.bn == b.bn && a.pair == b.pair && a.ksplit == b.ksplit && a.tail == b.tail;
+}
+
+struct TuneKey {
+  int dev, sig;
+  long long M;
+  int N, K;
+  bool operator<(const TuneKey& o) const {
+    return std::tie(dev, sig, M, N, K) < std::tie(o.dev, o.sig, o.M, o.N, o.K);
+  }
+};
+std::mutex g_tune_mu;
+std::map<TuneKey, GemmChoice> g_tuned;
+
+bool gemm_tune_on() {
+  static const bool on = env_int("FI_GEMM_TUNE", 1) != 0 && !getenv("FI_GEMM_PAIR") &&
+                         !getenv("FI_GEMM_BN") && !getenv("FI_GEMM_KSPLIT");
+  return on;
+}
+
+struct TuningScope {
+  TuningScope() { ++g_tuning; }
+  ~TuningScope() { --g_tuning; }
+};
+
+// candidates timed per shape: model cost within kTuneSpan x the cheapest, at most kTuneMax
+static const double kTuneSpan = env_int("FI_GEMM_TUNE_SPAN_PCT", 160) / 100.0;
+static const int kTuneMax = env_int("FI_GEMM_TUNE_MAX", 10);
+
+template <typename L>
+int tuned_choice(const TuneKey& key, GemmChoice model, std::vector<GemmCand> cands,
+                 cudaStream_t st, L&& launch, GemmChoice* out) {
+  *out = model;
+  {
+    std::lock_guard<std::mutex> lk(g_tune_mu);
+    auto it = g_tuned.find(key);
+    if (it != g_tuned.end()) {
+      *out = it->second;
+      return FI_OK;
+    }
+  }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  FI_CUDA(cudaStreamIsCapturing(st, &cs));
+  if (cs != cudaStreamCaptureStatusNone) return FI_OK;  // never time inside a capture
+  // distinct candidates, cheapest first; the model's pick leads
+  std::stable_sort(cands.begin(), cands.end(),
+                   [](const GemmCand& a, const GemmCand& b) { return a.cost < b.cost; });
+  std::vector<GemmChoice> list{model};
+  const double limit = (cands.empty() ? 0.0 : cands.front().cost) * kTuneSpan;
+  for (const GemmCand& g : cands) {
+    if (static_cast<int>(list.size()) >= kTuneMax || g.cost > limit) break;
+    bool dup = false;
+    for (const GemmChoice& c : list) dup = dup || same_choice(c, g.c);
+    if (!dup) list.push_back(g.c);
+  }
+  GemmChoice best = model;
+  if (list.size() > 1) {
+    TuningScope mute;
+    cudaEvent_t e0, e1;
+    FI_CUDA(cudaEventCreate(&e0));
+    FI_CUDA(cudaEventCreate(&e1));
+    float best_ms = 1e30f;
+    int rc = FI_OK;
+    for (size_t i = 0; i < list.size() && rc == FI_OK; ++i) {
+      rc = launch(list[i]);  // warm (TMA descriptors, first-touch)
+      if (rc != FI_OK) break;
+      cudaEventRecord(e0, st);
+      for (int r = 0; r < 3 && rc == FI_OK; ++r) rc = launch(list[i]);
+      cudaEventRecord(e1, st);
+      if (rc != FI_OK || cudaEventSynchronize(e1) != cudaSuccess) break;
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      // an alternative has to beat the model's pick by 2% to replace it
+      if (ms < best_ms * (i == 0 ? 1.f : 0.98f)) {
+        best_ms = ms;
+        best = list[i];
+      }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (rc != FI_OK) return rc;
+    FI_CUDA(cudaGetLastError());
+  }
+  std::lock_guard<std::mutex> lk(g_tune_mu);
+  g_tuned[key] = best;
+  *out = best;
+  return FI_OK;
 }
 
 template <typename T, bool AMN, bool BMN, int EPI, bool SPLIT>
@@ -728,11 +843,33 @@ int run_gemm_s(const Operand& A, const Operand& B, int M, int N, int K, int a_ro
           B, A, N, M, K, a_row0, ep, st, t.bn, t.ksplit, t.tail);
     }
   }
-  const GemmChoice c = choose_gemm(M, N, k_iters, kBnSingle, kBnMax, step1, step2, kChunk == 0);
-  if (log_choice)
-    fprintf(stderr, "[fi gemm] EPI=%d M=%d N=%d K=%d -> bn=%d pair=%d ksplit=%d tail=%d\n", EPI, M,
-            N, K, c.bn, static_cast<int>(c.pair), c.ksplit, c.tail);
+  std::vector<GemmCand> cands;
+  const bool tune = gemm_tune_on();
+  GemmChoice c = choose_gemm(M, N, k_iters, kBnSingle, kBnMax, step1, step2, kChunk == 0,
+                             tune ? &cands : nullptr);
   if (c.bn == 0) return set_err(FI_ERR_ARG, "no GEMM tile for N=%d (FI_GEMM_BN?)", N);
+  auto launch = [&](const GemmChoice& ch) -> int {
+    if (ch.pair) {
+      if (ch.bn > kBnSingle)  // 256 x 512-class pair tiles: two MMAs per K step
+        return launch_gemm<T, kBnMax, AMN, BMN, EPI, SPLIT, kChunk, true>(
+            A, B, M, N, K, a_row0, ep, st, ch.bn, ch.ksplit, ch.tail);
+      return launch_gemm<T, kBnSingle, AMN, BMN, EPI, SPLIT, kChunk, true>(
+          A, B, M, N, K, a_row0, ep, st, ch.bn, ch.ksplit, ch.tail);
+    }
+    return launch_gemm<T, kBnSingle, AMN, BMN, EPI, SPLIT, kChunk, false>(
+        A, B, M, N, K, a_row0, ep, st, ch.bn, ch.ksplit, ch.tail);
+  };
+  const GemmChoice model = c;
+  if (tune) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int sig = (((EPI * 8 + static_cast<int>(sizeof(T))) * 2 + AMN) * 2 + BMN) * 2 + SPLIT;
+    FI_TRY(tuned_choice(TuneKey{dev, sig, M, N, K}, model, std::move(cands), st, launch, &c));
+  }
+  if (log_choice)
+    fprintf(stderr, "[fi gemm] EPI=%d M=%d N=%d K=%d -> bn=%d pair=%d ksplit=%d tail=%d%s\n", EPI,
+            M, N, K, c.bn, static_cast<int>(c.pair), c.ksplit, c.tail,
+            same_choice(c, model) ? "" : " (measured; model picked another)");
   // FI_GEMM_MC=1: pair tiles of N <= 256 run as multicast clusters of two
   // pairs (A rows shared, adjacent N tiles; see k_gemm) when eligible
   static const int use_mc = env_int("FI_GEMM_MC", 0);
@@ -741,15 +878,7 @@ int run_gemm_s(const Operand& A, const Operand& B, int M, int N, int K, int a_ro
       return launch_gemm<T, kBnSingle, AMN, BMN, EPI, SPLIT, kChunk, true, true>(
           A, B, M, N, K, a_row0, ep, st, c.bn, 1, 0);
   }
-  if (c.pair) {
-    if (c.bn > kBnSingle)  // 256 x 512-class pair tiles: two MMAs per K step
-      return launch_gemm<T, kBnMax, AMN, BMN, EPI, SPLIT, kChunk, true>(A, B, M, N, K, a_row0, ep,
-                                                                        st, c.bn, c.ksplit, c.tail);
-    return launch_gemm<T, kBnSingle, AMN, BMN, EPI, SPLIT, kChunk, true>(A, B, M, N, K, a_row0, ep,
-                                                                         st, c.bn, c.ksplit, c.tail);
-  }
-  return launch_gemm<T, kBnSingle, AMN, BMN, EPI, SPLIT, kChunk, false>(A, B, M, N, K, a_row0, ep,
-                                                                        st, c.bn, c.ksplit, c.tail);
+  return launch(c);
 }
 
 // Dispatch on the split (fp32 / bf16x3) mode; tf32 operands are never split.

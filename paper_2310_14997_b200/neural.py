@@ -389,7 +389,7 @@ class TrainStep:
             if bad.numel():  # this rank holds the sentence (else another rank does)
                 b = int(bad[0, 0])
                 raise TrainError(f"non-finite loss at step {step_no}: sentence {b} has log "
-                                 f"probability {float(log_z[b])}")
+                                 f"probability {float(log_z[b].detach())}")
             raise TrainError(f"non-finite loss at step {step_no} (on another rank)")
         if not grad_finite:
             raise ParamError("non-finite gradient")

@@ -9,6 +9,7 @@ import subprocess
 import sys
 from pathlib import Path
 
+import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
@@ -54,6 +55,8 @@ print(json.dumps(out))
     {"FI_GEMM_TRANS": "1"},
     {"FI_GEMM_TRANS": "1", "FI_GEMM_KSPLIT": "3", "FI_GEMM_PAIR": "0"},
     {"FI_GEMM_TRANS": "1", "FI_GEMM_KSPLIT": "2", "FI_GEMM_PAIR": "1", "FI_GEMM_BN": "128"},
+    {"FI_GEMM_TUNE": "0"},                        # the cost model's tile, never measured
+    {"FI_GEMM_TUNE_SPAN_PCT": "1000", "FI_GEMM_TUNE_MAX": "40"},  # time (run) many more tiles
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_schedule_matches_oracle(env):
     res = subprocess.run([sys.executable, "-c", CHILD], cwd=ROOT, capture_output=True, text=True,
@@ -63,3 +66,17 @@ def test_schedule_matches_oracle(env):
     for case, e in errs.items():
         for k, v in e.items():
             assert v < 2e-3, f"{env} {case} {k}: {v:.2e}"
+
+
+def test_measured_tile_choice_is_reused():
+    """The first eager launch of a GEMM shape times candidate tiles (FI_GEMM_TUNE,
+    on by default); later launches of the shape reuse the stored pick, so a
+    repeated call is bit-identical to the first."""
+    sys.path[:0] = [str(ROOT), str(ROOT / "tests")]
+    from test_gpu_parity import make_case, run_op
+    root, left, right, emit, unary, lens, _ = make_case(1024, 1024, 64, 6, 14, 11, None)
+    grad = -np.ones(6) / 6
+    first = run_op(root, left, right, unary, lens, grad, "bf16")
+    again = run_op(root, left, right, unary, lens, grad, "bf16")
+    for k in first:
+        assert np.array_equal(first[k], again[k]), k
