@@ -450,7 +450,8 @@ int max_clusters(K kern, int cl, int threads, size_t smem) {
 template <typename T, int BN, bool AMN, bool BMN, int EPI, bool SPLIT, int CHUNK, bool PAIR,
           bool MC = false, bool TR = false>
 int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_row0,
-                const GemmEpi& ep, cudaStream_t st, int bn, int ksplit, int tail) {
+                const GemmEpi& ep, cudaStream_t st, int bn, int ksplit, int tail,
+                bool streamk = false) {
   using Cf = GemmCfg<T, BN>;
   constexpr int NCTA = PAIR ? 2 : 1;
   constexpr int CL = MC ? 4 : NCTA;
@@ -499,6 +500,26 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
   sh.sem = nullptr;
   sh.tile_begin = 0;
   sh.tile_end = 0;
+  sh.sk = 0;
+  sh.sk_first = 0;
+
+  // persistent: one CTA (pair, cluster) per SM (pair, group of 4 SMs)
+  const int nslots = MC ? 0 : num_sms() / NCTA;
+  if (streamk && !MC && !TR && CHUNK == 0 && g_kpart.ptr && g_kpart.sem && tail > 0 &&
+      tail == tiles % nslots && tail <= kKPartSems &&
+      sh.stages * stage_bytes >= Cf::BM * (bn + 4) * 4 &&  // the finalizer's staging tile
+      static_cast<size_t>(2) * nslots * Cf::BM * NCTA * bn <= g_kpart.floats) {
+    // one launch: whole waves, then the last `tail` tiles' K iterations in
+    // equal runs over every slot, reduced in-kernel (see GemmShape::sk)
+    sh.sk = nslots;
+    sh.sk_first = tiles - tail;
+    sh.part = g_kpart.ptr;
+    sh.sem = g_kpart.sem;
+  }
+  if (streamk) {
+    tail = 0;
+    ksplit = 1;
+  }
   const long long tsplit = tail > 0 ? tail : tiles;
   if (ksplit > 1 && CHUNK == 0 && g_kpart.ptr &&
       static_cast<size_t>(ksplit) * tsplit * Cf::BM * NCTA * bn <= g_kpart.floats) {
@@ -529,12 +550,17 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
                        : num_sms() / NCTA;
   static const int log_slots = env_int("FI_GEMM_LOG", 0);
   if (log_slots && MC) fprintf(stderr, "[fi gemm] multicast clusters: %d co-resident\n", slots);
+  if (log_slots && PAIR && !MC)
+    fprintf(stderr, "[fi gemm] pair clusters: %d co-resident (smem %zu)\n",
+            max_clusters(kern, 2, gemm_threads<CHUNK>(), smem_bytes), smem_bytes);
   ProfScope prof(g_prof_class >= 0 ? g_prof_class
                  : EPI == EPI_FWD || EPI == EPI_FWD_H ? FI_PROF_GEMM_FWD
                  : EPI == EPI_WGRAD ? FI_PROF_GEMM_WGRAD
                  : EPI == EPI_STORE ? FI_PROF_PREP : FI_PROF_GEMM_DGRAD, st);  // DGRAD(_H), DUNARY
   auto go = [&](const GemmShape& g) -> int {
-    const int units = ((g.tile_end > 0 ? g.tile_end : tiles) - g.tile_begin) * g.ksplit;
+    // (stream-K: exactly one CTA per slot -- the runs are cut per slot)
+    const int units = g.sk > 0 ? g.sk
+                               : ((g.tile_end > 0 ? g.tile_end : tiles) - g.tile_begin) * g.ksplit;
     const int grid = (units < slots ? units : slots) * CL;
     if (grid <= 0) return FI_OK;
     if constexpr (PAIR) {
@@ -603,6 +629,7 @@ struct GemmChoice {
   bool pair;
   int ksplit;
   int tail;  // > 0: whole waves, then the last `tail` tiles split ksplit ways over K
+  bool sk = false;  // the `tail` tiles are run stream-K over every slot (ksplit 1)
 };
 
 double gemm_t_single(int bn) { return 0.77 + 0.23 * bn / 256.0; }
@@ -669,11 +696,11 @@ GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int bn_max_p
         if (inkernel_red) return 3.0 + 2.0 * 128 * bn * 4.0 / 60.0e3;
         return fix_us + 2.0 * ks * static_cast<double>(r) * tile_rows * bn * 4.0 / (fix_gbs * 1e3);
       };
-      auto consider = [&](double cost, int ks, int tail) {
-        if (all) all->push_back({cost, {bn, pair != 0, ks, tail}});
+      auto consider = [&](double cost, int ks, int tail, bool sk = false) {
+        if (all) all->push_back({cost, {bn, pair != 0, ks, tail, sk}});
         if (cost < best_cost * 0.995) {
           best_cost = cost;
-          best = {bn, pair != 0, ks, tail};
+          best = {bn, pair != 0, ks, tail, sk};
         }
       };
       // whole tiles, optionally all split over K (small M: fewer tiles than slots)
@@ -698,6 +725,24 @@ GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int bn_max_p
           consider(cost, ks, static_cast<int>(r));
         }
       }
+      // stream-K (one launch): whole waves, then the K iterations of the last
+      // r tiles (all T tiles below one wave) cut into equal runs over every
+      // slot; a tile's segments are summed in-kernel by the one that ends it.
+      // Kept to r >= slots / 12 (<= 13 segments per tile), partials that fit,
+      // and the double-buffered tiles (bn <= 256: the finalizer waits while
+      // holding its accumulator).
+      // FI_GEMM_STREAMK: 0 (default) never, 1 a candidate (cost model / tuner), 2 whenever it fits
+      static const int sk_env = gemm_env("FI_GEMM_STREAMK", 0);
+      if (sk_env != 0 && !no_tail && force_ks != 1 && allow_ksplit && r > 0 && r * 12 >= slots &&
+          bn <= 256 && r <= kKPartSems &&
+          2.0 * slots * tile_rows * bn <= static_cast<double>(g_kpart.floats)) {
+        const double per = static_cast<double>(r) * k_iters / slots;
+        const double segs = static_cast<double>(r + slots);
+        const double cost = static_cast<double>(T / slots) * (k_iters * t + gemm_epi_serial(bn)) +
+                            (per + 2.0) * t + gemm_epi_serial(bn) + 2.0 +
+                            2.0 * segs * tile_rows * bn * 4.0 / (fix_gbs * 1e3);
+        consider(sk_env == 2 ? cost * 0.01 : cost, 1, static_cast<int>(r), true);
+      }
     }
   }
   return best;
@@ -716,7 +761,8 @@ GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int bn_max_p
 // function of its operands, so re-running a launch while timing it is
 // harmless.  A forced tile (FI_GEMM_PAIR / BN / KSPLIT) disables tuning.
 bool same_choice(const GemmChoice& a, const GemmChoice& b) {
-  return a.bn == b.bn && a.pair == b.pair && a.ksplit == b.ksplit && a.tail == b.tail;
+  return a.bn == b.bn && a.pair == b.pair && a.ksplit == b.ksplit && a.tail == b.tail &&
+         a.sk == b.sk;
 }
 
 struct TuneKey {
@@ -788,6 +834,11 @@ int tuned_choice(const TuneKey& key, GemmChoice model, std::vector<GemmCand> can
       if (rc != FI_OK || cudaEventSynchronize(e1) != cudaSuccess) break;
       float ms = 0.f;
       cudaEventElapsedTime(&ms, e0, e1);
+      static const int log_tune = env_int("FI_GEMM_LOG", 0);
+      if (log_tune >= 2)
+        fprintf(stderr, "[fi tune] sig=%d M=%lld N=%d K=%d  bn=%d pair=%d ks=%d tail=%d%s: %.1f us\n",
+                key.sig, key.M, key.N, key.K, list[i].bn, static_cast<int>(list[i].pair),
+                list[i].ksplit, list[i].tail, list[i].sk ? " sk" : "", ms * 1e3f / 3.f);
       // an alternative has to beat the model's pick by 2% to replace it
       if (ms < best_ms * (i == 0 ? 1.f : 0.98f)) {
         best_ms = ms;
@@ -852,12 +903,12 @@ int run_gemm_s(const Operand& A, const Operand& B, int M, int N, int K, int a_ro
     if (ch.pair) {
       if (ch.bn > kBnSingle)  // 256 x 512-class pair tiles: two MMAs per K step
         return launch_gemm<T, kBnMax, AMN, BMN, EPI, SPLIT, kChunk, true>(
-            A, B, M, N, K, a_row0, ep, st, ch.bn, ch.ksplit, ch.tail);
+            A, B, M, N, K, a_row0, ep, st, ch.bn, ch.ksplit, ch.tail, ch.sk);
       return launch_gemm<T, kBnSingle, AMN, BMN, EPI, SPLIT, kChunk, true>(
-          A, B, M, N, K, a_row0, ep, st, ch.bn, ch.ksplit, ch.tail);
+          A, B, M, N, K, a_row0, ep, st, ch.bn, ch.ksplit, ch.tail, ch.sk);
     }
     return launch_gemm<T, kBnSingle, AMN, BMN, EPI, SPLIT, kChunk, false>(
-        A, B, M, N, K, a_row0, ep, st, ch.bn, ch.ksplit, ch.tail);
+        A, B, M, N, K, a_row0, ep, st, ch.bn, ch.ksplit, ch.tail, ch.sk);
   };
   const GemmChoice model = c;
   if (tune) {
@@ -867,8 +918,9 @@ int run_gemm_s(const Operand& A, const Operand& B, int M, int N, int K, int a_ro
     FI_TRY(tuned_choice(TuneKey{dev, sig, M, N, K}, model, std::move(cands), st, launch, &c));
   }
   if (log_choice)
-    fprintf(stderr, "[fi gemm] EPI=%d M=%d N=%d K=%d -> bn=%d pair=%d ksplit=%d tail=%d%s\n", EPI,
-            M, N, K, c.bn, static_cast<int>(c.pair), c.ksplit, c.tail,
+    fprintf(stderr, "[fi gemm] EPI=%d M=%d N=%d K=%d -> bn=%d pair=%d ksplit=%d tail=%d%s%s\n",
+            EPI, M, N, K, c.bn, static_cast<int>(c.pair), c.ksplit, c.tail,
+            c.sk ? " stream-K" : "",
             same_choice(c, model) ? "" : " (measured; model picked another)");
   // FI_GEMM_MC=1: pair tiles of N <= 256 run as multicast clusters of two
   // pairs (A rows shared, adjacent N tiles; see k_gemm) when eligible

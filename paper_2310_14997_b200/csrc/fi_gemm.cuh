@@ -71,7 +71,89 @@ struct GemmShape {
   // tail" GEMM is two launches over one shape: whole waves, then the tail
   // split over K)
   int tile_begin, tile_end;
+  // stream-K (sk > 0: the persistent slot count, ksplit 1): tiles
+  // [0, sk_first) run whole (sk_first is a multiple of sk, so every slot
+  // gets the same number), and the K iterations of the last tiles
+  // [sk_first, T) (at most sk of them) are cut into sk equal contiguous
+  // runs, one per slot.  A run spans at most two tiles; each of its
+  // segments that does not end its tile stores a raw partial at
+  // part + (slot + seg * sk) * tile_rows * bn and counts itself on
+  // sem[tile - sk_first]; the segment that ends the tile waits for its
+  // tile's other segments, adds their partials to its accumulator in slot
+  // order and runs the epilogue (and re-arms the counter).  A slot runs its
+  // non-final segment first, so no wait ever waits on a waiting CTA.
+  int sk, sk_first;
 };
+
+// Work unit i of persistent slot `slot`: tile, K range [k0, k1) (empty:
+// skip) and the partial-tile slot (-1: the epilogue writes the output).
+struct GemmUnit {
+  int tile, k0, k1, pidx;
+  int skt;  // stream-K: tile index within the stream-K tiles, else -1
+};
+__device__ __forceinline__ bool gemm_unit(const GemmShape& sh, int slot, int nslot, int i, int ks,
+                                          int k_iters, int tb, int tile_e, GemmUnit& x) {
+  x.skt = -1;
+  x.pidx = -1;
+  if (sh.sk > 0) {
+    const int ndp = sh.sk_first / nslot;  // whole tiles per slot
+    if (i < ndp) {
+      x.tile = slot + i * nslot;
+      x.k0 = 0;
+      x.k1 = k_iters;
+      return true;
+    }
+    const int j = i - ndp;
+    if (j >= 2) return false;
+    const long long W = static_cast<long long>(tile_e - sh.sk_first) * k_iters;
+    const long long st = W * slot / nslot, en = W * (slot + 1) / nslot;
+    const int ta = static_cast<int>(st / k_iters);
+    const bool two = en > static_cast<long long>(ta + 1) * k_iters;
+    // order: the segment in the next tile (never final unless it fills it) first
+    const int seg = two ? 1 - j : (j == 0 ? 0 : -1);
+    if (seg < 0 || en <= st) {
+      x.tile = tb;
+      x.k0 = x.k1 = 0;
+      return true;
+    }
+    const long long t0 = static_cast<long long>(ta + seg) * k_iters;
+    const long long a = seg == 0 ? st : t0;
+    const long long b = en < t0 + k_iters ? en : t0 + k_iters;
+    x.skt = ta + seg;
+    x.tile = sh.sk_first + x.skt;
+    x.k0 = static_cast<int>(a - t0);
+    x.k1 = static_cast<int>(b - t0);
+    x.pidx = slot + seg * nslot;
+    return true;
+  }
+  const int u = slot + i * nslot;
+  if (u >= (tile_e - tb) * ks) return false;
+  const int tu = u / ks, kp = u - tu * ks;
+  x.tile = tb + tu;
+  x.k0 = k_iters * kp / ks;
+  x.k1 = k_iters * (kp + 1) / ks;
+  x.pidx = ks > 1 ? kp * (tile_e - tb) + tu : -1;
+  return true;
+}
+
+// Stream-K: the partial slots of stream-K tile `skt`'s segments, in slot
+// order, except `own`; returns their count (<= 15).
+__device__ __forceinline__ int sk_parts(const GemmShape& sh, int skt, int nslot, int k_iters,
+                                        int tile_e, int own, int (&pid)[16]) {
+  const long long W = static_cast<long long>(tile_e - sh.sk_first) * k_iters;
+  const long long lo = static_cast<long long>(skt) * k_iters, hi = lo + k_iters;
+  long long s = lo * nslot / W;
+  s = s > 0 ? s - 1 : 0;
+  int n = 0;
+  for (; s < nslot && n < 16; ++s) {
+    const long long st = W * s / nslot, en = W * (s + 1) / nslot;
+    if (st >= hi) break;
+    if (en <= lo || en <= st) continue;
+    const int p = static_cast<int>(s) + (st >= lo ? 0 : 1) * nslot;
+    if (p != own) pid[n++] = p;
+  }
+  return n;
+}
 
 struct GemmEpi {
   int M;              // valid output rows
@@ -404,7 +486,6 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
   const int ks = sh.ksplit > 1 ? sh.ksplit : 1;
   const int tb = sh.tile_begin;
   const int tile_e = sh.tile_end > 0 ? sh.tile_end : num_tiles;
-  const int nunits = (tile_e - tb) * ks;
   const int bn = sh.bn;                       // runtime N tile <= BN
   const int bn_cta = bn / NCTA;               // B rows staged by this CTA
   const int nbuf = SPLIT || bn <= C::TMEM_HALF ? 2 : 1;  // accumulator buffers in TMEM
@@ -454,12 +535,12 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
       int stage = 0;
       uint32_t phase = 0;
       const uint32_t stage_tx = NCTA * (kAStage + sh.b_stage);
-      for (int u = tile0; u < nunits; u += tstep) {
-        const int tu = u / ks, kpart = u - tu * ks;
-        const int tile = tb + tu;
-        const int k0 = k_iters * kpart / ks, k1 = k_iters * (kpart + 1) / ks;
+      GemmUnit un;
+      for (int ui = 0; gemm_unit(sh, tile0, tstep, ui, ks, k_iters, tb, tile_e, un); ++ui) {
+        const int k0 = un.k0, k1 = un.k1;
+        if (k0 >= k1) continue;
         int m_blk, n_blk;
-        tile_mn(tile, m_blk, n_blk);
+        tile_mn(un.tile, m_blk, n_blk);
         const int m0 = m_blk * (C::BM * NCTA) + rank * C::BM;  // this CTA's A rows
         const int n0 = n_blk * bn + rank * bn_cta;              // this CTA's B rows
         for (int it = k0; it < k1; ++it) {
@@ -540,9 +621,10 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = tile0; u < nunits; u += tstep) {
-        const int kpart = u % ks;
-        const int k0 = k_iters * kpart / ks, k1 = k_iters * (kpart + 1) / ks;
+      GemmUnit un;
+      for (int ui = 0; gemm_unit(sh, tile0, tstep, ui, ks, k_iters, tb, tile_e, un); ++ui) {
+        const int k0 = un.k0, k1 = un.k1;
+        if (k0 >= k1) continue;
         const int cl = CHUNK > 0 ? CHUNK : k1 - k0;
         uint32_t d_tmem = tmem_base;
         int kc = 0;  // K iteration within the accumulator chunk (no per-iteration division)
@@ -641,12 +723,14 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
         else mbar_arrive(&tempty[a]);
       }
     };
-    for (int u = tile0; u < nunits; u += tstep) {
-      const int tu = u / ks, kpart = u - tu * ks;
-      const int tile = tb + tu;
-      const int k0 = k_iters * kpart / ks, k1 = k_iters * (kpart + 1) / ks;
+    GemmUnit un;
+    for (int ui = 0; gemm_unit(sh, tile0, tstep, ui, ks, k_iters, tb, tile_e, un); ++ui) {
+      const int k0 = un.k0, k1 = un.k1;
+      if (k0 >= k1) continue;
+      const int u = tile0 + ui * tstep;
+      const int tu = un.tile - tb, kpart = u - tu * ks;  // (in-kernel reduction only)
       int m_blk, n_blk;
-      tile_mn(tile, m_blk, n_blk);
+      tile_mn(un.tile, m_blk, n_blk);
       const int lrow = m_blk * (C::BM * NCTA) + rank * C::BM + r;  // row within this GEMM
       // (TR: rows are output columns; the row epilogue runs after the transpose)
       const EpiRow er = TR ? EpiRow{} : epi_row<EPI>(ep, lrow);
@@ -662,17 +746,88 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
         const int q = w >= hs ? 1 : 0;  // w < 2 hs: the CTA half, without a division
         return q * bn_cta + sb * 128 + (w - q * hs);
       };
-      auto emit = [&](int j, const float (&v)[32]) {
+      // stream-K: the segment that ends its tile sums the others' partials
+      const bool sk_final = un.skt >= 0 && un.k1 == k_iters;
+      int sk_pid[16];
+      const int sk_np = sk_final ? sk_parts(sh, un.skt, tstep, k_iters, tile_e, un.pidx, sk_pid) : 0;
+      const bool to_part = un.pidx >= 0 && !sk_final;
+      int* sk_cnt = un.skt >= 0 ? sh.sem + un.skt : nullptr;
+      constexpr int kEpiThreadsAll = 32 * gemm_epi_warps<CHUNK>();
+      constexpr int tile_rows_u = C::BM * NCTA;
+      if (sk_np > 0) {  // wait until every other segment of the tile has published
+        if (threadIdx.x == 128)
+          while (ld_acquire_gpu(sk_cnt) < sk_np * NCTA) __nanosleep(64);
+        epi_bar_sync(kEpiThreadsAll);
+      }
+      // the final segment is this CTA's last unit: once its accumulator is
+      // full the smem ring is idle and holds the other segments' sum
+      // (128 x bn, rows padded by 16 B), read with coalesced loads
+      const uint32_t sk_tile = smem_u32(smem);
+      constexpr int kSkDepth = 16;
+      auto sk_stage = [&]() {
+        // a partial row-block is contiguous (tile_rows_u x bn floats per part):
+        // kSkDepth float4 loads in flight per thread per part, then st.shared
+        const int n4 = C::BM * bn / 4;
+        const float4* base = reinterpret_cast<const float4*>(
+            sh.part + static_cast<long long>(rank * C::BM) * bn);
+        const long long pstr4 = static_cast<long long>(tile_rows_u) * bn / 4;
+        for (int i0 = threadIdx.x - 128; i0 < n4; i0 += kSkDepth * kEpiThreadsAll) {
+          float4 a[kSkDepth];
+#pragma unroll
+          for (int u = 0; u < kSkDepth; ++u) {
+            const int i = i0 + u * kEpiThreadsAll;
+            a[u] = i < n4 ? __ldcg(base + sk_pid[0] * pstr4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+          for (int pi = 1; pi < sk_np; ++pi) {  // slot order: deterministic
+            const float4* pp = base + sk_pid[pi] * pstr4;
+            float4 w[kSkDepth];
+#pragma unroll
+            for (int u = 0; u < kSkDepth; ++u) {
+              const int i = i0 + u * kEpiThreadsAll;
+              w[u] = i < n4 ? __ldcg(pp + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < kSkDepth; ++u) {
+              a[u].x += w[u].x;
+              a[u].y += w[u].y;
+              a[u].z += w[u].z;
+              a[u].w += w[u].w;
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kSkDepth; ++u) {
+            const int i = i0 + u * kEpiThreadsAll;
+            if (i < n4) {
+              const int row = i / (bn / 4), c4 = i - row * (bn / 4);
+              st_shared_v4(sk_tile + static_cast<uint32_t>((row * (bn + 4) + c4 * 4) * 4), a[u]);
+            }
+          }
+        }
+        epi_bar_sync(kEpiThreadsAll);
+      };
+      auto emit = [&](int j, const float (&v0)[32]) {
         const int tc = tile_col(j);
-        if (ks > 1) {  // split-K: raw fp32 partial, summed + transformed below / by k_gemm_fixup
-          constexpr int tile_rows = C::BM * NCTA;
-          const long long tsplit = tile_e - tb;
-          float4* dst = reinterpret_cast<float4*>(
-              sh.part + ((kpart * tsplit + tu) * tile_rows + rank * C::BM + r) * bn + tc);
+        if (to_part) {  // split-K / stream-K: raw fp32 partial, summed + transformed
+          float4* dst = reinterpret_cast<float4*>(    // below or by k_gemm_fixup
+              sh.part + (static_cast<long long>(un.pidx) * tile_rows_u + rank * C::BM + r) * bn + tc);
 #pragma unroll
           for (int q = 0; q < 8; ++q)
-            dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            dst[q] = make_float4(v0[4 * q], v0[4 * q + 1], v0[4 * q + 2], v0[4 * q + 3]);
           return;
+        }
+        float v[32];
+#pragma unroll
+        for (int t = 0; t < 32; ++t) v[t] = v0[t];
+        if (sk_np > 0) {  // + the other segments' sum, staged in the idle ring (below)
+          const uint32_t src = sk_tile + static_cast<uint32_t>((r * (bn + 4) + tc) * 4);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 w = ld_shared_v4(src + 16u * q);
+            v[4 * q] += w.x;
+            v[4 * q + 1] += w.y;
+            v[4 * q + 2] += w.z;
+            v[4 * q + 3] += w.w;
+          }
         }
         if constexpr (TR) {  // v = 32 output rows of output column lrow: transpose
           float* tw = tbuf + (warp - 4) * (32 * 33);
@@ -695,6 +850,7 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
       if constexpr (CHUNK == 0) {
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
+        if (sk_np > 0) sk_stage();
         const uint32_t t_row = t_lane + static_cast<uint32_t>(acc * kTmemHalf);
         const int nch = bn / 32;
         constexpr int kHalves = gemm_epi_warps<CHUNK>() / 4;
@@ -715,7 +871,16 @@ __global__ void __launch_bounds__(gemm_threads<CHUNK>(), 1)
           acc = 0;
           acc_phase ^= 1;
         }
-        if (ks > 1 && sh.sem) {
+        if (un.skt >= 0 && !sk_final) {  // publish this segment's partial rows
+          __threadfence();
+          epi_bar_sync(kEpiThreadsAll);
+          if (threadIdx.x == 128) atomicAdd(sk_cnt, 1);
+        } else if (sk_np > 0) {  // the last CTA of the finalizing pair re-arms the counter
+          epi_bar_sync(kEpiThreadsAll);
+          if (threadIdx.x == 128 && atomicAdd(sk_cnt, 1) == sk_np * NCTA + NCTA - 1)
+            atomicExch(sk_cnt, 0);
+        }
+        if (ks > 1 && sh.sem && sh.sk == 0) {
           constexpr int tile_rows = C::BM * NCTA;
           constexpr int kEpiThreads = 32 * gemm_epi_warps<CHUNK>();
           const long long tsplit = tile_e - tb;
@@ -824,12 +989,12 @@ __global__ void __launch_bounds__(256) k_gemm_fixup(const float* __restrict__ pa
   const int row_base = (tile % num_m) * tile_rows + r0;   // GEMM row of smem row 0
   const int col_base = (tile / num_m) * bn;
   const long long pstride = tsplit * tile_rows * static_cast<long long>(bn);
-  const float4* src = reinterpret_cast<const float4*>(
-      part + ((tile - tile_begin) * static_cast<long long>(tile_rows) + r0) * bn);
   // shared layout [row][chunk][36 floats]: 32 values + 4 pad, so the
   // epilogue threads' 16-B reads of consecutive chunks hit distinct banks
   const int chunks = bn / 32;
   const int n4 = kFixRows * bn / 4;
+  const float4* src = reinterpret_cast<const float4*>(
+      part + ((tile - tile_begin) * static_cast<long long>(tile_rows) + r0) * bn);
   for (int i = threadIdx.x; i < n4; i += blockDim.x) {
     float4 acc = __ldcg(src + i);
     for (int k = 1; k < ksplit; ++k) {

@@ -56,6 +56,7 @@ print(json.dumps(out))
     {"FI_GEMM_TRANS": "1", "FI_GEMM_KSPLIT": "3", "FI_GEMM_PAIR": "0"},
     {"FI_GEMM_TRANS": "1", "FI_GEMM_KSPLIT": "2", "FI_GEMM_PAIR": "1", "FI_GEMM_BN": "128"},
     {"FI_GEMM_TUNE": "0"},                        # the cost model's tile, never measured
+    {"FI_GEMM_STREAMK": "2", "FI_GEMM_TUNE": "0"},  # stream-K tails wherever they fit
     {"FI_GEMM_TUNE_SPAN_PCT": "1000", "FI_GEMM_TUNE_MAX": "40"},  # time (run) many more tiles
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_schedule_matches_oracle(env):
