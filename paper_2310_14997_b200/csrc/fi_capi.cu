@@ -521,7 +521,7 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
     ksplit = 1;
   }
   const long long tsplit = tail > 0 ? tail : tiles;
-  if (ksplit > 1 && CHUNK == 0 && g_kpart.ptr &&
+  if (ksplit > 1 && g_kpart.ptr &&
       static_cast<size_t>(ksplit) * tsplit * Cf::BM * NCTA * bn <= g_kpart.floats) {
     sh.ksplit = ksplit;
     sh.part = g_kpart.ptr;
@@ -532,7 +532,7 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
     // the other needs, so it is opt-in (measured: no faster than the fixup
     // kernel at config 3, 14.35-14.48 vs 14.41-14.64 ms).
     static const int inkernel = env_int("FI_GEMM_INKERNEL_RED", 0);
-    if (inkernel && !TR && g_kpart.sem && tsplit <= kKPartSems) sh.sem = g_kpart.sem;
+    if (inkernel && !TR && CHUNK == 0 && g_kpart.sem && tsplit <= kKPartSems) sh.sem = g_kpart.sem;
   } else {
     tail = 0;  // no split-K available: whole tiles only
   }
@@ -896,7 +896,8 @@ int run_gemm_s(const Operand& A, const Operand& B, int M, int N, int K, int a_ro
   }
   std::vector<GemmCand> cands;
   const bool tune = gemm_tune_on();
-  GemmChoice c = choose_gemm(M, N, k_iters, kBnSingle, kBnMax, step1, step2, kChunk == 0,
+  // (fp32 mode: split-K partials are the chunked round-to-nearest sums)
+  GemmChoice c = choose_gemm(M, N, k_iters, kBnSingle, kBnMax, step1, step2, true,
                              tune ? &cands : nullptr);
   if (c.bn == 0) return set_err(FI_ERR_ARG, "no GEMM tile for N=%d (FI_GEMM_BN?)", N);
   auto launch = [&](const GemmChoice& ch) -> int {
