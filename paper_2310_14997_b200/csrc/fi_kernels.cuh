@@ -382,7 +382,6 @@ __device__ __forceinline__ void ring_init(BulkRing& r, int consumer_warps) {
 
 template <typename T, typename CT, int V>
 __global__ void __launch_bounds__(288) k_split_fwd_bulk(SplitArgs a, int stages) {
-  pdl_wait();  // inputs of the previous kernel visible from here
   constexpr bool kHalf = sizeof(CT) == 2;
   extern __shared__ __align__(128) uint8_t dsm[];
   __shared__ float red[33];
@@ -441,6 +440,12 @@ __global__ void __launch_bounds__(288) k_split_fwd_bulk(SplitArgs a, int stages)
     terms[t].d = d;
     terms[t].c = exp2f(d - 2.f * kChartScale);
   }
+  // The term table above reads only X and the W bounds, written two or more
+  // launches back in the PDL chain (complete before the previous launch
+  // passed its own wait and released this one); the a / b rows of width
+  // w-1 come from the previous GEMM, so the wait sits here, before any
+  // chart read or write.
+  pdl_wait();
 
   if (i + w > len) {  // span outside the sentence: never feeds a valid span
     if (ci >= 0) {
@@ -628,12 +633,41 @@ __global__ void __launch_bounds__(288, 3) k_split_fwd_pers(SplitArgs a, int stag
     fence_mbar_init();
   }
   __syncthreads();
-  pdl_wait();     // a / b / X of earlier widths are visible from here
-  pdl_trigger();  // persistent: the next kernel may queue behind this one
   const float lnn = a.wsum[0] > 0.f ? log2f(a.wsum[0]) : 0.f;
   const float rnn = a.wsum[1] > 0.f ? log2f(a.wsum[1]) : 0.f;
   const float lnp = a.wsum[2] > 0.f ? log2f(a.wsum[2]) : 0.f;
   const float rnp = a.wsum[3] > 0.f ? log2f(a.wsum[3]) : 0.f;
+  // the producer's term table of row kk: fp64 shift sums xs of each split
+  // (ptab) and the row's fixed shift D (their bound); dead rows feed nothing
+  auto row_table = [&](int kk, bool& dead) -> double {
+    const int local = a.b0 * n_w + kk;
+    const int b = local / n_w, i = local % n_w;
+    dead = i + w > a.lengths[b];
+    double ub = -1.0e300;
+    if (!dead) {
+      for (int t = lane; t < nsplit; t += 32) {
+        const int m = t + 1;
+        const double xs = a.X[chart_row(m, b, i, a.B, a.lmax)] +
+                          a.X[chart_row(w - m, b, i + m, a.B, a.lmax)];
+        ptab[t] = xs;
+        ub = fmax(ub, xs + (m == 1 ? lnp : lnn) + (w - m == 1 ? rnp : rnn));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ub = fmax(ub, __shfl_xor_sync(0xffffffffu, ub, o));
+    __syncwarp();
+    return ub;
+  };
+  // The first row's table is built before the dependency wait: X and the
+  // W bounds come from launches at least two back in the PDL chain (the
+  // splits of narrower widths, the weight prep), which had completed before
+  // the previous launch passed its own wait and released this one; only the
+  // a / b rows of width w-1 (read through the ring) need the wait.
+  bool dead0 = true;
+  double D0 = 0.0;
+  if (warp == 0 && static_cast<int>(blockIdx.x) < nrows) D0 = row_table(blockIdx.x, dead0);
+  pdl_wait();     // a / b of width w-1 (the previous GEMM) are visible from here
+  pdl_trigger();  // persistent: the next kernel may queue behind this one
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -652,21 +686,8 @@ __global__ void __launch_bounds__(288, 3) k_split_fwd_pers(SplitArgs a, int stag
     for (int kk = blockIdx.x; kk < nrows; kk += gridDim.x) {
       const int local = a.b0 * n_w + kk;
       const int b = local / n_w, i = local % n_w;
-      const bool dead = i + w > a.lengths[b];
-      double ub = -1.0e300;
-      if (!dead) {
-        for (int t = lane; t < nsplit; t += 32) {
-          const int m = t + 1;
-          const double xs = a.X[chart_row(m, b, i, a.B, a.lmax)] +
-                            a.X[chart_row(w - m, b, i + m, a.B, a.lmax)];
-          ptab[t] = xs;
-          ub = fmax(ub, xs + (m == 1 ? lnp : lnn) + (w - m == 1 ? rnp : rnn));
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) ub = fmax(ub, __shfl_xor_sync(0xffffffffu, ub, o));
-      __syncwarp();
-      const double D = ub;
+      bool dead = dead0;
+      const double D = kk == static_cast<int>(blockIdx.x) ? D0 : row_table(kk, dead);
       if (dead) {
         if (lane == 0) {
           mbar_wait(&empty[rs], rph ^ 1);
@@ -904,7 +925,6 @@ struct GatherTerm {
 
 template <typename T, typename CT, int V>
 __global__ void __launch_bounds__(288) k_gather_bwd_bulk(GatherArgs a, int stages, int nprod) {
-  pdl_wait();  // inputs of the previous kernel visible from here
   constexpr bool kHalf = sizeof(CT) == 2;
   nprod = nprod < 1 ? 1 : (nprod > stages ? stages : (nprod > 32 ? 32 : nprod));
   extern __shared__ __align__(128) uint8_t dsm[];
@@ -926,6 +946,7 @@ __global__ void __launch_bounds__(288) k_gather_bwd_bulk(GatherArgs a, int stage
   T* G = reinterpret_cast<T*>(a.G) + row * (2LL * a.Np);
 
   if (i + m > len) {
+    pdl_wait();
     if (ci >= 0) {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
@@ -961,6 +982,10 @@ __global__ void __launch_bounds__(288) k_gather_bwd_bulk(GatherArgs a, int stage
     gterms[t].rp = rp;
     gterms[t].d = static_cast<float>(xm + a.X[rs] - a.X[rp]);
   }
+  // The term table reads only forward-pass data (X, the sanitized lengths);
+  // the parents' LQ rows come from the previous dgrad launches, so the
+  // dependency wait sits here, before the ring streams them.
+  pdl_wait();
   ring_init(ring, ncons >> 5);
 
   float gl[4 * V], gr[4 * V];
