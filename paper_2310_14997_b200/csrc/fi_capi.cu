@@ -1193,18 +1193,39 @@ int forward_impl(const Plan& p, const float* L, const float* R, const float* roo
       }));
       if (use_pers) return FI_OK;
     }
-    const int stages = dc.stages;
+    // one-shot kernel (the widest spans: few rows, many terms each): with
+    // fewer rows than half the SMs, cut each row into more column chunks (a
+    // cluster per row, <= 8 CTAs) toward ~3 CTAs per SM, the ring deepened
+    // to keep ~24 KB per CTA in flight.  (With more rows it measured slower:
+    // widths 35-36 at |N| = 4096, B = 64 went 47 -> 57 us at 2 CTAs per row.)
+    Decomp dcl = dc;
+    static const int wide = env_int("FI_SPLIT_WIDE", 1);
+    const long long nrows_w = static_cast<long long>(nb) * n_w;
+    if (wide && !getenv("FI_CLUSTER") && 2 * nrows_w < num_sms()) {
+      const long long want = (3LL * num_sms() + nrows_w - 1) / nrows_w;
+      for (int c = static_cast<int>(want < 8 ? want : 8); c > dc.clusters; --c) {
+        Decomp t;
+        if (decomp_for(p.Np, c, &t)) {
+          t.stages = static_cast<int>(24576 / (2 * t.cols_per_cta * sizeof(CT)));
+          t.stages = t.stages < dc.stages ? dc.stages : (t.stages > 16 ? 16 : t.stages);
+          dcl = t;
+          break;
+        }
+      }
+    }
+    sa.cols_per_cta = dcl.cols_per_cta;
+    const int stages = dcl.stages;
     const size_t smem = align128(sizeof(SplitTerm) * (w - 1)) +
-                        static_cast<size_t>(stages) * (2 * dc.cols_per_cta * sizeof(CT) + 16);
-    const dim3 grid(dc.clusters, nb * n_w);
-    const dim3 block(32 + dc.threads);
-    return dispatch_v(dc.v, [&](auto vc) {
+                        static_cast<size_t>(stages) * (2 * dcl.cols_per_cta * sizeof(CT) + 16);
+    const dim3 grid(dcl.clusters, nb * n_w);
+    const dim3 block(32 + dcl.threads);
+    return dispatch_v(dcl.v, [&](auto vc) {
       constexpr int V = decltype(vc)::value;
       if constexpr (V > 4) {
         return set_err(FI_ERR_UNSUPPORTED, "split decomposition V=%d", V);
       } else {
         FI_TRY(set_smem(k_split_fwd_bulk<T, CT, V>, smem));
-        return launch_cluster(k_split_fwd_bulk<T, CT, V>, dc.clusters, grid, block, smem, s, sa,
+        return launch_cluster(k_split_fwd_bulk<T, CT, V>, dcl.clusters, grid, block, smem, s, sa,
                               stages);
       }
     });
