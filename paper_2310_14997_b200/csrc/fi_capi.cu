@@ -804,7 +804,10 @@ int tuned_choice(const TuneKey& key, GemmChoice model, std::vector<GemmCand> can
     }
   }
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  FI_CUDA(cudaStreamIsCapturing(st, &cs));
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {  // e.g. the legacy stream while another
+    cudaGetLastError();                                  // stream captures: do not time
+    return FI_OK;
+  }
   if (cs != cudaStreamCaptureStatusNone) return FI_OK;  // never time inside a capture
   // distinct candidates, cheapest first; the model's pick leads
   std::stable_sort(cands.begin(), cands.end(),
