@@ -630,6 +630,7 @@ struct GemmChoice {
   int ksplit;
   int tail;  // > 0: whole waves, then the last `tail` tiles split ksplit ways over K
   bool sk = false;  // the `tail` tiles are run stream-K over every slot (ksplit 1)
+  bool tr = false;  // transposed output (weight table on the MMA's M side; see k_gemm TR)
 };
 
 double gemm_t_single(int bn) { return 0.77 + 0.23 * bn / 256.0; }
@@ -762,7 +763,7 @@ GemmChoice choose_gemm(long long M, int N, int k_iters, int bn_max, int bn_max_p
 // harmless.  A forced tile (FI_GEMM_PAIR / BN / KSPLIT) disables tuning.
 bool same_choice(const GemmChoice& a, const GemmChoice& b) {
   return a.bn == b.bn && a.pair == b.pair && a.ksplit == b.ksplit && a.tail == b.tail &&
-         a.sk == b.sk;
+         a.sk == b.sk && a.tr == b.tr;
 }
 
 struct TuneKey {
@@ -841,7 +842,8 @@ int tuned_choice(const TuneKey& key, GemmChoice model, std::vector<GemmCand> can
       if (log_tune >= 2)
         fprintf(stderr, "[fi tune] sig=%d M=%lld N=%d K=%d  bn=%d pair=%d ks=%d tail=%d%s: %.1f us\n",
                 key.sig, key.M, key.N, key.K, list[i].bn, static_cast<int>(list[i].pair),
-                list[i].ksplit, list[i].tail, list[i].sk ? " sk" : "", ms * 1e3f / 3.f);
+                list[i].ksplit, list[i].tail, list[i].sk ? " sk" : list[i].tr ? " tr" : "",
+                ms * 1e3f / 3.f);
       // an alternative has to beat the model's pick by 2% to replace it
       if (ms < best_ms * (i == 0 ? 1.f : 0.98f)) {
         best_ms = ms;
@@ -880,11 +882,13 @@ int run_gemm_s(const Operand& A, const Operand& B, int M, int N, int K, int a_ro
   const int step2 = BMN ? 2 * ATOM : 32;
   static const int log_choice = env_int("FI_GEMM_LOG", 0);
   // Transposed output (TR, see k_gemm): the weight table on the MMA's M side
-  // and the chart rows as the N tile.  FI_GEMM_TRANS=1 forces it where it
-  // applies (bf16 operands, K-major chart rows, not the weight gradients).
-  static const int use_tr = env_int("FI_GEMM_TRANS", 0);
-  if constexpr (!AMN && !SPLIT && kChunk == 0 && sizeof(T) == 2 && EPI != EPI_WGRAD) {
-    if (use_tr) {
+  // and the chart rows as the N tile, where it applies (bf16 operands,
+  // K-major chart rows, not the weight gradients).  FI_GEMM_TRANS=1 forces
+  // it, 0 never uses it; by default its tiles are tuner candidates.
+  static const int use_tr = env_int("FI_GEMM_TRANS", -1);
+  constexpr bool kTrOk = !AMN && !SPLIT && kChunk == 0 && sizeof(T) == 2 && EPI != EPI_WGRAD;
+  if constexpr (kTrOk) {
+    if (use_tr == 1) {
       const GemmChoice t = choose_gemm(N, M, k_iters, kBnSingle, kBnSingle, 32, 32, true);
       if (log_choice)
         fprintf(stderr, "[fi gemm] EPI=%d M=%d N=%d K=%d -> TR bn=%d pair=%d ksplit=%d tail=%d\n",
@@ -903,7 +907,27 @@ int run_gemm_s(const Operand& A, const Operand& B, int M, int N, int K, int a_ro
   GemmChoice c = choose_gemm(M, N, k_iters, kBnSingle, kBnMax, step1, step2, true,
                              tune ? &cands : nullptr);
   if (c.bn == 0) return set_err(FI_ERR_ARG, "no GEMM tile for N=%d (FI_GEMM_BN?)", N);
+  if constexpr (kTrOk) {
+    if (tune && use_tr < 0) {  // the transposed tiles compete in the measured choice
+      std::vector<GemmCand> tc;
+      choose_gemm(N, M, k_iters, kBnSingle, kBnSingle, 32, 32, true, &tc);
+      for (GemmCand& x : tc) {
+        if (x.c.sk) continue;
+        x.c.tr = true;
+        cands.push_back(x);
+      }
+    }
+  }
   auto launch = [&](const GemmChoice& ch) -> int {
+    if constexpr (kTrOk) {
+      if (ch.tr) {
+        if (ch.pair)
+          return launch_gemm<T, kBnSingle, BMN, false, EPI, SPLIT, kChunk, true, false, true>(
+              B, A, N, M, K, a_row0, ep, st, ch.bn, ch.ksplit, ch.tail);
+        return launch_gemm<T, kBnSingle, BMN, false, EPI, SPLIT, kChunk, false, false, true>(
+            B, A, N, M, K, a_row0, ep, st, ch.bn, ch.ksplit, ch.tail);
+      }
+    }
     if (ch.pair) {
       if (ch.bn > kBnSingle)  // 256 x 512-class pair tiles: two MMAs per K step
         return launch_gemm<T, kBnMax, AMN, BMN, EPI, SPLIT, kChunk, true>(
@@ -922,15 +946,15 @@ int run_gemm_s(const Operand& A, const Operand& B, int M, int N, int K, int a_ro
     FI_TRY(tuned_choice(TuneKey{dev, sig, M, N, K}, model, std::move(cands), st, launch, &c));
   }
   if (log_choice)
-    fprintf(stderr, "[fi gemm] EPI=%d M=%d N=%d K=%d -> bn=%d pair=%d ksplit=%d tail=%d%s%s\n",
+    fprintf(stderr, "[fi gemm] EPI=%d M=%d N=%d K=%d -> bn=%d pair=%d ksplit=%d tail=%d%s%s%s\n",
             EPI, M, N, K, c.bn, static_cast<int>(c.pair), c.ksplit, c.tail,
-            c.sk ? " stream-K" : "",
+            c.sk ? " stream-K" : "", c.tr ? " transposed" : "",
             same_choice(c, model) ? "" : " (measured; model picked another)");
   // FI_GEMM_MC=1: pair tiles of N <= 256 run as multicast clusters of two
   // pairs (A rows shared, adjacent N tiles; see k_gemm) when eligible
   static const int use_mc = env_int("FI_GEMM_MC", 0);
   if constexpr (!AMN && !SPLIT && kChunk == 0) {
-    if (use_mc && c.pair && c.bn <= kBnSingle && c.ksplit == 1 && c.tail == 0)
+    if (use_mc && !c.tr && c.pair && c.bn <= kBnSingle && c.ksplit == 1 && c.tail == 0)
       return launch_gemm<T, kBnSingle, AMN, BMN, EPI, SPLIT, kChunk, true, true>(
           A, B, M, N, K, a_row0, ep, st, c.bn, 1, 0);
   }
