@@ -813,13 +813,19 @@ int tuned_choice(const TuneKey& key, GemmChoice model, std::vector<GemmCand> can
   // distinct candidates, cheapest first; the model's pick leads
   std::stable_sort(cands.begin(), cands.end(),
                    [](const GemmCand& a, const GemmCand& b) { return a.cost < b.cost; });
+  // distinct candidates, at most two per tile shape (bn, pair, transposed):
+  // the split-K variants of one shape differ little, other shapes may win
   std::vector<GemmChoice> list{model};
   const double limit = (cands.empty() ? 0.0 : cands.front().cost) * kTuneSpan;
   for (const GemmCand& g : cands) {
     if (static_cast<int>(list.size()) >= kTuneMax || g.cost > limit) break;
     bool dup = false;
-    for (const GemmChoice& c : list) dup = dup || same_choice(c, g.c);
-    if (!dup) list.push_back(g.c);
+    int same_shape = 0;
+    for (const GemmChoice& c : list) {
+      dup = dup || same_choice(c, g.c);
+      same_shape += c.bn == g.c.bn && c.pair == g.c.pair && c.tr == g.c.tr;
+    }
+    if (!dup && same_shape < 2) list.push_back(g.c);
   }
   GemmChoice best = model;
   if (list.size() > 1) {
