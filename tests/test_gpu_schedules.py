@@ -43,6 +43,7 @@ print(json.dumps(out))
     {"FI_GEMM_KSPLIT": "4"},                      # split-K through the fixup kernel
     {"FI_SPLIT_PERS": "0"},                       # one-shot split kernel at every width
     {"FI_SPLIT_PERS": "2"},                       # persistent split kernel at every width
+    {"FI_SPLIT_WIDE": "0"},                       # widest spans with the plan's column split
     {"FI_PDL": "0"},
     {"FI_GATHER_PERS": "0"},                      # one-shot gather at every width
     {"FI_GATHER_PERS": "2"},                      # persistent gather at every width
