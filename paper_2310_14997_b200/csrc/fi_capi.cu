@@ -504,7 +504,7 @@ int launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, int a_r
   sh.sk_first = 0;
 
   // persistent: one CTA (pair, cluster) per SM (pair, group of 4 SMs)
-  const int nslots = MC ? 0 : num_sms() / NCTA;
+  const int nslots = num_sms() / NCTA;
   if (streamk && !MC && !TR && CHUNK == 0 && g_kpart.ptr && g_kpart.sem && tail > 0 &&
       tail == tiles % nslots && tail <= kKPartSems &&
       sh.stages * stage_bytes >= Cf::BM * (bn + 4) * 4 &&  // the finalizer's staging tile
