@@ -1133,8 +1133,9 @@ int forward_impl(const Plan& p, const float* L, const float* R, const float* roo
   }
   {
   ProfScope prof(FI_PROF_PREP, st);
+  const int vec1 = p.P % 4 == 0 && (reinterpret_cast<uintptr_t>(unary) & 15) == 0;
   FI_TRY(launch_ex(k_prep_width1<T>, 1, dim3(p.B * p.l), dim3(256), 0, st, unary, lengths, e1, X,
-                   p.l, p.P, p.Pp, p.e1_lo));
+                   p.l, p.P, p.Pp, p.e1_lo, vec1));
   FI_CUDA(cudaGetLastError());
   }
 

@@ -238,19 +238,41 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_prep_width1(const float* __restrict__ unary,
                                                      const int* __restrict__ lengths,
                                                      T* __restrict__ e1, double* __restrict__ X,
-                                                     int lmax, int P, int Pp, long long e1_lo) {
+                                                     int lmax, int P, int Pp, long long e1_lo,
+                                                     int vec) {
   pdl_wait();
   __shared__ float red[33];
   const int r = blockIdx.x;  // = b * lmax + i = chart_row(1, b, i)
   const int b = r / lmax, i = r % lmax;
   const bool ok = i < lengths[b];
   const float* u = unary + static_cast<long long>(r) * P;
+  T* dst = e1 + static_cast<long long>(r) * Pp;
   float mx = kNegInf;
+  if (vec) {  // P a multiple of 4, 16-B rows: float4 loads, 4-wide stores
+    const float4* u4 = reinterpret_cast<const float4*>(u);
+    if (ok)
+      for (int t = threadIdx.x; t < P / 4; t += blockDim.x) {
+        const float4 x = __ldg(u4 + t);
+        mx = fmaxf(mx, fmaxf(fmaxf(x.x * kLog2e, x.y * kLog2e), fmaxf(x.z * kLog2e, x.w * kLog2e)));
+      }
+    mx = block_reduce<true>(mx, red);
+    const float xs = (mx == kNegInf) ? 0.f : mx;
+    for (int t = threadIdx.x; t < Pp / 4; t += blockDim.x) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (ok && 4 * t < P) {
+        const float4 x = __ldg(u4 + t);
+        v = make_float4(ex2(fmaf(x.x, kLog2e, -xs)), ex2(fmaf(x.y, kLog2e, -xs)),
+                        ex2(fmaf(x.z, kLog2e, -xs)), ex2(fmaf(x.w, kLog2e, -xs)));
+      }
+      store4s<T>(dst + 4 * t, e1_lo, v.x, v.y, v.z, v.w);
+    }
+    if (threadIdx.x == 0) X[r] = xs;
+    return;
+  }
   if (ok)
     for (int t = threadIdx.x; t < P; t += blockDim.x) mx = fmaxf(mx, u[t] * kLog2e);
   mx = block_reduce<true>(mx, red);
   const float xs = (mx == kNegInf) ? 0.f : mx;
-  T* dst = e1 + static_cast<long long>(r) * Pp;
   for (int t = threadIdx.x; t < Pp; t += blockDim.x)
     store1s<T>(dst + t, e1_lo, (ok && t < P) ? ex2(fmaf(u[t], kLog2e, -xs)) : 0.f);
   if (threadIdx.x == 0) X[r] = xs;
