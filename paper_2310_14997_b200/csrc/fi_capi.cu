@@ -1326,7 +1326,7 @@ int backward_impl(const Plan& p, const float* L, const float* R, const float* ro
   {
   ProfScope prof(FI_PROF_SEED, st);
   (void)logZ;  // the fp64-consistent log2 Z - x† (TOPZ) is used instead
-  FI_TRY(launch_ex(k_seed_bwd<sizeof(CT) == 2>, 1, dim3((p.Np + 255) / 256), dim3(256), 0, st,
+  FI_TRY(launch_ex(k_seed_bwd<sizeof(CT) == 2>, 1, dim3((p.Np + 255) / 256, p.B), dim3(256), 0, st,
                    root, static_cast<const float*>(TOP), static_cast<const float*>(TOPZ), g,
                    lengths, static_cast<void*>(LQ), LQS, droot, flag, p.B, p.l, p.N, p.Np));
   FI_CUDA(cudaGetLastError());

@@ -878,22 +878,33 @@ __global__ void k_seed_bwd(const float* __restrict__ root, const float* __restri
                            float* __restrict__ LQS, float* __restrict__ droot,
                            int* __restrict__ flag, int B, int lmax, int N, int Np) {
   pdl_wait();
-  // blockDim is a multiple of 32 and Np of 256: each warp owns one 32-column chunk
+  // grid (Np / blockDim, B): block (x, b) seeds sentence b's top span for
+  // one column range; the blocks of b = 0 also sum d_root over all
+  // sentences (in sentence order: deterministic).  blockDim is a multiple
+  // of 32 and Np of 256: each warp owns one 32-column chunk.
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= Np) return;
-  float acc = 0.f;
-  for (int b = 0; b < B; ++b) {
+  if (blockIdx.y == 0 && c < N) {
+    float acc = 0.f;
+#pragma unroll 4
+    for (int b = 0; b < B; ++b) {
+      const float z = TOPZ[b];
+      const float gb = g[b];
+      if (lengths[b] >= 2 && isfinite(z) && gb != 0.f)
+        acc += gb * exp2f(TOP[static_cast<long long>(b) * Np + c] - z);
+    }
+    droot[c] = acc;
+  }
+  {
+    const int b = blockIdx.y;
     const float z = TOPZ[b];
     const float gb = g[b];
     const int len = lengths[b];  // sanitized: 0 marks an invalid sentence (k_check_lengths)
-    if (len < 2) continue;
+    if (len < 2) return;
     const bool finite = isfinite(z);
     if (!finite && c == 0) atomicOr(flag, FI_FLAG_ZERO_PROB);
     float lq = kNegInf;
-    if (finite && gb != 0.f && c < N) {
-      lq = fmaf(root[c], kLog2e, -z) + log2f(fabsf(gb));
-      acc += gb * exp2f(TOP[static_cast<long long>(b) * Np + c] - z);
-    }
+    if (finite && gb != 0.f && c < N) lq = fmaf(root[c], kLog2e, -z) + log2f(fabsf(gb));
     const long long row = chart_row(len, b, 0, B, lmax);
     if constexpr (kHalfLQ) {  // fp16 outside weight with a per-chunk exponent
       float mx = lq;
@@ -907,7 +918,6 @@ __global__ void k_seed_bwd(const float* __restrict__ root, const float* __restri
       static_cast<float*>(LQv)[row * Np + c] = lq;
     }
   }
-  if (c < N) droot[c] = acc;
 }
 
 // ---------------------------------------------------------------------------
